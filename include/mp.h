@@ -1,0 +1,187 @@
+/*
+ * mp.h — C-ABI of the B200-native MultiScope proxy-guided window path.
+ *
+ * The library (paper_2103_14695_b200/libmp_b200.so, sm_100a) exposes the three
+ * per-frame data-parallel calls of MultiScope's segmentation-proxy inference
+ * (Bastani & Madden, arXiv 2103.14695, §3.3 "Inference" /
+ * "Grouping Cells during Execution", lines 176-186), plus the two steps this
+ * build adds around the detector (crop/resize in, remap/NMS out; SURVEY.md
+ * §8(a) a5-a7, readings R15-R20 in DESIGN.md §3).
+ *
+ * Conventions common to every call
+ *  - Ownership: the caller allocates and owns every buffer (the Python binding
+ *    uses torch tensors).  The library never allocates, frees or retains device
+ *    memory between calls.  Scratch memory comes in as (d_ws, ws_bytes) sized
+ *    by the matching *_workspace_size() query.
+ *  - "d_" pointers are DEVICE pointers; every other pointer is a HOST pointer
+ *    read synchronously before the call returns.
+ *  - Asynchrony: all device work is enqueued on stream `s` (a cudaStream_t,
+ *    passed as void* so this header needs no CUDA include; NULL = legacy
+ *    default stream).  The call returns without synchronising.  Device inputs
+ *    must stay alive until the stream passes the call.  No call allocates or
+ *    synchronises, so every call is CUDA-graph capturable.
+ *  - Errors: invalid host parameters return MP_ERR_INVALID (or
+ *    MP_ERR_UNSUPPORTED for valid-but-unsupported sizes) before anything is
+ *    launched.  A failed launch returns MP_ERR_CUDA.  Data-dependent overflow
+ *    (more windows / boxes than the caller's capacity) cannot be known on the
+ *    host: the kernels store MP_ERR_CAPACITY into the device word *d_status
+ *    (never clearing it; the caller zeroes it), still write all counts and
+ *    offsets so the caller can grow buffers and retry, and skip writes that
+ *    would fall outside the buffers.
+ *  - Determinism: outputs are a pure function of the inputs, independent of
+ *    launch configuration, stream, or how frames are sharded across GPUs.
+ *    The library is re-entrant and keeps no global mutable state.
+ */
+#ifndef MP_H_
+#define MP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MP_OK = 0,
+  MP_ERR_INVALID = 1,     /* bad host parameters (checked before any launch) */
+  MP_ERR_CUDA = 2,        /* a CUDA launch / attribute call failed            */
+  MP_ERR_CAPACITY = 3,    /* device-side: an output buffer was too small      */
+  MP_ERR_UNSUPPORTED = 4  /* valid but beyond this build's limits             */
+} mp_status;
+
+/* A window size (w_i, h_i) in S, in frame pixels.  PAPER.md:182 "a fixed set
+ * of window sizes ... S = {(w_1,h_1),...,(w_k,h_k)}". */
+typedef struct { int32_t w, h; } mp_size;
+
+/* One rectangle r_i = (r.x, r.y, r.w, r.h) of R_t, plus the
+ * frame it belongs to, the index of its size in S, and `slot` = its index in
+ * the batched detector input of that size class (rank among the windows of
+ * that size in (frame, list) order).  28 bytes, frame pixels. */
+typedef struct { int32_t frame, x, y, w, h, size_idx, slot; } mp_window;
+
+/* A detection box, corner form, 24 bytes.  Detector output (input of
+ * mp_remap_nms) is in the window's detector-input pixels [0,ow]x[0,oh];
+ * output of mp_remap_nms is in frame pixels.  Reading R17. */
+typedef struct { float x1, y1, x2, y2, score; int32_t cls; } mp_box;
+
+typedef enum {
+  MP_OUT_F32_NCHW = 0,  /* class k tensor: float [cap_k][3][oh_k][ow_k], 0..255 scale, RGB */
+  MP_OUT_U8_NHWC = 1    /* class k tensor: uint8 [cap_k][oh_k][ow_k][3], round-half-up      */
+} mp_out_format;
+
+/* Planner parameters.  PAPER.md:178 (B_proxy), :182 (S, T_{w,h}), :193 (the
+ * full frame (W,H) is always in S). */
+typedef struct {
+  int32_t W, H;            /* frame size, px, 1..16384                                   */
+  int32_t cell_w, cell_h;  /* cell size in frame px (paper: 32x32);
+                              grid = ceil(H/cell_h) rows x ceil(W/cell_w) cols; the last
+                              row/col is clipped to the frame (reading R1)                 */
+  float b_proxy;           /* a cell is positive iff score > b_proxy (strict, R2)         */
+  int32_t k;               /* |S|, 1..16                                                  */
+  const mp_size* sizes;    /* host [k]: distinct, 1<=w<=W, 1<=h<=H, MUST contain (W,H)    */
+  const int64_t* cost;     /* host [k]: T_{w,h} > 0 and area_i < area_j => T_i < T_j
+                              (R13; pairs of equal area are unconstrained)                */
+} mp_plan_params;
+
+/* Bytes of scratch mp_plan_windows needs for F frames (0 on invalid params). */
+size_t mp_plan_workspace_size(const mp_plan_params* p, int32_t F);
+
+/*
+ * mp_plan_windows — steps a1-a4: threshold the per-cell proxy scores
+ * (PAPER.md:178), form one cluster per 4-connected component of positive cells
+ * ("We initialize a cluster C_i for each connected component"),
+ * run the greedy agglomerative merge of PAPER.md:184 under the costs T
+ * (R4-R9, R11-R13), and emit one window per final cluster, centred on the
+ * cluster's bounding box and clamped into the frame (R10).
+ *
+ *  d_scores      device float [F][R][C] row-major, R = ceil(H/cell_h), C = ceil(W/cell_w).
+ *  d_mask        device uint32 [F][R][ceil(C/32)] or NULL: bit (c%32) of word c/32
+ *                of row r is cell (r,c)'s positive flag; padding bits are 0.
+ *  d_windows     device mp_window [max_windows]: all windows of all frames,
+ *                frame ascending, then final cluster-list order.
+ *  d_frame_off   device int32 [F+1]: CSR, windows of frame f are
+ *                [d_frame_off[f], d_frame_off[f+1]); d_frame_off[F] = total
+ *                (the true total even on overflow).
+ *  d_class_count device int32 [k]: number of windows of each size (true counts).
+ *  d_status      device int32: set to MP_ERR_CAPACITY if total > max_windows.
+ *  Limits: grid R*C <= 16384 cells (else MP_ERR_UNSUPPORTED).
+ */
+mp_status mp_plan_windows(const mp_plan_params* p, const float* d_scores, int32_t F,
+                          uint32_t* d_mask, mp_window* d_windows, int32_t max_windows,
+                          int32_t* d_frame_off, int32_t* d_class_count, int32_t* d_status,
+                          void* d_ws, size_t ws_bytes, void* stream);
+
+/* Bytes of scratch mp_gather_resize needs (0 on invalid params). */
+size_t mp_gather_workspace_size(int32_t k, const int32_t* out_cap);
+
+/*
+ * mp_gather_resize — step a5: gather every window's crop from its full
+ * resolution frame and bilinearly resample it to its size class's detector
+ * input dims, writing one batched tensor per size class (PAPER.md:152
+ * "initializes the detector on the GPU to execute at each of those sizes";
+ * resampling convention R15/R16: half-pixel centres, taps clamped to the crop,
+ * exact integer tap positions, fp32 arithmetic).
+ *
+ *  d_frame_ptrs  device array [F] of device pointers; frame f is uint8
+ *                [H][pitch] with RGB24 pixels, 16-byte aligned.
+ *  pitch         bytes per frame row, multiple of 16, >= 3*W.
+ *  d_windows     device mp_window[n_win], n_win = d_frame_off[F] (read on
+ *                device); each window must lie inside the frame, have
+ *                (w,h) == sizes[size_idx], and slots of a class must be
+ *                0..count-1 (as mp_plan_windows produces; violations set
+ *                *d_status = MP_ERR_INVALID and skip the window).
+ *  sizes         host [k] window sizes; out_dims host [k] (ow_k, oh_k) >= 1.
+ *  d_out         host [k] of device pointers to class tensors (see
+ *                mp_out_format), 16-byte aligned, batch capacity out_cap[k].
+ *  A class with more than out_cap[k] windows sets MP_ERR_CAPACITY and the
+ *  extra slots are skipped.
+ */
+mp_status mp_gather_resize(const uint8_t* const* d_frame_ptrs, int32_t pitch, int32_t W,
+                           int32_t H, int32_t F, const mp_window* d_windows,
+                           const int32_t* d_frame_off, int32_t k, const mp_size* sizes,
+                           const mp_size* out_dims, void* const* d_out, const int32_t* out_cap,
+                           mp_out_format fmt, int32_t* d_status, void* d_ws, size_t ws_bytes,
+                           void* stream);
+
+/* Bytes of scratch mp_remap_nms needs for F frames and max_boxes raw boxes. */
+size_t mp_remap_nms_workspace_size(int32_t F, int32_t max_boxes);
+
+/*
+ * mp_remap_nms — steps a6-a7 (not in the paper; readings R17-R20): for every
+ * raw detector box of every window, drop it unless score > score_thr, clip it
+ * to the detector-input extent [0,ow]x[0,oh], drop it if degenerate, map it to
+ * frame pixels with one fp64 rounding sequence X = fp32(x_l*w/ow + x); then
+ * per frame run class-aware greedy NMS in (score desc, candidate index asc)
+ * order, suppressing a later same-class box iff its fp32 IoU > iou_thr.
+ *
+ *  d_boxes        device mp_box[n_box]; n_box = d_win_box_off[n_win] <= max_boxes.
+ *  d_win_box_off  device int32 [n_win+1]: boxes of window i are
+ *                 [d_win_box_off[i], d_win_box_off[i+1]) (window order).
+ *  d_windows, d_frame_off  as produced by mp_plan_windows (n_win = d_frame_off[F]).
+ *  out_dims       host [k] detector-input dims per size class.
+ *  d_out, d_out_src  device [max_out]: kept boxes (frame px) and the index of
+ *                 the input box each came from; frame-major, keep order.
+ *  d_out_frame_off device int32 [F+1]: CSR of kept boxes (true totals).
+ *  Limits: at most 4096 raw boxes per frame (else *d_status = MP_ERR_CAPACITY
+ *  and that frame keeps nothing).
+ */
+mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_box_off,
+                       const mp_window* d_windows, const int32_t* d_frame_off, int32_t F,
+                       int32_t k, const mp_size* out_dims, int32_t W, int32_t H,
+                       float score_thr, float iou_thr, mp_box* d_out, int32_t* d_out_src,
+                       int32_t max_out, int32_t* d_out_frame_off, int32_t* d_status,
+                       int32_t max_boxes, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Human-readable name of a status code (static string, never NULL). */
+const char* mp_status_string(mp_status st);
+
+/* Number of device kernels the last-built library launches per call
+ * (diagnostic, used by bench.py to count launches): which = 0 plan,
+ * 1 gather, 2 remap_nms. */
+int32_t mp_launches_per_call(int32_t which);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MP_H_ */

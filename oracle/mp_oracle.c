@@ -1,0 +1,567 @@
+/*
+ * mp_oracle.c — CPU ORACLE for the MultiScope proxy-guided window path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_2103_14695_b200/) never links, imports or calls it,
+ * and shares no code, header, table or helper with it.
+ *
+ * It is a plain, slow, obviously-correct C99 implementation of what the path
+ * computes, written from the paper (PAPER.md = arXiv 2103.14695 LaTeX source)
+ * and from the readings recorded in DESIGN.md §3 where the paper is silent.
+ * Floating point: fp64 wherever the paper does not fix a precision, except
+ * where an integer or ordering decision must be taken in the same precision as
+ * the CUDA path (the threshold compare in fp32, NMS IoU in fp32, remap's final
+ * fp32 rounding) — each such place says so.  Build with -O2 -ffp-contract=off.
+ *
+ * Pins (what ties this oracle to something other than itself) are listed in
+ * tests/test_oracle_*.py and DESIGN.md §4.  Every function here is pinned;
+ * there is no "parity unpinned" function.
+ *
+ * Citations: "P:n" = PAPER.md line n; "Rn" = reading n in DESIGN.md §3.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* Own types (the oracle includes no product header).  Layouts are plain
+ * int32/float records: window = 7 x int32, box = 5 x float + int32. */
+typedef struct { int32_t w, h; } mpo_size;
+typedef struct { int32_t frame, x, y, w, h, size_idx, slot; } mpo_window;
+typedef struct { float x1, y1, x2, y2, score; int32_t cls; } mpo_box;
+
+enum { MPO_OK = 0, MPO_ERR_INVALID = 1, MPO_ERR_CAPACITY = 3 };
+enum { MPO_F32_NCHW = 0, MPO_U8_NHWC = 1, MPO_F64_NCHW = 2 };
+
+/* ------------------------------------------------------------------------ */
+/* a1. Threshold — P:150 "where the score exceeds a threshold parameter
+ * B_proxy", "a binary grid consisting of a (possibly empty) set of
+ * positive cells where the output scores exceeded B_proxy".  Reading R2:
+ * strict ">", compared in fp32 (the scores' own precision); NaN is never
+ * positive.  pos[r*C+c] = 1/0.  Returns the number of positive cells. */
+int64_t mpo_threshold(const float* scores, int32_t R, int32_t C, float b_proxy, uint8_t* pos) {
+  int64_t n = 0;
+  for (int32_t r = 0; r < R; r++)
+    for (int32_t c = 0; c < C; c++) {
+      float s = scores[(int64_t)r * C + c];
+      pos[(int64_t)r * C + c] = (s > b_proxy) ? 1 : 0;
+      n += pos[(int64_t)r * C + c];
+    }
+  return n;
+}
+
+/* Bit-pack a positive grid: bit (c%32) of word c/32 of row r.  (ABI layout of
+ * d_mask, include/mp.h.) */
+void mpo_pack_mask(const uint8_t* pos, int32_t R, int32_t C, uint32_t* mask) {
+  int32_t words = (C + 31) / 32;
+  for (int32_t r = 0; r < R; r++)
+    for (int32_t wd = 0; wd < words; wd++) {
+      uint32_t m = 0;
+      for (int32_t bit = 0; bit < 32; bit++) {
+        int32_t c = wd * 32 + bit;
+        if (c < C && pos[(int64_t)r * C + c]) m |= (1u << bit);
+      }
+      mask[(int64_t)r * words + wd] = m;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* a2. Connected components — P:184 "We initialize a cluster C_i for each
+ * connected component of positive cells".  Reading R3: 4-connectivity;
+ * components numbered in order of their first cell in a row-major scan.
+ * Plain definition: flood fill (BFS) started from each unlabelled positive
+ * cell in raster order.  labels[r*C+c] = component id or -1.  bbox[4*i..] =
+ * (c0, r0, c1, r1), inclusive cell coordinates.  Returns the component count. */
+int32_t mpo_components(const uint8_t* pos, int32_t R, int32_t C, int32_t* labels, int32_t* bbox) {
+  int64_t N = (int64_t)R * C;
+  int32_t* queue = (int32_t*)malloc(sizeof(int32_t) * (N > 0 ? N : 1));
+  int32_t ncomp = 0;
+  for (int64_t i = 0; i < N; i++) labels[i] = -1;
+  for (int32_t r = 0; r < R; r++) {
+    for (int32_t c = 0; c < C; c++) {
+      int64_t start = (int64_t)r * C + c;
+      if (!pos[start] || labels[start] >= 0) continue;
+      int32_t id = ncomp++;
+      int32_t c0 = c, r0 = r, c1 = c, r1 = r;
+      int64_t head = 0, tail = 0;
+      labels[start] = id;
+      queue[tail++] = (int32_t)start;
+      while (head < tail) {
+        int32_t cell = queue[head++];
+        int32_t cr = cell / C, cc = cell % C;
+        if (cc < c0) c0 = cc;
+        if (cc > c1) c1 = cc;
+        if (cr < r0) r0 = cr;
+        if (cr > r1) r1 = cr;
+        /* the four edge neighbours: up, down, left, right */
+        int32_t nr[4] = {cr - 1, cr + 1, cr, cr};
+        int32_t nc[4] = {cc, cc, cc - 1, cc + 1};
+        for (int q = 0; q < 4; q++) {
+          if (nr[q] < 0 || nr[q] >= R || nc[q] < 0 || nc[q] >= C) continue;
+          int64_t nb = (int64_t)nr[q] * C + nc[q];
+          if (pos[nb] && labels[nb] < 0) {
+            labels[nb] = id;
+            queue[tail++] = (int32_t)nb;
+          }
+        }
+      }
+      bbox[4 * id + 0] = c0;
+      bbox[4 * id + 1] = r0;
+      bbox[4 * id + 2] = c1;
+      bbox[4 * id + 3] = r1;
+    }
+  }
+  free(queue);
+  return ncomp;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Planner geometry.  Reading R1: a cell is cell_w x cell_h frame px, the last
+ * row/column clipped to the frame.  Pixel bbox of a cell bbox (c0,r0,c1,r1):
+ * [c0*cw, min((c1+1)*cw, W)) x [r0*ch, min((r1+1)*ch, H)). */
+typedef struct {
+  int32_t W, H, cw, ch, k;
+  const mpo_size* sizes;
+  const int64_t* cost;
+} mpo_plan_ctx;
+
+static void pix_extent(const mpo_plan_ctx* P, int32_t c0, int32_t r0, int32_t c1, int32_t r1,
+                       int32_t* px0, int32_t* py0, int32_t* bw, int32_t* bh) {
+  int32_t x0 = c0 * P->cw, y0 = r0 * P->ch;
+  int32_t x1 = (c1 + 1) * P->cw, y1 = (r1 + 1) * P->ch;
+  if (x1 > P->W) x1 = P->W;
+  if (y1 > P->H) y1 = P->H;
+  *px0 = x0;
+  *py0 = y0;
+  *bw = x1 - x0;
+  *bh = y1 - y0;
+}
+
+/* P:184 "identify the smallest-area window size (w,h) that contains the
+ * bounding box".  Reading R6: among sizes with w_i >= bw and h_i >= bh,
+ * minimise (w_i*h_i, w_i, h_i).  Returns the index, or -1 if none fits (never
+ * happens for a validated S, which contains (W,H)). */
+int32_t mpo_smallest_window(const mpo_size* sizes, int32_t k, int32_t bw, int32_t bh) {
+  int32_t best = -1;
+  for (int32_t i = 0; i < k; i++) {
+    if (sizes[i].w < bw || sizes[i].h < bh) continue;
+    if (best < 0) { best = i; continue; }
+    int64_t ai = (int64_t)sizes[i].w * sizes[i].h, ab = (int64_t)sizes[best].w * sizes[best].h;
+    if (ai < ab || (ai == ab && (sizes[i].w < sizes[best].w ||
+                                 (sizes[i].w == sizes[best].w && sizes[i].h < sizes[best].h))))
+      best = i;
+  }
+  return best;
+}
+
+typedef struct { int32_t c0, r0, c1, r1, size; } cluster;
+
+static int32_t cluster_size(const mpo_plan_ctx* P, int32_t c0, int32_t r0, int32_t c1, int32_t r1) {
+  int32_t px0, py0, bw, bh;
+  pix_extent(P, c0, r0, c1, r1, &px0, &py0, &bw, &bh);
+  return mpo_smallest_window(P->sizes, P->k, bw, bh);
+}
+
+static int fits(const mpo_plan_ctx* P, int32_t c0, int32_t r0, int32_t c1, int32_t r1, int32_t s) {
+  int32_t px0, py0, bw, bh;
+  pix_extent(P, c0, r0, c1, r1, &px0, &py0, &bw, &bh);
+  return bw <= P->sizes[s].w && bh <= P->sizes[s].h;
+}
+
+static int32_t imin(int32_t a, int32_t b) { return a < b ? a : b; }
+static int32_t imax(int32_t a, int32_t b) { return a > b ? a : b; }
+
+/*
+ * a3 + a4 for one frame, from its component bounding boxes (in label order).
+ * The greedy of P:184, step by step ("Grouping Cells during Execution"):
+ *   "We then iterate over the clusters.  For each cluster C_i, we identify its
+ *    closest neighbor C_j [R5: squared distance of bbox centres, ties -> the
+ *    smallest list position].  We create a proposed merged cluster C_merged,
+ *    and identify the smallest-area window size (w,h) that contains the
+ *    bounding box of C_merged [R6].  For every other cluster C_k, we check if
+ *    we can add C_k to C_merged without needing a larger window size [R7:
+ *    k ascending, absorbed at once].  Finally ... we compare ... T_{w,h} with
+ *    the sum of the time to process the individual clusters ... If the
+ *    execution time for C_merged is smaller [R8: strict <], then we remove the
+ *    individual clusters and add C_merged [R4: appended at the end].  We
+ *    repeatedly loop over the clusters until we perform a pass without any new
+ *    merges [R9]."
+ *   P:186 "we construct a set of rectangular windows R by creating one
+ *    rectangle for each cluster" — placement R10 (centred, clamped).
+ *   R11: if est(R) > T[full] the plan becomes one full-frame window.
+ *   R12: no components -> no windows.
+ * Writes up to n_comp windows (frame, x, y, w, h, size_idx; slot = -1) and
+ * returns the count.  *passes_out (optional) = number of passes run.
+ */
+int32_t mpo_plan_frame(const mpo_plan_ctx* P, const int32_t* comp_bbox, int32_t n_comp,
+                       int32_t frame, mpo_window* out, int32_t* passes_out) {
+  int32_t passes = 0;
+  if (n_comp == 0) {
+    if (passes_out) *passes_out = 0;
+    return 0;
+  }
+  cluster* L = (cluster*)malloc(sizeof(cluster) * n_comp);
+  uint8_t* member = (uint8_t*)malloc(n_comp);
+  int32_t n = n_comp;
+  for (int32_t i = 0; i < n; i++) {
+    L[i].c0 = comp_bbox[4 * i + 0];
+    L[i].r0 = comp_bbox[4 * i + 1];
+    L[i].c1 = comp_bbox[4 * i + 2];
+    L[i].r1 = comp_bbox[4 * i + 3];
+    L[i].size = cluster_size(P, L[i].c0, L[i].r0, L[i].c1, L[i].r1);
+  }
+  int merged_in_pass = 1;
+  while (merged_in_pass) {
+    merged_in_pass = 0;
+    passes++;
+    int32_t i = 0;
+    while (i < n && n >= 2) {
+      /* (a) closest neighbour j != i; distance between bbox centres, in
+       * doubled-cell units: centre_x*2 = c0 + c1 + 1 (the +1 cancels). */
+      int32_t j = -1;
+      int64_t best_d = 0;
+      for (int32_t q = 0; q < n; q++) {
+        if (q == i) continue;
+        int64_t dx = (int64_t)(L[i].c0 + L[i].c1) - (L[q].c0 + L[q].c1);
+        int64_t dy = (int64_t)(L[i].r0 + L[i].r1) - (L[q].r0 + L[q].r1);
+        int64_t d = dx * dx + dy * dy;
+        if (j < 0 || d < best_d) { j = q; best_d = d; }
+      }
+      /* (b) proposed merge and its smallest containing window size */
+      int32_t mc0 = imin(L[i].c0, L[j].c0), mr0 = imin(L[i].r0, L[j].r0);
+      int32_t mc1 = imax(L[i].c1, L[j].c1), mr1 = imax(L[i].r1, L[j].r1);
+      int32_t s = cluster_size(P, mc0, mr0, mc1, mr1);
+      memset(member, 0, n);
+      member[i] = member[j] = 1;
+      /* (c) absorb every other cluster that fits without a larger window */
+      for (int32_t q = 0; q < n; q++) {
+        if (member[q]) continue;
+        int32_t nc0 = imin(mc0, L[q].c0), nr0 = imin(mr0, L[q].r0);
+        int32_t nc1 = imax(mc1, L[q].c1), nr1 = imax(mr1, L[q].r1);
+        if (fits(P, nc0, nr0, nc1, nr1, s)) {
+          mc0 = nc0; mr0 = nr0; mc1 = nc1; mr1 = nr1;
+          member[q] = 1;
+        }
+      }
+      /* (d) accept iff T_merged < sum of the members' individual times */
+      int64_t sum = 0;
+      for (int32_t q = 0; q < n; q++)
+        if (member[q]) sum += P->cost[L[q].size];
+      if (P->cost[s] < sum) {
+        int32_t before_i = 0, w = 0;
+        for (int32_t q = 0; q < n; q++) {
+          if (member[q]) {
+            if (q < i) before_i++;
+            continue;
+          }
+          L[w++] = L[q];
+        }
+        L[w].c0 = mc0; L[w].r0 = mr0; L[w].c1 = mc1; L[w].r1 = mr1; L[w].size = s;
+        n = w + 1;
+        i -= before_i;
+        merged_in_pass = 1;
+      } else {
+        i++;
+      }
+    }
+  }
+  if (passes_out) *passes_out = passes;
+
+  /* R11 full-frame fallback */
+  int32_t full = -1;
+  for (int32_t q = 0; q < P->k; q++)
+    if (P->sizes[q].w == P->W && P->sizes[q].h == P->H) full = q;
+  int64_t est = 0;
+  for (int32_t q = 0; q < n; q++) est += P->cost[L[q].size];
+  int32_t nw;
+  if (est > P->cost[full]) {
+    out[0].frame = frame; out[0].x = 0; out[0].y = 0;
+    out[0].w = P->W; out[0].h = P->H; out[0].size_idx = full; out[0].slot = -1;
+    nw = 1;
+  } else {
+    /* a4 placement, R10: centre the window on the bbox, clamp into frame */
+    for (int32_t q = 0; q < n; q++) {
+      int32_t px0, py0, bw, bh;
+      pix_extent(P, L[q].c0, L[q].r0, L[q].c1, L[q].r1, &px0, &py0, &bw, &bh);
+      int32_t ws = P->sizes[L[q].size].w, hs = P->sizes[L[q].size].h;
+      int32_t x = px0 - (ws - bw) / 2;   /* ws >= bw, so / is floor */
+      int32_t y = py0 - (hs - bh) / 2;
+      if (x > P->W - ws) x = P->W - ws;
+      if (x < 0) x = 0;
+      if (y > P->H - hs) y = P->H - hs;
+      if (y < 0) y = 0;
+      out[q].frame = frame; out[q].x = x; out[q].y = y; out[q].w = ws; out[q].h = hs;
+      out[q].size_idx = L[q].size; out[q].slot = -1;
+    }
+    nw = n;
+  }
+  free(L);
+  free(member);
+  return nw;
+}
+
+/* Host-side validation shared in meaning (not in code) with the ABI. */
+static int plan_params_ok(int32_t W, int32_t H, int32_t cw, int32_t ch, int32_t k,
+                          const mpo_size* sizes, const int64_t* cost) {
+  if (W < 1 || H < 1 || cw < 1 || ch < 1 || k < 1 || k > 16 || !sizes || !cost) return 0;
+  int full = 0;
+  for (int32_t i = 0; i < k; i++) {
+    if (sizes[i].w < 1 || sizes[i].h < 1 || sizes[i].w > W || sizes[i].h > H || cost[i] <= 0)
+      return 0;
+    if (sizes[i].w == W && sizes[i].h == H) full = 1;
+    for (int32_t j = 0; j < k; j++) {
+      if (i == j) continue;
+      if (sizes[i].w == sizes[j].w && sizes[i].h == sizes[j].h) return 0;
+      int64_t ai = (int64_t)sizes[i].w * sizes[i].h, aj = (int64_t)sizes[j].w * sizes[j].h;
+      if (ai < aj && !(cost[i] < cost[j])) return 0;
+    }
+  }
+  return full;
+}
+
+/*
+ * Batched a1-a4 with the ABI's semantics (include/mp.h mp_plan_windows), on
+ * host pointers.  windows: frame ascending, then list order; slot = rank among
+ * the windows of the same size in that global order; frame_off CSR.
+ * passes (optional, [F]) receives the merge pass count per frame.
+ */
+int32_t mpo_plan_windows(int32_t W, int32_t H, int32_t cw, int32_t ch, float b_proxy, int32_t k,
+                         const mpo_size* sizes, const int64_t* cost, const float* scores,
+                         int32_t F, uint32_t* mask, mpo_window* windows, int32_t max_windows,
+                         int32_t* frame_off, int32_t* class_count, int32_t* passes) {
+  if (!plan_params_ok(W, H, cw, ch, k, sizes, cost) || F < 0) return MPO_ERR_INVALID;
+  int32_t R = (H + ch - 1) / ch, C = (W + cw - 1) / cw;
+  int64_t N = (int64_t)R * C;
+  mpo_plan_ctx P = {W, H, cw, ch, k, sizes, cost};
+  uint8_t* pos = (uint8_t*)malloc(N);
+  int32_t* labels = (int32_t*)malloc(sizeof(int32_t) * N);
+  int32_t* bbox = (int32_t*)malloc(sizeof(int32_t) * 4 * N);
+  mpo_window* fw = (mpo_window*)malloc(sizeof(mpo_window) * (N > 0 ? N : 1));
+  int status = MPO_OK;
+  int32_t total = 0;
+  for (int32_t q = 0; q < k; q++) class_count[q] = 0;
+  for (int32_t f = 0; f < F; f++) {
+    const float* sc = scores + (int64_t)f * N;
+    mpo_threshold(sc, R, C, b_proxy, pos);
+    if (mask) mpo_pack_mask(pos, R, C, mask + (int64_t)f * R * ((C + 31) / 32));
+    int32_t nc = mpo_components(pos, R, C, labels, bbox);
+    int32_t pf = 0;
+    int32_t nw = mpo_plan_frame(&P, bbox, nc, f, fw, &pf);
+    if (passes) passes[f] = pf;
+    frame_off[f] = total;
+    for (int32_t q = 0; q < nw; q++) {
+      fw[q].slot = class_count[fw[q].size_idx]++;
+      if (total < max_windows) windows[total] = fw[q];
+      else status = MPO_ERR_CAPACITY;
+      total++;
+    }
+  }
+  frame_off[F] = total;
+  free(pos); free(labels); free(bbox); free(fw);
+  return status;
+}
+
+/* ------------------------------------------------------------------------ */
+/* a5. Gather + bilinear resize.  The paper never resizes (it decodes at the
+ * detector resolution, and runs the detector "at each of those
+ * sizes"); reading R15 fixes the convention: half-pixel centres
+ * (align_corners=False), taps clamped to the crop, exact integer taps:
+ *   n = (2d+1)*in - out;  n < 0 -> (i0=0, lambda=0);
+ *   else i0 = floor(n / 2out), lambda = (n mod 2out) / 2out;
+ *   i0 >= in-1 -> (i0=in-1, lambda=0);  i1 = min(i0+1, in-1).
+ * Value (fp64): v = (1-ly)[(1-lx)p00 + lx p01] + ly[(1-lx)p10 + lx p11].
+ * f32 out = v (0..255 scale, NCHW); u8 out = clamp(floor(v+0.5), 0, 255)
+ * (R16, NHWC); f64 out (oracle only, for pins) = v, NCHW. */
+void mpo_taps(int32_t in, int32_t out, int32_t d, int32_t* i0, int32_t* i1, double* lam) {
+  int64_t n = (int64_t)(2 * (int64_t)d + 1) * in - out;
+  int64_t a, rem;
+  if (n < 0) {
+    a = 0;
+    rem = 0;
+  } else {
+    a = n / (2 * (int64_t)out);
+    rem = n % (2 * (int64_t)out);
+  }
+  if (a >= in - 1) {
+    a = in - 1;
+    rem = 0;
+  }
+  *i0 = (int32_t)a;
+  *i1 = (int32_t)(a + 1 < in - 1 ? a + 1 : in - 1);
+  *lam = (double)rem / (double)(2 * (int64_t)out);
+}
+
+int32_t mpo_gather_resize(const uint8_t* const* frames, int32_t pitch, int32_t W, int32_t H,
+                          int32_t F, const mpo_window* windows, int32_t n_win, int32_t k,
+                          const mpo_size* sizes, const mpo_size* out_dims, void* const* out,
+                          const int32_t* out_cap, int32_t fmt) {
+  int status = MPO_OK;
+  for (int32_t wi = 0; wi < n_win; wi++) {
+    mpo_window win = windows[wi];
+    if (win.frame < 0 || win.frame >= F || win.size_idx < 0 || win.size_idx >= k ||
+        win.w != sizes[win.size_idx].w || win.h != sizes[win.size_idx].h || win.x < 0 ||
+        win.y < 0 || win.x + win.w > W || win.y + win.h > H || win.slot < 0) {
+      status = MPO_ERR_INVALID;
+      continue;
+    }
+    int32_t kk = win.size_idx;
+    if (win.slot >= out_cap[kk]) {
+      status = MPO_ERR_CAPACITY;
+      continue;
+    }
+    int32_t ow = out_dims[kk].w, oh = out_dims[kk].h;
+    const uint8_t* fr = frames[win.frame];
+    for (int32_t oy = 0; oy < oh; oy++) {
+      int32_t y0, y1;
+      double ly;
+      mpo_taps(win.h, oh, oy, &y0, &y1, &ly);
+      for (int32_t ox = 0; ox < ow; ox++) {
+        int32_t x0, x1;
+        double lx;
+        mpo_taps(win.w, ow, ox, &x0, &x1, &lx);
+        for (int32_t c = 0; c < 3; c++) {
+          double p00 = fr[(int64_t)(win.y + y0) * pitch + (int64_t)(win.x + x0) * 3 + c];
+          double p01 = fr[(int64_t)(win.y + y0) * pitch + (int64_t)(win.x + x1) * 3 + c];
+          double p10 = fr[(int64_t)(win.y + y1) * pitch + (int64_t)(win.x + x0) * 3 + c];
+          double p11 = fr[(int64_t)(win.y + y1) * pitch + (int64_t)(win.x + x1) * 3 + c];
+          double v = (1.0 - ly) * ((1.0 - lx) * p00 + lx * p01) + ly * ((1.0 - lx) * p10 + lx * p11);
+          int64_t plane = (int64_t)oh * ow;
+          if (fmt == MPO_F32_NCHW) {
+            float* o = (float*)out[kk];
+            o[((int64_t)win.slot * 3 + c) * plane + (int64_t)oy * ow + ox] = (float)v;
+          } else if (fmt == MPO_F64_NCHW) {
+            double* o = (double*)out[kk];
+            o[((int64_t)win.slot * 3 + c) * plane + (int64_t)oy * ow + ox] = v;
+          } else {
+            uint8_t* o = (uint8_t*)out[kk];
+            double r = floor(v + 0.5);
+            if (r < 0) r = 0;
+            if (r > 255) r = 255;
+            o[(((int64_t)win.slot * oh + oy) * ow + ox) * 3 + c] = (uint8_t)r;
+          }
+        }
+      }
+    }
+  }
+  return status;
+}
+
+/* ------------------------------------------------------------------------ */
+/* a6. Remap one detector box (reading R18; not in the paper).  Returns 0 if
+ * the box is dropped.  Steps: keep iff score > score_thr (NaN dropped);
+ * clip each coordinate to [0,ow] / [0,oh] with fmin/fmax (a NaN coordinate
+ * becomes the bound); drop if x2 <= x1 or y2 <= y1; map each coordinate
+ * X = fp32( (x_l * w) / ow + x ) with the product, quotient and sum each
+ * rounded in fp64 (the product is exact) and one final rounding to fp32. */
+int32_t mpo_remap_box(mpo_box in, int32_t wx, int32_t wy, int32_t ww, int32_t wh, int32_t ow,
+                      int32_t oh, float score_thr, mpo_box* out) {
+  if (!(in.score > score_thr)) return 0;
+  float x1 = fminf(fmaxf(in.x1, 0.0f), (float)ow);
+  float x2 = fminf(fmaxf(in.x2, 0.0f), (float)ow);
+  float y1 = fminf(fmaxf(in.y1, 0.0f), (float)oh);
+  float y2 = fminf(fmaxf(in.y2, 0.0f), (float)oh);
+  if (!(x2 > x1) || !(y2 > y1)) return 0;
+  volatile double t;
+  t = (double)x1 * (double)ww; t = t / (double)ow; t = t + (double)wx; out->x1 = (float)t;
+  t = (double)y1 * (double)wh; t = t / (double)oh; t = t + (double)wy; out->y1 = (float)t;
+  t = (double)x2 * (double)ww; t = t / (double)ow; t = t + (double)wx; out->x2 = (float)t;
+  t = (double)y2 * (double)wh; t = t / (double)oh; t = t + (double)wy; out->y2 = (float)t;
+  out->score = in.score;
+  out->cls = in.cls;
+  return 1;
+}
+
+/* a7 IoU in fp32, every operation rounded, none contracted (reading R19, the
+ * formula order of torchvision's CPU nms kernel). */
+float mpo_iou(mpo_box a, mpo_box b) {
+  volatile float area_a = (a.x2 - a.x1) * (a.y2 - a.y1);
+  volatile float area_b = (b.x2 - b.x1) * (b.y2 - b.y1);
+  float xx1 = fmaxf(a.x1, b.x1), yy1 = fmaxf(a.y1, b.y1);
+  float xx2 = fminf(a.x2, b.x2), yy2 = fminf(a.y2, b.y2);
+  volatile float iw = xx2 - xx1;
+  volatile float ih = yy2 - yy1;
+  if (iw < 0.0f) iw = 0.0f;
+  if (ih < 0.0f) ih = 0.0f;
+  volatile float inter = iw * ih;
+  volatile float uni = area_a + area_b;
+  uni = uni - inter;
+  volatile float r = inter / uni;
+  return r;
+}
+
+typedef struct { float score; int32_t q; } cand_key;
+
+static int cand_cmp(const void* pa, const void* pb) {
+  const cand_key* a = (const cand_key*)pa;
+  const cand_key* b = (const cand_key*)pb;
+  /* score descending in fp32 value order (-0.0 == +0.0), then q ascending */
+  if (a->score > b->score) return -1;
+  if (a->score < b->score) return 1;
+  return (a->q < b->q) ? -1 : (a->q > b->q);
+}
+
+/*
+ * Batched a6+a7 with the ABI's semantics (include/mp.h mp_remap_nms) on host
+ * pointers.  Per frame: the candidates are the boxes of the frame's windows
+ * (window order, then box order) that survive remap; candidate index q =
+ * global input box index.  Sort by (score desc, q asc); greedy: take each
+ * not-yet-suppressed candidate in order, keep it, suppress every later
+ * candidate of the same cls with IoU > iou_thr (strict).
+ */
+int32_t mpo_remap_nms(const mpo_box* boxes, const int32_t* win_box_off, const mpo_window* windows,
+                      const int32_t* frame_off, int32_t F, int32_t k, const mpo_size* out_dims,
+                      int32_t W, int32_t H, float score_thr, float iou_thr, mpo_box* out,
+                      int32_t* out_src, int32_t max_out, int32_t* out_frame_off) {
+  (void)W;
+  (void)H;
+  int status = MPO_OK;
+  int32_t total = 0;
+  for (int32_t f = 0; f < F; f++) {
+    out_frame_off[f] = total;
+    int32_t w_lo = frame_off[f], w_hi = frame_off[f + 1];
+    int32_t b_lo = win_box_off[w_lo], b_hi = win_box_off[w_hi];
+    int32_t nmax = b_hi - b_lo;
+    if (nmax <= 0) continue;
+    mpo_box* cb = (mpo_box*)malloc(sizeof(mpo_box) * nmax);
+    int32_t* csrc = (int32_t*)malloc(sizeof(int32_t) * nmax);
+    cand_key* key = (cand_key*)malloc(sizeof(cand_key) * nmax);
+    uint8_t* supp = (uint8_t*)calloc(nmax, 1);
+    int32_t n = 0;
+    for (int32_t wi = w_lo; wi < w_hi; wi++) {
+      mpo_window win = windows[wi];
+      if (win.size_idx < 0 || win.size_idx >= k) { status = MPO_ERR_INVALID; continue; }
+      int32_t ow = out_dims[win.size_idx].w, oh = out_dims[win.size_idx].h;
+      for (int32_t b = win_box_off[wi]; b < win_box_off[wi + 1]; b++) {
+        mpo_box r;
+        if (mpo_remap_box(boxes[b], win.x, win.y, win.w, win.h, ow, oh, score_thr, &r)) {
+          cb[n] = r;
+          csrc[n] = b;
+          key[n].score = (r.score == 0.0f) ? 0.0f : r.score; /* -0.0 -> +0.0 */
+          key[n].q = n;
+          n++;
+        }
+      }
+    }
+    qsort(key, n, sizeof(cand_key), cand_cmp);
+    for (int32_t a = 0; a < n; a++) {
+      int32_t ia = key[a].q;
+      if (supp[ia]) continue;
+      if (total < max_out) {
+        out[total] = cb[ia];
+        out_src[total] = csrc[ia];
+      } else {
+        status = MPO_ERR_CAPACITY;
+      }
+      total++;
+      for (int32_t b = a + 1; b < n; b++) {
+        int32_t ib = key[b].q;
+        if (supp[ib] || cb[ib].cls != cb[ia].cls) continue;
+        if (mpo_iou(cb[ia], cb[ib]) > iou_thr) supp[ib] = 1;
+      }
+    }
+    free(cb); free(csrc); free(key); free(supp);
+  }
+  out_frame_off[F] = total;
+  return status;
+}
