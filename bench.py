@@ -1,0 +1,464 @@
+#!/usr/bin/env python3
+"""bench.py — throughput of the proxy-guided window path (plan -> gather/resize
+-> remap/NMS, detector excluded) on B200, per the driver contract.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--config c2_1080p_sparse] [--fmt f32|u8]
+
+A step = one pass of the whole hot path over one synthetic clip (configs[1]:
+1800 frames of 1080p, sparse traffic, S = {256^2, 512^2, full}), inputs
+resident in HBM.  Frames (11.2 GB) exceed L2 (126 MB), so no flush is needed
+between steps.  Multi-GPU: one process per GPU (torchrun), clip c = rank, no
+data-path collective; NCCL all-reduces the counters and the max elapsed time
+once at the end (weak scaling).
+
+--impl reference runs the CPU oracle (oracle/, plain C) on the host cores on a
+bounded sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import synth as S  # noqa: E402
+
+
+# --------------------------------------------------------------------------- shared helpers
+def host_cpu_desc():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model
+
+
+def tapped(n_in, n_out):
+    """Number of distinct source indices the R15 taps touch along one axis."""
+    d = np.arange(n_out, dtype=np.int64)
+    n = (2 * d + 1) * n_in - n_out
+    i0 = np.where(n < 0, 0, n // (2 * n_out))
+    i0 = np.minimum(i0, n_in - 1)
+    i1 = np.minimum(i0 + 1, n_in - 1)
+    return len(np.union1d(i0, i1))
+
+
+def union_area(rects):
+    """Exact area of a union of axis-aligned rectangles (x, y, w, h)."""
+    if len(rects) == 0:
+        return 0
+    xs = np.unique(np.concatenate([rects[:, 0], rects[:, 0] + rects[:, 2]]))
+    ys = np.unique(np.concatenate([rects[:, 1], rects[:, 1] + rects[:, 3]]))
+    cov = np.zeros((len(ys) - 1, len(xs) - 1), bool)
+    for x, y, w, h in rects:
+        i0, i1 = np.searchsorted(xs, [x, x + w])
+        j0, j1 = np.searchsorted(ys, [y, y + h])
+        cov[j0:j1, i0:i1] = True
+    return int((np.diff(ys)[:, None] * np.diff(xs)[None, :] * cov).sum())
+
+
+def algorithmic_bytes(cfg, windows, frame_off, n_box, n_kept, F, fmt_bytes):
+    """SURVEY.md §8(d) algorithmic bytes.  Returns dict with the gather kernel's
+    bytes (union-of-footprints read, conservative; and per-window sum) and the
+    whole step's bytes."""
+    R, C = cfg.grid
+    od = cfg.out_dims
+    sizes = cfg.sizes
+    tap_area = {q: tapped(sizes[q][0], od[q][0]) * tapped(sizes[q][1], od[q][1]) for q in range(len(sizes))}
+    full_tap = all(tap_area[q] == sizes[q][0] * sizes[q][1] for q in tap_area)
+    out_b = sum(3 * od[q][0] * od[q][1] * fmt_bytes for q in windows[:, 5])
+    read_sum = sum(3 * tap_area[q] for q in windows[:, 5])
+    if full_tap:
+        read_union = 0
+        for f in range(F):
+            w = windows[frame_off[f]:frame_off[f + 1]]
+            read_union += 3 * union_area(w[:, 1:5].astype(np.int64))
+    else:
+        read_union = read_sum
+    n_win = len(windows)
+    gather = read_union + out_b + 28 * n_win
+    step = (4 * R * C * F + 28 * n_win * 3 + read_union + out_b + 24 * n_box + 28 * n_kept + 8 * (F + 1))
+    return dict(gather_union=gather, gather_sum=read_sum + out_b + 28 * n_win, step=step, out=out_b,
+                read_union=read_union, read_sum=read_sum)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                smax.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- oracle leg
+ORACLE_MAX_FRAMES = 240
+
+
+def oracle_prepare(cfg, clip, n_frames):
+    """Seeded inputs for the first n_frames of a clip (generation is untimed)."""
+    import oracle as O
+    scene = S.make_scene(cfg, clip, n_frames)
+    scores = S.score_grids(cfg, clip, scene)
+    frames = [S.frame_pixels_np(S.frame_seed(clip, f), cfg.H, cfg.pitch) for f in range(n_frames)]
+    plan_all = O.plan_windows(cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores)
+    boxes, wbo = S.standin_boxes(cfg, clip, scene, plan_all["windows"])
+    return dict(n=n_frames, scores=scores, frames=frames, plan=plan_all, boxes=boxes, wbo=wbo)
+
+
+def oracle_run(cfg, inp, n_frames, threads):
+    """Run the CPU oracle over the first n_frames of the prepared inputs (plan +
+    gather + remap/NMS), frame-parallel over `threads` host threads (ctypes
+    releases the GIL).  Returns elapsed seconds."""
+    import oracle as O
+    from concurrent.futures import ThreadPoolExecutor
+    scores, frames, plan_all, boxes, wbo = inp["scores"], inp["frames"], inp["plan"], inp["boxes"], inp["wbo"]
+    chunks = np.array_split(np.arange(n_frames), max(1, min(threads, n_frames)))
+
+    def work(idx):
+        a, b = int(idx[0]), int(idx[-1]) + 1
+        p = O.plan_windows(cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores[a:b])
+        caps = [int(c) for c in p["class_count"]]
+        O.gather_resize(frames[a:b], cfg.pitch, cfg.W, cfg.H, p["windows"], cfg.sizes, cfg.out_dims, caps)
+        w0, w1 = plan_all["frame_off"][a], plan_all["frame_off"][b]
+        sub_off = plan_all["frame_off"][a:b + 1] - w0
+        bx = boxes[wbo[w0]:wbo[w1]]
+        sub_wbo = wbo[w0:w1 + 1] - wbo[w0]
+        O.remap_nms(bx, sub_wbo, p["windows"], sub_off, cfg.out_dims, cfg.W, cfg.H, cfg.score_thr, cfg.iou_thr)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(work, [c for c in chunks if len(c)]))
+    return time.perf_counter() - t0
+
+
+def oracle_baseline(cfg, clip, threads, target_s):
+    """Bounded oracle sample taking about target_s seconds: returns (fps, n)."""
+    n_max = min(cfg.frames, ORACLE_MAX_FRAMES)
+    inp = oracle_prepare(cfg, clip, n_max)
+    probe_n = min(n_max, max(threads, 8))
+    per_frame = oracle_run(cfg, inp, probe_n, threads) / probe_n
+    n = int(max(1, min(n_max, target_s / max(per_frame, 1e-9))))
+    return inp, n
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = S.CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    import oracle as O
+    O.build()
+    # size each step's sample so the whole run stays within a few minutes
+    inp, n = oracle_baseline(cfg, 0, threads, 120.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        oracle_run(cfg, inp, n, threads)
+    tot = 0.0
+    for _ in range(args.steps):
+        tot += oracle_run(cfg, inp, n, threads)
+    fps = n * args.steps / tot
+    line = {"metric": "frames/sec of proxy-guided window pipeline", "value": fps, "unit": "frames/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "frames_per_step": n, "W": cfg.W, "H": cfg.H},
+            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "oracle",
+                             "sample": f"first {n} frames of clip 0 of {cfg.name} per step "
+                                       f"(plan+gather+remap/NMS), {threads} threads on {host_cpu_desc()}"},
+            "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- B200 leg
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2103_14695_b200 as mp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cfg = S.CONFIGS[args.config]
+    F = cfg.frames
+    clip = rank
+    fmt = mp.MP_OUT_F32_NCHW if args.fmt == "f32" else mp.MP_OUT_U8_NHWC
+    fmt_bytes = 4 if args.fmt == "f32" else 1
+
+    # ---- untimed setup: synthetic inputs resident in HBM
+    scene = S.make_scene(cfg, clip, F)
+    scores_np = S.score_grids(cfg, clip, scene)
+    scores = torch.from_numpy(scores_np).to(dev)
+    frames = S.frame_pixels_torch([S.frame_seed(clip, f) for f in range(F)], cfg.H, cfg.pitch, device=dev)
+    ptrs = mp.WindowPipeline.frame_ptrs(frames)
+    pipe = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
+                             cfg.iou_thr, fmt=fmt, device=dev)
+    R, C = cfg.grid
+    pipe.reserve(F, F * R * ((C + 1) // 2))
+    pipe.plan(scores)
+    torch.cuda.synchronize()
+    pipe.check_status()
+    n_win = int(pipe.frame_off[F].item())
+    counts = pipe.class_count.cpu().tolist()
+    windows = pipe.windows[:n_win].cpu().numpy()
+    frame_off = pipe.frame_off.cpu().numpy()
+    boxes, wbo = S.standin_boxes(cfg, clip, scene, windows)      # detector stand-in (untimed)
+    pipe.reserve(F, n_win, caps=counts, max_boxes=max(len(boxes), 1))
+    boxes_t = torch.from_numpy(boxes.view(np.float32).reshape(-1, 6).copy()).to(dev) if len(boxes) else \
+        torch.zeros((1, 6), dtype=torch.float32, device=dev)
+    wbo_t = torch.from_numpy(wbo).to(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        pipe.plan(scores)
+        if ev is not None:
+            ev[0].record(stream)
+        pipe.gather(ptrs)
+        if ev is not None:
+            ev[1].record(stream)
+        pipe.merge(boxes_t, wbo_t)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    pipe.check_status()
+    n_kept = int(pipe.nms_frame_off[F].item())
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for i in range(args.steps):
+        step(evs[i])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    elapsed_ms = t0.elapsed_time(t1)
+    gather_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    pipe.check_status()
+
+    ab = algorithmic_bytes(cfg, windows, frame_off, len(boxes), n_kept, F, fmt_bytes)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    achieved = ab["gather_union"] / (gather_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_gather_summary.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            if pj.get("config") == cfg.name and pj.get("fmt") == args.fmt:
+                traffic = pj.get("dram_bytes_per_step")
+        except (OSError, ValueError):
+            pass
+
+    # ---- end to end through the public API from pinned host memory (rank-local)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(cfg, clip, scene, scores_np, boxes, wbo, fmt, dev, args)
+
+    frames_done = torch.tensor([F * args.steps], dtype=torch.int64, device=dev)
+    tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(frames_done, op=dist.ReduceOp.SUM)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    total_frames = int(frames_done.item())
+    tmax_ms = float(tmax.item())
+    value = total_frames / (tmax_ms * 1e-3)
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            threads = os.cpu_count() or 1
+            inp, n = oracle_baseline(cfg, clip, threads, 15.0)
+            dt = oracle_run(cfg, inp, n, threads)
+            cpu = {"value": n / dt, "unit": "frames/s", "cores": threads, "kind": "oracle",
+                   "sample": f"first {n} of {F} frames of clip {clip} ({cfg.name}), plan+gather+remap/NMS, "
+                             f"{threads} threads, {host_cpu_desc()}"}
+        line = {
+            "metric": "frames/sec of proxy-guided window pipeline", "value": value, "unit": "frames/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tmax_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "frames_per_step_per_gpu": F, "W": cfg.W, "H": cfg.H,
+                       "sizes": cfg.sizes, "out_dims": cfg.out_dims, "out_format": args.fmt,
+                       "b_proxy": cfg.b_proxy, "windows_per_step": n_win, "class_count": counts,
+                       "raw_boxes_per_step": int(len(boxes)), "kept_boxes_per_step": n_kept,
+                       "l2": "inputs (%.1f GB frames) exceed L2; no flush" % (frames.numel() / 1e9),
+                       "parallelism": f"clip-sharded x{world}"},
+            "roofline": {"bound": "hbm", "kernel": "gather_resize (prep + gather_kernel)",
+                         "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "alg_bytes_per_launch": ab["gather_union"],
+                         "alg_bytes_per_launch_window_sum": ab["gather_sum"],
+                         "launch_ms": gather_ms, "step_alg_bytes": ab["step"],
+                         "step_GBps": ab["step"] / (tmax_ms / args.steps * 1e-3) / 1e9,
+                         "gather_share_of_step": gather_ms / (tmax_ms / args.steps)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * (mp.launches_per_call(0) + mp.launches_per_call(1) +
+                                          mp.launches_per_call(2)),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(cfg, clip, scene, scores_np, boxes, wbo, fmt, dev, args):
+    """Same metric through WindowPipeline with HOST inputs: each step copies the
+    clip's frames (from a pinned host pool), scores and detector boxes H2D and
+    reads the kept boxes back D2H, inside the timed region."""
+    import torch
+
+    import paper_2103_14695_b200 as mp
+    F = cfg.frames
+    pool = min(F, 128)
+    host_frames = torch.empty((pool, cfg.H, cfg.pitch), dtype=torch.uint8).pin_memory()
+    for i in range(pool):
+        host_frames[i].copy_(torch.from_numpy(S.frame_pixels_np(S.frame_seed(clip, i), cfg.H, cfg.pitch)))
+    host_scores = torch.from_numpy(scores_np).pin_memory()
+    host_boxes = torch.from_numpy(boxes.view(np.float32).reshape(-1, 6).copy()).pin_memory()
+    host_wbo = torch.from_numpy(wbo).pin_memory()
+    frames = torch.empty((F, cfg.H, cfg.pitch), dtype=torch.uint8, device=dev)
+    scores = torch.empty_like(host_scores, device=dev)
+    boxes_t = torch.empty_like(host_boxes, device=dev)
+    wbo_t = torch.empty_like(host_wbo, device=dev)
+    ptrs = mp.WindowPipeline.frame_ptrs(frames)
+    pipe = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
+                             cfg.iou_thr, fmt=fmt, device=dev)
+    R, C = cfg.grid
+    pipe.reserve(F, F * R * ((C + 1) // 2))
+    scores.copy_(host_scores)
+    pipe.plan(scores)
+    torch.cuda.synchronize()
+    n_win = int(pipe.frame_off[F].item())
+    pipe.reserve(F, n_win, caps=pipe.class_count.cpu().tolist(), max_boxes=max(len(boxes), 1))
+    out_host = torch.empty((pipe.max_out, 6), dtype=torch.float32).pin_memory()
+    off_host = torch.empty((F + 1,), dtype=torch.int32).pin_memory()
+    stream = torch.cuda.current_stream(dev)
+    h2d = F * cfg.H * cfg.pitch + host_scores.numel() * 4 + host_boxes.numel() * 4 + host_wbo.numel() * 4
+    d2h = off_host.numel() * 4 + out_host.numel() * 4
+
+    def step():
+        for f in range(F):
+            frames[f].copy_(host_frames[f % pool], non_blocking=True)
+        scores.copy_(host_scores, non_blocking=True)
+        boxes_t.copy_(host_boxes, non_blocking=True)
+        wbo_t.copy_(host_wbo, non_blocking=True)
+        pipe.plan(scores)
+        pipe.gather(ptrs)
+        pipe.merge(boxes_t, wbo_t)
+        off_host.copy_(pipe.nms_frame_off, non_blocking=True)
+        out_host.copy_(pipe.nms_out, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    n = max(1, min(args.steps, 3))
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(n):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    pipe.check_status()
+    return {"value": F * n / (ms * 1e-3), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": n}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2_1080p_sparse", choices=sorted(S.CONFIGS))
+    ap.add_argument("--fmt", default="f32", choices=["f32", "u8"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

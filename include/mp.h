@@ -105,7 +105,9 @@ size_t mp_plan_workspace_size(const mp_plan_params* p, int32_t F);
  *                (the true total even on overflow).
  *  d_class_count device int32 [k]: number of windows of each size (true counts).
  *  d_status      device int32: set to MP_ERR_CAPACITY if total > max_windows.
- *  Limits: grid R*C <= 16384 cells (else MP_ERR_UNSUPPORTED).
+ *  Limits: one CTA per frame holds the grid in shared memory (~32 bytes per
+ *  possible run, R*ceil(C/2) runs): up to ~7000 runs (4K at 32 px = 4080)
+ *  and R*C <= 16384 cells; larger grids return MP_ERR_UNSUPPORTED.
  */
 mp_status mp_plan_windows(const mp_plan_params* p, const float* d_scores, int32_t F,
                           uint32_t* d_mask, mp_window* d_windows, int32_t max_windows,
@@ -163,7 +165,9 @@ size_t mp_remap_nms_workspace_size(int32_t F, int32_t max_boxes);
  *  d_out, d_out_src  device [max_out]: kept boxes (frame px) and the index of
  *                 the input box each came from; frame-major, keep order.
  *  d_out_frame_off device int32 [F+1]: CSR of kept boxes (true totals).
- *  Limits: at most 4096 raw boxes per frame (else *d_status = MP_ERR_CAPACITY
+ *  max_boxes      capacity of d_boxes; frames whose boxes extend past it are
+ *                 skipped with *d_status = MP_ERR_INVALID.
+ *  Limits: at most 2048 raw boxes per frame (else *d_status = MP_ERR_CAPACITY
  *  and that frame keeps nothing).
  */
 mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_box_off,

@@ -1,0 +1,13 @@
+"""paper_2103_14695_b200 — B200-native hot path of MultiScope (arXiv 2103.14695):
+proxy-guided window detection around the detector.
+
+The compute lives in libmp_b200.so (hand-written CUDA for sm_100a behind the
+C-ABI of include/mp.h); this package is its thin Python binding plus a buffer
+-owning pipeline wrapper.  Importing it without the built library raises —
+there is no CPU fallback.
+"""
+from ._binding import (MP_ERR_CAPACITY, MP_ERR_CUDA, MP_ERR_INVALID, MP_ERR_UNSUPPORTED, MP_OK,  # noqa: F401
+                       MP_OUT_F32_NCHW, MP_OUT_U8_NHWC, LIB_PATH, MPError, PlanParams, launches_per_call,
+                       mp_gather_resize, mp_gather_workspace_size, mp_plan_windows, mp_plan_workspace_size,
+                       mp_remap_nms, mp_remap_nms_workspace_size, status_string)
+from .pipeline import WindowPipeline  # noqa: F401

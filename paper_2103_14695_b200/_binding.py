@@ -1,0 +1,212 @@
+"""Thin ctypes binding of libmp_b200.so (include/mp.h).
+
+Argument marshalling only: every step of the path runs in the CUDA kernels of
+the library.  Device buffers are torch CUDA tensors; the library never
+allocates.  There is no CPU fallback: if the library is missing this module
+raises at import time.
+
+Tensor conventions (byte-identical to the C structs):
+  windows   int32  [n, 7]  (frame, x, y, w, h, size_idx, slot)      = mp_window
+  boxes     float32 [n, 6] (x1, y1, x2, y2, score, cls-as-int32-bits) = mp_box
+  sizes     list of (w, h)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmp_b200.so")
+
+MP_OK, MP_ERR_INVALID, MP_ERR_CUDA, MP_ERR_CAPACITY, MP_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
+MP_OUT_F32_NCHW, MP_OUT_U8_NHWC = 0, 1
+
+
+class MPError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        super().__init__(f"{where}: {_lib.mp_status_string(code).decode()} (code {code})")
+        self.code = code
+
+
+class mp_size(C.Structure):
+    _fields_ = [("w", C.c_int32), ("h", C.c_int32)]
+
+
+class mp_plan_params(C.Structure):
+    _fields_ = [("W", C.c_int32), ("H", C.c_int32), ("cell_w", C.c_int32), ("cell_h", C.c_int32),
+                ("b_proxy", C.c_float), ("k", C.c_int32), ("sizes", C.POINTER(mp_size)),
+                ("cost", C.POINTER(C.c_int64))]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(nvcc, sm_100a).  There is no CPU fallback.")
+    L = C.CDLL(LIB_PATH)
+    vp, sz, i32, f32 = C.c_void_p, C.c_size_t, C.c_int32, C.c_float
+    L.mp_status_string.restype = C.c_char_p
+    L.mp_status_string.argtypes = [C.c_int]
+    L.mp_launches_per_call.restype = i32
+    L.mp_launches_per_call.argtypes = [i32]
+    L.mp_plan_workspace_size.restype = sz
+    L.mp_plan_workspace_size.argtypes = [C.POINTER(mp_plan_params), i32]
+    L.mp_plan_windows.restype = C.c_int
+    L.mp_plan_windows.argtypes = [C.POINTER(mp_plan_params), vp, i32, vp, vp, i32, vp, vp, vp, vp, sz, vp]
+    L.mp_gather_workspace_size.restype = sz
+    L.mp_gather_workspace_size.argtypes = [i32, vp]
+    L.mp_gather_resize.restype = C.c_int
+    L.mp_gather_resize.argtypes = [vp, i32, i32, i32, i32, vp, vp, i32, vp, vp, vp, vp, C.c_int, vp, vp, sz, vp]
+    L.mp_remap_nms_workspace_size.restype = sz
+    L.mp_remap_nms_workspace_size.argtypes = [i32, i32]
+    L.mp_remap_nms.restype = C.c_int
+    L.mp_remap_nms.argtypes = [vp, vp, vp, vp, i32, i32, vp, i32, i32, f32, f32, vp, vp, i32, vp, vp, i32, vp,
+                               sz, vp]
+    return L
+
+
+_lib = _load()
+
+EXPORTED = ("mp_plan_workspace_size", "mp_plan_windows", "mp_gather_workspace_size", "mp_gather_resize",
+            "mp_remap_nms_workspace_size", "mp_remap_nms", "mp_status_string", "mp_launches_per_call")
+
+
+def lib():
+    return _lib
+
+
+def status_string(code: int) -> str:
+    return _lib.mp_status_string(code).decode()
+
+
+def launches_per_call(which: int) -> int:
+    return int(_lib.mp_launches_per_call(which))
+
+
+def _p(t) -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _dev(t, dtype, name):
+    if t is None:
+        return
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _sizes(sizes: Sequence) -> C.Array:
+    arr = (mp_size * len(sizes))()
+    for i, (w, h) in enumerate(sizes):
+        arr[i].w, arr[i].h = int(w), int(h)
+    return arr
+
+
+class PlanParams:
+    """Host-side planner parameters (mp_plan_params); keeps its arrays alive."""
+
+    def __init__(self, W, H, sizes, cost, b_proxy=0.5, cell_w=32, cell_h=32):
+        self.W, self.H, self.cell_w, self.cell_h = int(W), int(H), int(cell_w), int(cell_h)
+        self.b_proxy = float(b_proxy)
+        self.sizes = [(int(w), int(h)) for (w, h) in sizes]
+        self.cost = [int(c) for c in cost]
+        self._sz = _sizes(self.sizes)
+        self._cost = (C.c_int64 * len(self.cost))(*self.cost)
+        self.c = mp_plan_params(self.W, self.H, self.cell_w, self.cell_h, C.c_float(self.b_proxy),
+                                len(self.sizes), self._sz, self._cost)
+
+    @property
+    def grid(self):
+        return (-(-self.H // self.cell_h), -(-self.W // self.cell_w))
+
+    def with_b(self, b_proxy: float) -> "PlanParams":
+        return PlanParams(self.W, self.H, self.sizes, self.cost, b_proxy, self.cell_w, self.cell_h)
+
+
+def mp_plan_workspace_size(params: PlanParams, F: int) -> int:
+    return int(_lib.mp_plan_workspace_size(C.byref(params.c), int(F)))
+
+
+def mp_plan_windows(params: PlanParams, scores, F, mask, windows, frame_off, class_count, status, ws,
+                    stream=None) -> None:
+    """a1-a4.  scores float32 [F,R,C]; mask uint32-as-int32 [F,R,words] or None;
+    windows int32 [max,7]; frame_off int32 [F+1]; class_count int32 [k];
+    status int32 [1]; ws uint8 workspace."""
+    _dev(scores, torch.float32, "scores")
+    _dev(mask, torch.int32, "mask")
+    _dev(windows, torch.int32, "windows")
+    _dev(frame_off, torch.int32, "frame_off")
+    _dev(class_count, torch.int32, "class_count")
+    _dev(status, torch.int32, "status")
+    _dev(ws, torch.uint8, "ws")
+    max_w = 0 if windows is None else windows.shape[0]
+    st = _lib.mp_plan_windows(C.byref(params.c), _p(scores), int(F), _p(mask), _p(windows), max_w,
+                              _p(frame_off), _p(class_count), _p(status), _p(ws),
+                              0 if ws is None else ws.numel(), _stream(stream))
+    if st != MP_OK:
+        raise MPError(st, "mp_plan_windows")
+
+
+def mp_gather_workspace_size(out_cap: Sequence[int]) -> int:
+    cap = (C.c_int32 * len(out_cap))(*[int(c) for c in out_cap])
+    return int(_lib.mp_gather_workspace_size(len(out_cap), cap))
+
+
+def mp_gather_resize(frame_ptrs, pitch, W, H, F, windows, frame_off, sizes, out_dims, outs, fmt, status, ws,
+                     stream=None) -> None:
+    """a5.  frame_ptrs int64 CUDA tensor [F] of device addresses of uint8
+    [H][pitch] frames; outs = list of k class tensors (f32 [cap,3,oh,ow] or
+    u8 [cap,oh,ow,3]); capacity = outs[k].shape[0]."""
+    _dev(frame_ptrs, torch.int64, "frame_ptrs")
+    _dev(windows, torch.int32, "windows")
+    _dev(frame_off, torch.int32, "frame_off")
+    _dev(status, torch.int32, "status")
+    _dev(ws, torch.uint8, "ws")
+    k = len(sizes)
+    if len(outs) != k or len(out_dims) != k:
+        raise ValueError("sizes, out_dims and outs must have one entry per size class")
+    odt = torch.float32 if fmt == MP_OUT_F32_NCHW else torch.uint8
+    for q, o in enumerate(outs):
+        _dev(o, odt, f"outs[{q}]")
+    ptrs = (C.c_void_p * k)(*[o.data_ptr() for o in outs])
+    cap = (C.c_int32 * k)(*[int(o.shape[0]) for o in outs])
+    st = _lib.mp_gather_resize(_p(frame_ptrs), int(pitch), int(W), int(H), int(F), _p(windows), _p(frame_off), k,
+                               _sizes(sizes), _sizes(out_dims), ptrs, cap, int(fmt), _p(status), _p(ws),
+                               ws.numel(), _stream(stream))
+    if st != MP_OK:
+        raise MPError(st, "mp_gather_resize")
+
+
+def mp_remap_nms_workspace_size(F: int, max_boxes: int) -> int:
+    return int(_lib.mp_remap_nms_workspace_size(int(F), int(max_boxes)))
+
+
+def mp_remap_nms(boxes, win_box_off, windows, frame_off, F, out_dims, W, H, score_thr, iou_thr, out, out_src,
+                 out_frame_off, status, ws, stream=None) -> None:
+    """a6-a7.  boxes float32 [max_boxes,6]; win_box_off int32 [n_win+1];
+    out float32 [max_out,6]; out_src int32 [max_out]; out_frame_off int32 [F+1]."""
+    _dev(boxes, torch.float32, "boxes")
+    _dev(win_box_off, torch.int32, "win_box_off")
+    _dev(windows, torch.int32, "windows")
+    _dev(frame_off, torch.int32, "frame_off")
+    _dev(out, torch.float32, "out")
+    _dev(out_src, torch.int32, "out_src")
+    _dev(out_frame_off, torch.int32, "out_frame_off")
+    _dev(status, torch.int32, "status")
+    _dev(ws, torch.uint8, "ws")
+    st = _lib.mp_remap_nms(_p(boxes), _p(win_box_off), _p(windows), _p(frame_off), int(F), len(out_dims),
+                           _sizes(out_dims), int(W), int(H), C.c_float(score_thr), C.c_float(iou_thr), _p(out),
+                           _p(out_src), int(out.shape[0]), _p(out_frame_off), _p(status),
+                           int(boxes.shape[0]), _p(ws), ws.numel(), _stream(stream))
+    if st != MP_OK:
+        raise MPError(st, "mp_remap_nms")

@@ -1,0 +1,26 @@
+// mp_abi.cu — the small non-compute entry points of the C-ABI (include/mp.h).
+#include "mp_internal.cuh"
+
+extern "C" const char* mp_status_string(mp_status st) {
+  switch (st) {
+    case MP_OK: return "MP_OK";
+    case MP_ERR_INVALID: return "MP_ERR_INVALID: invalid parameters";
+    case MP_ERR_CUDA: return "MP_ERR_CUDA: a CUDA launch or attribute call failed";
+    case MP_ERR_CAPACITY: return "MP_ERR_CAPACITY: an output buffer was too small";
+    case MP_ERR_UNSUPPORTED: return "MP_ERR_UNSUPPORTED: beyond this build's limits";
+  }
+  return "unknown mp_status";
+}
+
+// Kernel launches per call (for bench.py's gpu_launches count):
+//   plan: plan_frames + plan_scan + plan_scatter
+//   gather: gather_prep + gather_kernel
+//   remap_nms: memset (not a kernel) + small + large + scan + scatter
+extern "C" int32_t mp_launches_per_call(int32_t which) {
+  switch (which) {
+    case 0: return 3;
+    case 1: return 2;
+    case 2: return 4;
+  }
+  return 0;
+}

@@ -1,0 +1,171 @@
+// mp_internal.cuh — device helpers shared by the sm_100a kernels of
+// libmp_b200.so (never by the oracle).  PTX wrappers for mbarriers and 1-D
+// bulk (TMA-engine) copies, warp/block scans, and the host-side status enum.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "../../include/mp.h"
+
+namespace mpk {
+
+constexpr int kMaxClasses = 16;
+
+// ----------------------------------------------------------------- status
+__device__ __forceinline__ void set_status(int32_t* d_status, int32_t code) {
+  if (d_status) atomicCAS(d_status, 0, code);   // first error wins; never cleared
+}
+
+// ----------------------------------------------------------------- warp helpers
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+__device__ __forceinline__ long long warp_sum_i64(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int w = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += w;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of a[0..n) in shared memory, in place; returns the
+// total.  `tmp` = shared scratch of >= 33 ints.  All threads must call.
+__device__ __forceinline__ int block_excl_scan_smem(int* a, int n, int* tmp) {
+  const int nt = blockDim.x, tid = threadIdx.x;
+  const int per = (n + nt - 1) / nt;
+  const int lo = min(n, tid * per), hi = min(n, lo + per);
+  int s = 0;
+  for (int i = lo; i < hi; i++) s += a[i];
+  const int lane = tid & 31, wid = tid >> 5, nw = (nt + 31) >> 5;
+  int inc = warp_incl_scan(s);
+  if (lane == 31) tmp[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int v = lane < nw ? tmp[lane] : 0;
+    int vi = warp_incl_scan(v);
+    if (lane < nw) tmp[lane] = vi - v;
+    if (lane == nw - 1) tmp[32] = vi;
+  }
+  __syncthreads();
+  int run = tmp[wid] + inc - s;
+  for (int i = lo; i < hi; i++) {
+    int v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  int total = tmp[32];
+  __syncthreads();
+  return total;
+}
+
+// Block-wide exclusive scan over a strided global int sequence
+// a[0], a[stride], ... (n items) in place; returns the total.  One CTA.
+__device__ __forceinline__ int block_scan_global(int* a, int n, int stride, int* tmp) {
+  const int nt = blockDim.x, tid = threadIdx.x;
+  const int per = (n + nt - 1) / nt;
+  const int lo = min(n, tid * per), hi = min(n, lo + per);
+  int s = 0;
+  for (int i = lo; i < hi; i++) s += a[(size_t)i * stride];
+  const int lane = tid & 31, wid = tid >> 5, nw = (nt + 31) >> 5;
+  int inc = warp_incl_scan(s);
+  if (lane == 31) tmp[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int v = lane < nw ? tmp[lane] : 0;
+    int vi = warp_incl_scan(v);
+    if (lane < nw) tmp[lane] = vi - v;
+    if (lane == nw - 1) tmp[32] = vi;
+  }
+  __syncthreads();
+  int run = tmp[wid] + inc - s;
+  for (int i = lo; i < hi; i++) {
+    int v = a[(size_t)i * stride];
+    a[(size_t)i * stride] = run;
+    run += v;
+  }
+  int total = tmp[32];
+  __syncthreads();
+  return total;
+}
+
+// ----------------------------------------------------------------- mbarrier / bulk copy (sm_90+ PTX, sm_100a here)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D bulk copy global -> shared through the TMA engine (SASS UBLKCP);
+// completion is signalled as tx bytes on `bar`.  src/dst 16-B aligned,
+// bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ----------------------------------------------------------------- misc
+__host__ __device__ __forceinline__ int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace mpk
+
+#define MP_CUDA_TRY(expr)                                  \
+  do {                                                     \
+    cudaError_t e_ = (expr);                               \
+    if (e_ != cudaSuccess) {                               \
+      (void)cudaGetLastError();                            \
+      return MP_ERR_CUDA;                                  \
+    }                                                      \
+  } while (0)

@@ -1,0 +1,430 @@
+// mp_nms.cu — steps a6-a7 (not in the paper; readings R17-R20):
+// remap window-local detector boxes to frame pixels (one fp64 rounding
+// sequence, bit-identical to the reading) and merge the windows of a frame
+// with class-aware greedy NMS over a shared-memory IoU bitmask.
+//
+// Launches:
+//   memset                      large-frame counter
+//   nms_small_kernel   F CTAs   frames with <= 512 raw boxes: remap, ordered
+//                               compaction, bitonic sort of (score desc, index)
+//                               keys, n x ceil(n/64) IoU bitmask, warp-0
+//                               greedy scan; larger frames are queued
+//   nms_large_kernel   #SM CTAs queued frames (<= 2048 raw boxes; bitmask up
+//                               to 1024 candidates, on-the-fly suppression
+//                               beyond)
+//   nms_scan_kernel    1 CTA    kept-box CSR per frame, capacity check
+//   nms_scatter_kernel          compact kept boxes into the caller's buffers
+#include "mp_internal.cuh"
+
+namespace mpk {
+
+struct NmsArgs {
+  int F, k, max_out, max_boxes;
+  float score_thr, iou_thr;
+  int ow[kMaxClasses], oh[kMaxClasses];
+};
+
+constexpr int kSmallCap = 512, kSmallThreads = 256;
+constexpr int kLargeCap = 2048, kLargeMaskCap = 1024, kLargeThreads = 1024;
+
+struct NmsSmem {
+  float4* bx;
+  int* cls;
+  float* score;
+  int* src;
+  int* order;
+  int* keep;
+  unsigned long long* key;    // sort keys, then reused for the IoU bitmask
+  unsigned char* supp;        // on-the-fly suppression flags (overlaps key/mask)
+  int* tmp;
+};
+
+__host__ __device__ inline int pow2_at_least(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+__host__ __device__ inline size_t nms_smem_bytes(int cap, int mask_cap, NmsSmem* S, unsigned char* base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 15) & ~size_t(15);
+    return base ? base + o : nullptr;
+  };
+  NmsSmem s;
+  s.bx = (float4*)take(sizeof(float4) * cap);
+  s.cls = (int*)take(sizeof(int) * cap);
+  s.score = (float*)take(sizeof(float) * cap);
+  s.src = (int*)take(sizeof(int) * cap);
+  s.order = (int*)take(sizeof(int) * cap);
+  s.keep = (int*)take(sizeof(int) * cap);
+  s.tmp = (int*)take(sizeof(int) * 64);
+  const size_t keyb = sizeof(unsigned long long) * pow2_at_least(cap);
+  const size_t maskb = sizeof(unsigned long long) * (size_t)mask_cap * ((mask_cap + 63) / 64);
+  size_t u = keyb > maskb ? keyb : maskb;
+  if ((size_t)cap > u) u = cap;
+  s.key = (unsigned long long*)take(u);
+  s.supp = (unsigned char*)s.key;
+  if (S) *S = s;
+  return off;
+}
+
+// R18: clip to [0,ow]x[0,oh] (fmin/fmax: NaN -> bound), drop degenerate,
+// X = fp32((x_l * w) / ow + x) with each fp64 operation rounded once.
+__device__ __forceinline__ bool remap(const mp_box& b, const mp_window& w, int ow, int oh, float thr, float4& o) {
+  if (!(b.score > thr)) return false;
+  const float x1 = fminf(fmaxf(b.x1, 0.0f), (float)ow), x2 = fminf(fmaxf(b.x2, 0.0f), (float)ow);
+  const float y1 = fminf(fmaxf(b.y1, 0.0f), (float)oh), y2 = fminf(fmaxf(b.y2, 0.0f), (float)oh);
+  if (!(x2 > x1) || !(y2 > y1)) return false;
+  const double W = (double)w.w, H = (double)w.h, OW = (double)ow, OH = (double)oh;
+  const double X = (double)w.x, Y = (double)w.y;
+  o.x = __double2float_rn(__dadd_rn(__ddiv_rn(__dmul_rn((double)x1, W), OW), X));
+  o.y = __double2float_rn(__dadd_rn(__ddiv_rn(__dmul_rn((double)y1, H), OH), Y));
+  o.z = __double2float_rn(__dadd_rn(__ddiv_rn(__dmul_rn((double)x2, W), OW), X));
+  o.w = __double2float_rn(__dadd_rn(__ddiv_rn(__dmul_rn((double)y2, H), OH), Y));
+  return true;
+}
+
+// R19: fp32 IoU, every operation individually rounded (no FMA contraction),
+// torchvision's formula order: inter / ((area_a + area_b) - inter).
+__device__ __forceinline__ float iou_rn(const float4 a, const float4 b) {
+  const float area_a = __fmul_rn(__fsub_rn(a.z, a.x), __fsub_rn(a.w, a.y));
+  const float area_b = __fmul_rn(__fsub_rn(b.z, b.x), __fsub_rn(b.w, b.y));
+  const float iw = fmaxf(__fsub_rn(fminf(a.z, b.z), fmaxf(a.x, b.x)), 0.0f);
+  const float ih = fmaxf(__fsub_rn(fminf(a.w, b.w), fmaxf(a.y, b.y)), 0.0f);
+  const float inter = __fmul_rn(iw, ih);
+  return __fdiv_rn(inter, __fsub_rn(__fadd_rn(area_a, area_b), inter));
+}
+
+__device__ __forceinline__ unsigned int score_desc_bits(float s) {
+  if (s == 0.0f) s = 0.0f;   // -0.0 -> +0.0 (equal in fp32 value order)
+  const unsigned int u = __float_as_uint(s);
+  const unsigned int asc = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ~asc;
+}
+
+// Index of the window containing raw box b: largest wi in [lo,hi) with off[wi] <= b.
+__device__ __forceinline__ int window_of(const int* __restrict__ off, int lo, int hi, int b) {
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(off + mid) <= b) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Process one frame with the whole CTA.  Returns nothing; writes kept boxes to
+// the frame's scratch region (raw-box offsets) and ws_kept[f].
+__device__ void nms_frame(const NmsArgs& A, int f, int b_lo, int b_hi, int w_lo, int w_hi, const NmsSmem& S,
+                          int cap, int mask_cap, const mp_box* __restrict__ boxes,
+                          const int* __restrict__ win_box_off, const mp_window* __restrict__ windows,
+                          mp_box* __restrict__ ws_box, int* __restrict__ ws_src, int* __restrict__ ws_kept) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  // ---- a6: remap + ordered compaction (candidate order = input order)
+  int n = 0;
+  for (int base = b_lo; base < b_hi; base += blockDim.x) {
+    const int b = base + tid;
+    bool ok = false;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    mp_box bb;
+    if (b < b_hi) {
+      const int wi = window_of(win_box_off, w_lo, w_hi, b);
+      const mp_window w = windows[wi];
+      bb = boxes[b];
+      const int q = w.size_idx;
+      ok = (q >= 0 && q < A.k) && remap(bb, w, A.ow[q], A.oh[q], A.score_thr, o);
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, ok);
+    if (lane == 0) S.tmp[wid] = __popc(m);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int q = 0; q < nw; q++) {
+      const int c = S.tmp[q];
+      before += (q < wid) ? c : 0;
+      tot += c;
+    }
+    if (ok) {
+      const int p = n + before + __popc(m & lanemask_lt());
+      S.bx[p] = o;
+      S.cls[p] = bb.cls;
+      S.score[p] = bb.score;
+      S.src[p] = b;
+      S.key[p] = ((unsigned long long)score_desc_bits(bb.score) << 32) | (unsigned)p;
+    }
+    n += tot;
+    __syncthreads();
+  }
+  // ---- sort keys ascending = (score desc, candidate index asc)
+  const int P = pow2_at_least(n < 1 ? 1 : n);
+  for (int p = n + tid; p < P; p += blockDim.x) S.key[p] = ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = tid; t < (P >> 1); t += blockDim.x) {
+        const int i = 2 * j * (t / j) + (t % j);
+        const int l = i + j;
+        const bool up = (i & k) == 0;
+        const unsigned long long a = S.key[i], c = S.key[l];
+        if ((a > c) == up) {
+          S.key[i] = c;
+          S.key[l] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int p = tid; p < n; p += blockDim.x) S.order[p] = (int)(S.key[p] & 0xffffffffu);
+  __syncthreads();
+
+  // ---- a7: greedy class-aware NMS
+  int nk = 0;
+  if (n <= mask_cap) {
+    const int words = (n + 63) >> 6;
+    unsigned long long* mask = S.key;
+    for (int idx = tid; idx < n * words; idx += blockDim.x) {
+      const int i = idx / words, wd = idx - i * words;
+      const int qi = S.order[i];
+      const float4 bi = S.bx[qi];
+      const int ci = S.cls[qi];
+      unsigned long long bits = 0;
+      const int j0 = max(i + 1, wd * 64), j1 = min(n, wd * 64 + 64);
+      for (int j = j0; j < j1; j++) {
+        const int qj = S.order[j];
+        if (S.cls[qj] == ci && iou_rn(bi, S.bx[qj]) > A.iou_thr) bits |= 1ull << (j - wd * 64);
+      }
+      mask[idx] = bits;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      unsigned long long r0 = 0, r1 = 0;
+      for (int i = 0; i < n; i++) {
+        const int wd = i >> 6;
+        const unsigned long long mine = (wd >> 5) ? r1 : r0;
+        const unsigned long long wv = __shfl_sync(0xffffffffu, mine, wd & 31);
+        if (!((wv >> (i & 63)) & 1ull)) {
+          if (lane == 0) S.keep[nk] = i;
+          nk++;
+          if (lane < words) r0 |= mask[(size_t)i * words + lane];
+          if (lane + 32 < words) r1 |= mask[(size_t)i * words + lane + 32];
+        }
+      }
+      if (lane == 0) S.tmp[32] = nk;
+    }
+    __syncthreads();
+    nk = S.tmp[32];
+  } else {
+    for (int p = tid; p < n; p += blockDim.x) S.supp[p] = 0;
+    __syncthreads();
+    for (int i = 0; i < n; i++) {
+      if (!S.supp[i]) {   // uniform across the CTA (read after the barrier)
+        const int qi = S.order[i];
+        const float4 bi = S.bx[qi];
+        const int ci = S.cls[qi];
+        if (tid == 0) S.keep[nk] = i;
+        nk++;
+        for (int j = i + 1 + tid; j < n; j += blockDim.x) {
+          const int qj = S.order[j];
+          if (!S.supp[j] && S.cls[qj] == ci && iou_rn(bi, S.bx[qj]) > A.iou_thr) S.supp[j] = 1;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ---- output in keep order to the frame's scratch region
+  for (int r = tid; r < nk; r += blockDim.x) {
+    const int q = S.order[S.keep[r]];
+    const float4 o = S.bx[q];
+    mp_box ob;
+    ob.x1 = o.x;
+    ob.y1 = o.y;
+    ob.x2 = o.z;
+    ob.y2 = o.w;
+    ob.score = S.score[q];
+    ob.cls = S.cls[q];
+    ws_box[b_lo + r] = ob;
+    ws_src[b_lo + r] = S.src[q];
+  }
+  if (tid == 0) ws_kept[f] = nk;
+}
+
+__device__ __forceinline__ bool frame_range(const NmsArgs& A, int f, const int* frame_off, const int* win_box_off,
+                                            int& w_lo, int& w_hi, int& b_lo, int& b_hi) {
+  w_lo = frame_off[f];
+  w_hi = frame_off[f + 1];
+  b_lo = win_box_off[w_lo];
+  b_hi = win_box_off[w_hi];
+  return b_lo >= 0 && b_hi >= b_lo && b_hi <= A.max_boxes;
+}
+
+__global__ void __launch_bounds__(kSmallThreads) nms_small_kernel(NmsArgs A, const mp_box* __restrict__ boxes,
+                                                                  const int* __restrict__ win_box_off,
+                                                                  const mp_window* __restrict__ windows,
+                                                                  const int* __restrict__ frame_off,
+                                                                  mp_box* __restrict__ ws_box, int* __restrict__ ws_src,
+                                                                  int* __restrict__ ws_kept, int* __restrict__ large_cnt,
+                                                                  int* __restrict__ large_list, int* __restrict__ d_status) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int f = blockIdx.x;
+  int w_lo, w_hi, b_lo, b_hi;
+  if (!frame_range(A, f, frame_off, win_box_off, w_lo, w_hi, b_lo, b_hi)) {
+    if (threadIdx.x == 0) {
+      ws_kept[f] = 0;
+      set_status(d_status, MP_ERR_INVALID);
+    }
+    return;
+  }
+  if (b_hi - b_lo > kSmallCap) {
+    if (threadIdx.x == 0) large_list[atomicAdd(large_cnt, 1)] = f;
+    return;
+  }
+  NmsSmem S;
+  nms_smem_bytes(kSmallCap, kSmallCap, &S, smem);
+  nms_frame(A, f, b_lo, b_hi, w_lo, w_hi, S, kSmallCap, kSmallCap, boxes, win_box_off, windows, ws_box, ws_src,
+            ws_kept);
+}
+
+__global__ void __launch_bounds__(kLargeThreads) nms_large_kernel(NmsArgs A, const mp_box* __restrict__ boxes,
+                                                                  const int* __restrict__ win_box_off,
+                                                                  const mp_window* __restrict__ windows,
+                                                                  const int* __restrict__ frame_off,
+                                                                  mp_box* __restrict__ ws_box, int* __restrict__ ws_src,
+                                                                  int* __restrict__ ws_kept, const int* __restrict__ large_cnt,
+                                                                  const int* __restrict__ large_list,
+                                                                  int* __restrict__ d_status) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  NmsSmem S;
+  nms_smem_bytes(kLargeCap, kLargeMaskCap, &S, smem);
+  const int nl = *large_cnt;
+  for (int li = blockIdx.x; li < nl; li += gridDim.x) {
+    const int f = large_list[li];
+    int w_lo, w_hi, b_lo, b_hi;
+    frame_range(A, f, frame_off, win_box_off, w_lo, w_hi, b_lo, b_hi);
+    if (b_hi - b_lo > kLargeCap) {
+      if (threadIdx.x == 0) {
+        ws_kept[f] = 0;
+        set_status(d_status, MP_ERR_CAPACITY);
+      }
+      continue;
+    }
+    nms_frame(A, f, b_lo, b_hi, w_lo, w_hi, S, kLargeCap, kLargeMaskCap, boxes, win_box_off, windows, ws_box,
+              ws_src, ws_kept);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024) nms_scan_kernel(int F, const int* __restrict__ ws_kept,
+                                                        int* __restrict__ out_frame_off, int max_out,
+                                                        int* __restrict__ d_status) {
+  __shared__ int tmp[40];
+  for (int f = threadIdx.x; f < F; f += blockDim.x) out_frame_off[f] = ws_kept[f];
+  __syncthreads();
+  const int total = block_scan_global(out_frame_off, F, 1, tmp);
+  if (threadIdx.x == 0) {
+    out_frame_off[F] = total;
+    if (total > max_out) set_status(d_status, MP_ERR_CAPACITY);
+  }
+}
+
+__global__ void __launch_bounds__(256) nms_scatter_kernel(int F, const int* __restrict__ frame_off,
+                                                          const int* __restrict__ win_box_off,
+                                                          const mp_box* __restrict__ ws_box,
+                                                          const int* __restrict__ ws_src, const int* __restrict__ ws_kept,
+                                                          const int* __restrict__ out_frame_off, mp_box* __restrict__ out,
+                                                          int* __restrict__ out_src, int max_out) {
+  const int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (f >= F) return;
+  const int b_lo = win_box_off[frame_off[f]];
+  const int n = ws_kept[f], base = out_frame_off[f];
+  for (int r = lane; r < n; r += 32) {
+    const int d = base + r;
+    if (d >= max_out) break;
+    out[d] = ws_box[b_lo + r];
+    out_src[d] = ws_src[b_lo + r];
+  }
+}
+
+struct NmsWs {
+  size_t box_off, src_off, kept_off, lcnt_off, llist_off, total;
+};
+
+static NmsWs nms_ws_layout(int F, int max_boxes) {
+  NmsWs L;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  L.box_off = 0;
+  L.src_off = al(sizeof(mp_box) * (size_t)max_boxes);
+  L.kept_off = al(L.src_off + sizeof(int) * (size_t)max_boxes);
+  L.lcnt_off = al(L.kept_off + sizeof(int) * (size_t)F);
+  L.llist_off = al(L.lcnt_off + sizeof(int));
+  L.total = al(L.llist_off + sizeof(int) * (size_t)F) + 256;
+  return L;
+}
+
+}  // namespace mpk
+
+using namespace mpk;
+
+extern "C" size_t mp_remap_nms_workspace_size(int32_t F, int32_t max_boxes) {
+  if (F < 0 || max_boxes < 0) return 0;
+  return nms_ws_layout(F, max_boxes).total;
+}
+
+extern "C" mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_box_off, const mp_window* d_windows,
+                                  const int32_t* d_frame_off, int32_t F, int32_t k, const mp_size* out_dims,
+                                  int32_t W, int32_t H, float score_thr, float iou_thr, mp_box* d_out,
+                                  int32_t* d_out_src, int32_t max_out, int32_t* d_out_frame_off, int32_t* d_status,
+                                  int32_t max_boxes, void* d_ws, size_t ws_bytes, void* stream) {
+  if (F < 0 || k < 1 || k > kMaxClasses || !out_dims || W < 1 || H < 1 || max_out < 0 || max_boxes < 0)
+    return MP_ERR_INVALID;
+  if (!d_out_frame_off || !d_status || !d_frame_off || !d_win_box_off) return MP_ERR_INVALID;
+  if (max_out > 0 && (!d_out || !d_out_src)) return MP_ERR_INVALID;
+  if (F > 0 && (!d_windows || (max_boxes > 0 && !d_boxes))) return MP_ERR_INVALID;
+  if (!(iou_thr == iou_thr) || !(score_thr == score_thr)) return MP_ERR_INVALID;
+  NmsArgs A;
+  memset(&A, 0, sizeof(A));
+  A.F = F;
+  A.k = k;
+  A.max_out = max_out;
+  A.max_boxes = max_boxes;
+  A.score_thr = score_thr;
+  A.iou_thr = iou_thr;
+  for (int q = 0; q < k; q++) {
+    if (out_dims[q].w < 1 || out_dims[q].h < 1) return MP_ERR_INVALID;
+    A.ow[q] = out_dims[q].w;
+    A.oh[q] = out_dims[q].h;
+  }
+  const NmsWs L = nms_ws_layout(F, max_boxes);
+  if (!d_ws || ws_bytes < L.total) return MP_ERR_INVALID;
+  unsigned char* ws = (unsigned char*)d_ws;
+  mp_box* ws_box = (mp_box*)(ws + L.box_off);
+  int* ws_src = (int*)(ws + L.src_off);
+  int* ws_kept = (int*)(ws + L.kept_off);
+  int* lcnt = (int*)(ws + L.lcnt_off);
+  int* llist = (int*)(ws + L.llist_off);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (F > 0) {
+    MP_CUDA_TRY(cudaMemsetAsync(lcnt, 0, sizeof(int), s));
+    const size_t sm_small = nms_smem_bytes(kSmallCap, kSmallCap, nullptr, nullptr);
+    const size_t sm_large = nms_smem_bytes(kLargeCap, kLargeMaskCap, nullptr, nullptr);
+    MP_CUDA_TRY(cudaFuncSetAttribute(nms_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_small));
+    MP_CUDA_TRY(cudaFuncSetAttribute(nms_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_large));
+    nms_small_kernel<<<F, kSmallThreads, sm_small, s>>>(A, d_boxes, d_win_box_off, d_windows, d_frame_off, ws_box,
+                                                        ws_src, ws_kept, lcnt, llist, d_status);
+    MP_CUDA_TRY(cudaGetLastError());
+    int dev = 0, sms = 0;
+    MP_CUDA_TRY(cudaGetDevice(&dev));
+    MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    nms_large_kernel<<<sms, kLargeThreads, sm_large, s>>>(A, d_boxes, d_win_box_off, d_windows, d_frame_off,
+                                                          ws_box, ws_src, ws_kept, lcnt, llist, d_status);
+    MP_CUDA_TRY(cudaGetLastError());
+  }
+  nms_scan_kernel<<<1, 1024, 0, s>>>(F, ws_kept, d_out_frame_off, max_out, d_status);
+  MP_CUDA_TRY(cudaGetLastError());
+  if (F > 0) {
+    nms_scatter_kernel<<<(F + 7) / 8, 256, 0, s>>>(F, d_frame_off, d_win_box_off, ws_box, ws_src, ws_kept,
+                                                   d_out_frame_off, d_out, d_out_src, max_out);
+    MP_CUDA_TRY(cudaGetLastError());
+  }
+  return MP_OK;
+}

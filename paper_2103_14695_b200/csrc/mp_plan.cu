@@ -1,0 +1,531 @@
+// mp_plan.cu — steps a1-a4 of the proxy-guided window path on sm_100a:
+// threshold the proxy score grid, label 4-connected components of positive
+// cells, run the greedy agglomerative merge of PAPER.md:184 and place one
+// window per cluster.  Readings R1-R14 are in DESIGN.md §3.
+//
+// Launches (all on the caller's stream, no host sync):
+//   K1-K3 plan_frames_kernel   one CTA per frame: ballot threshold -> run
+//                              extraction -> shared-memory union-find over
+//                              runs -> component bboxes -> warp-0 greedy merge
+//                              -> placement into per-frame scratch
+//   K4a   plan_scan_kernel     one CTA: frame CSR + per-class slot bases
+//   K4b   plan_scatter_kernel  warp per frame: final window records + slots
+#include <climits>
+
+#include "mp_internal.cuh"
+
+namespace mpk {
+
+struct PlanArgs {
+  int W, H, cw, ch, R, C, words, k, full, maxc;
+  float b;
+  int order[kMaxClasses];          // size indices sorted by (w*h, w, h)  (R6)
+  int sw[kMaxClasses], sh[kMaxClasses];
+  long long cost[kMaxClasses];
+};
+
+// R6: smallest-area size containing (bw, bh); ties by smaller w then h.
+__device__ __forceinline__ int smallest_size(const PlanArgs& P, int bw, int bh) {
+  for (int q = 0; q < P.k; q++) {
+    int i = P.order[q];
+    if (P.sw[i] >= bw && P.sh[i] >= bh) return i;
+  }
+  return P.full;   // unreachable: (W,H) is in S
+}
+
+// R1: pixel extent of a cell bbox, last row/col clipped to the frame.
+__device__ __forceinline__ void extent(const PlanArgs& P, int c0, int r0, int c1, int r1, int& px0,
+                                       int& py0, int& bw, int& bh) {
+  px0 = c0 * P.cw;
+  py0 = r0 * P.ch;
+  bw = min((c1 + 1) * P.cw, P.W) - px0;
+  bh = min((r1 + 1) * P.ch, P.H) - py0;
+}
+
+__device__ __forceinline__ int uf_find(volatile int* parent, int x) {
+  while (true) {
+    int p = parent[x];
+    if (p == x) return x;
+    int gp = parent[p];
+    if (gp != p) parent[x] = gp;   // path halving (benign: gp is an ancestor)
+    x = p;
+  }
+}
+
+// Link the larger root under the smaller one, so every final root is the
+// smallest run index of its component (= its first run in row-major order).
+__device__ __forceinline__ void uf_unite(int* parent, int a, int b) {
+  volatile int* vp = parent;
+  while (true) {
+    a = uf_find(vp, a);
+    b = uf_find(vp, b);
+    if (a == b) return;
+    if (a > b) {
+      int t = a;
+      a = b;
+      b = t;
+    }
+    int old = atomicCAS(&parent[b], b, a);
+    if (old == b) return;
+    b = old;
+  }
+}
+
+struct PlanSmem {
+  uint32_t* bits;
+  int *row_off, *tmp, *parent, *cid, *bc0, *br0, *bc1, *br1, *run;
+  short *rrow, *rcs, *rce;
+  unsigned char *csz, *memb;
+};
+
+__host__ __device__ inline size_t plan_smem_bytes(int R, int words, int maxc, PlanSmem* out,
+                                                  unsigned char* base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 15) & ~size_t(15);
+    return base ? base + o : nullptr;
+  };
+  PlanSmem s;
+  s.bits = (uint32_t*)take(sizeof(uint32_t) * R * words);
+  s.row_off = (int*)take(sizeof(int) * (R + 1));
+  s.tmp = (int*)take(sizeof(int) * 40);
+  s.run = (int*)take(sizeof(int) * kMaxClasses);
+  s.parent = (int*)take(sizeof(int) * maxc);
+  s.cid = (int*)take(sizeof(int) * maxc);
+  s.bc0 = (int*)take(sizeof(int) * maxc);
+  s.br0 = (int*)take(sizeof(int) * maxc);
+  s.bc1 = (int*)take(sizeof(int) * maxc);
+  s.br1 = (int*)take(sizeof(int) * maxc);
+  s.rrow = (short*)take(sizeof(short) * maxc);
+  s.rcs = (short*)take(sizeof(short) * maxc);
+  s.rce = (short*)take(sizeof(short) * maxc);
+  s.csz = (unsigned char*)take(maxc);
+  s.memb = (unsigned char*)take(maxc);
+  if (out) *out = s;
+  return off;
+}
+
+constexpr int kPlanThreads = 256;
+
+__global__ void __launch_bounds__(kPlanThreads) plan_frames_kernel(PlanArgs P, const float* __restrict__ scores,
+                                                                   uint32_t* __restrict__ mask_out,
+                                                                   int4* __restrict__ ws_win,
+                                                                   int* __restrict__ ws_count,
+                                                                   int* __restrict__ ws_cls) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PlanSmem S;
+  plan_smem_bytes(P.R, P.words, P.maxc, &S, smem_raw);
+
+  const int f = blockIdx.x;
+  const int R = P.R, C = P.C, words = P.words;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
+  const float* sc = scores + (size_t)f * R * C;
+
+  // ---- a1: threshold, one warp-ballot per 32 cells of a row (R2)
+  for (int rw = wid; rw < R * words; rw += nwarps) {
+    const int r = rw / words, w = rw - r * words, c = w * 32 + lane;
+    bool pos = false;
+    if (c < C) pos = __ldg(sc + (size_t)r * C + c) > P.b;   // NaN -> false
+    const uint32_t m = __ballot_sync(0xffffffffu, pos);
+    if (lane == 0) {
+      S.bits[rw] = m;
+      if (mask_out) mask_out[(size_t)f * R * words + rw] = m;
+    }
+  }
+  __syncthreads();
+
+  // ---- a2: horizontal runs of positive cells (run starts = m & ~(m<<1 | carry))
+  for (int r = tid; r < R; r += blockDim.x) {
+    int n = 0;
+    uint32_t prev = 0;
+    for (int w = 0; w < words; w++) {
+      const uint32_t m = S.bits[r * words + w];
+      n += __popc(m & ~((m << 1) | (prev >> 31)));
+      prev = m;
+    }
+    S.row_off[r] = n;
+  }
+  __syncthreads();
+  const int nruns = block_excl_scan_smem(S.row_off, R, S.tmp);
+  for (int r = tid; r < R; r += blockDim.x) {
+    const int base = S.row_off[r];
+    int ns = 0, ne = 0;
+    uint32_t prev = 0;
+    for (int w = 0; w < words; w++) {
+      const uint32_t m = S.bits[r * words + w];
+      const uint32_t next = (w + 1 < words) ? S.bits[r * words + w + 1] : 0u;
+      uint32_t starts = m & ~((m << 1) | (prev >> 31));
+      uint32_t ends = m & ~((m >> 1) | (next << 31));
+      while (starts) {
+        const int b = __ffs(starts) - 1;
+        starts &= starts - 1;
+        S.rcs[base + ns] = (short)(w * 32 + b);
+        S.rrow[base + ns] = (short)r;
+        ns++;
+      }
+      while (ends) {
+        const int b = __ffs(ends) - 1;
+        ends &= ends - 1;
+        S.rce[base + ne] = (short)(w * 32 + b);
+        ne++;
+      }
+      prev = m;
+    }
+  }
+  for (int u = tid; u < nruns; u += blockDim.x) S.parent[u] = u;
+  if (tid == 0) S.row_off[R] = nruns;
+  __syncthreads();
+
+  // 4-connectivity (R3): a run touches the runs of the previous row that share a column.
+  for (int u = tid; u < nruns; u += blockDim.x) {
+    const int r = S.rrow[u];
+    if (r == 0) continue;
+    const int cs = S.rcs[u], ce = S.rce[u];
+    for (int v = S.row_off[r - 1]; v < S.row_off[r]; v++) {
+      if (S.rcs[v] > ce) break;
+      if (S.rce[v] >= cs) uf_unite(S.parent, u, v);
+    }
+  }
+  __syncthreads();
+  // parent := root; cid := is-root flag, then exclusive scan -> component ids
+  // in order of first run (= first cell in a row-major scan).
+  for (int u = tid; u < nruns; u += blockDim.x) S.cid[u] = uf_find(S.parent, u);
+  __syncthreads();
+  for (int u = tid; u < nruns; u += blockDim.x) S.parent[u] = S.cid[u];
+  __syncthreads();
+  for (int u = tid; u < nruns; u += blockDim.x) S.cid[u] = (S.parent[u] == u) ? 1 : 0;
+  __syncthreads();
+  const int ncomp = block_excl_scan_smem(S.cid, nruns, S.tmp);
+  for (int q = tid; q < ncomp; q += blockDim.x) {
+    S.bc0[q] = INT_MAX;
+    S.br0[q] = INT_MAX;
+    S.bc1[q] = -1;
+    S.br1[q] = -1;
+  }
+  __syncthreads();
+  for (int u = tid; u < nruns; u += blockDim.x) {
+    const int q = S.cid[S.parent[u]];
+    atomicMin(&S.bc0[q], (int)S.rcs[u]);
+    atomicMax(&S.bc1[q], (int)S.rce[u]);
+    atomicMin(&S.br0[q], (int)S.rrow[u]);
+    atomicMax(&S.br1[q], (int)S.rrow[u]);
+  }
+  __syncthreads();
+  for (int q = tid; q < ncomp; q += blockDim.x) {
+    int px0, py0, bw, bh;
+    extent(P, S.bc0[q], S.br0[q], S.bc1[q], S.br1[q], px0, py0, bw, bh);
+    S.csz[q] = (unsigned char)smallest_size(P, bw, bh);
+    S.memb[q] = 0;
+  }
+  if (tid < kMaxClasses) S.run[tid] = 0;
+  __syncthreads();
+  if (wid != 0) return;
+
+  // ---- a3: greedy agglomerative merge, warp 0 ------------
+  const long long* T = P.cost;
+  int n = ncomp;
+  bool again = n > 0;
+  while (again) {
+    again = false;
+    int i = 0;
+    while (i < n && n >= 2) {
+      const int ic0 = S.bc0[i], ir0 = S.br0[i], ic1 = S.bc1[i], ir1 = S.br1[i];
+      const int sx = ic0 + ic1, sy = ir0 + ir1;
+      // (a) closest neighbour: squared distance of bbox centres (doubled cell
+      //     units), ties -> smallest position (R5)
+      unsigned long long best = ~0ull;
+      for (int j = lane; j < n; j += 32) {
+        if (j == i) continue;
+        const int dx = sx - (S.bc0[j] + S.bc1[j]);
+        const int dy = sy - (S.br0[j] + S.br1[j]);
+        const unsigned long long key =
+            ((unsigned long long)(unsigned)(dx * dx + dy * dy) << 32) | (unsigned)j;
+        best = key < best ? key : best;
+      }
+      best = warp_min_u64(best);
+      const int j = (int)(best & 0xffffffffu);
+      // (b) proposed merge and its smallest containing size (R6)
+      int m0 = min(ic0, S.bc0[j]), n0 = min(ir0, S.br0[j]);
+      int m1 = max(ic1, S.bc1[j]), n1 = max(ir1, S.br1[j]);
+      int px0, py0, bw, bh;
+      extent(P, m0, n0, m1, n1, px0, py0, bw, bh);
+      const int s = smallest_size(P, bw, bh);
+      const int ws = P.sw[s], hs = P.sh[s];
+      long long sum = T[S.csz[i]] + T[S.csz[j]];
+      int before_i = (j < i) ? 1 : 0;
+      if (lane == 0) {
+        S.memb[i] = 1;
+        S.memb[j] = 1;
+      }
+      // (c) absorb, k ascending, each fitting cluster immediately (R7): a
+      //     ballot finds the first fitting k; earlier non-fitting ones can never
+      //     fit later because the box only grows.
+      int pos = 0;
+      while (pos < n) {
+        const int q = pos + lane;
+        bool fit = false;
+        if (q < n && q != i && q != j) {
+          int a0 = min(m0, S.bc0[q]), a1 = min(n0, S.br0[q]);
+          int a2 = max(m1, S.bc1[q]), a3 = max(n1, S.br1[q]);
+          int qx, qy, qw, qh;
+          extent(P, a0, a1, a2, a3, qx, qy, qw, qh);
+          fit = (qw <= ws) && (qh <= hs);
+        }
+        const uint32_t msk = __ballot_sync(0xffffffffu, fit);
+        if (msk) {
+          const int qq = pos + __ffs(msk) - 1;
+          m0 = min(m0, S.bc0[qq]);
+          n0 = min(n0, S.br0[qq]);
+          m1 = max(m1, S.bc1[qq]);
+          n1 = max(n1, S.br1[qq]);
+          sum += T[S.csz[qq]];
+          before_i += (qq < i) ? 1 : 0;
+          if (lane == 0) S.memb[qq] = 1;
+          pos = qq + 1;
+        } else {
+          pos += 32;
+        }
+      }
+      __syncwarp();
+      // (d) accept iff strictly faster (R8); remove members, append merged (R4)
+      if (T[s] < sum) {
+        int wpos = 0;
+        for (int base = 0; base < n; base += 32) {
+          const int q = base + lane;
+          bool keep = false;
+          int v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+          unsigned char vs = 0;
+          if (q < n) {
+            keep = !S.memb[q];
+            v0 = S.bc0[q]; v1 = S.br0[q]; v2 = S.bc1[q]; v3 = S.br1[q]; vs = S.csz[q];
+          }
+          const uint32_t km = __ballot_sync(0xffffffffu, keep);
+          __syncwarp();
+          if (keep) {
+            const int d = wpos + __popc(km & lanemask_lt());
+            S.bc0[d] = v0; S.br0[d] = v1; S.bc1[d] = v2; S.br1[d] = v3; S.csz[d] = vs;
+          }
+          if (q < n) S.memb[q] = 0;
+          wpos += __popc(km);
+          __syncwarp();
+        }
+        if (lane == 0) {
+          S.bc0[wpos] = m0; S.br0[wpos] = n0; S.bc1[wpos] = m1; S.br1[wpos] = n1;
+          S.csz[wpos] = (unsigned char)s;
+        }
+        __syncwarp();
+        n = wpos + 1;
+        i -= before_i;
+        again = true;
+      } else {
+        for (int q = lane; q < n; q += 32) S.memb[q] = 0;
+        __syncwarp();
+        i++;
+      }
+    }
+  }
+
+  // ---- R11 fallback + a4 placement (R10) into per-frame scratch ----------
+  long long est = 0;
+  for (int q = lane; q < n; q += 32) est += T[S.csz[q]];
+  est = warp_sum_i64(est);
+  int4* out = ws_win + (size_t)f * P.maxc;
+  if (n > 0 && est > T[P.full]) {
+    if (lane == 0) {
+      out[0] = make_int4(0, 0, P.full, 0);
+      ws_count[f] = 1;
+      for (int kk = 0; kk < P.k; kk++) ws_cls[(size_t)f * P.k + kk] = (kk == P.full) ? 1 : 0;
+    }
+    return;
+  }
+  for (int base = 0; base < n; base += 32) {
+    const int q = base + lane;
+    int s = -1, x = 0, y = 0;
+    if (q < n) {
+      s = S.csz[q];
+      int px0, py0, bw, bh;
+      extent(P, S.bc0[q], S.br0[q], S.bc1[q], S.br1[q], px0, py0, bw, bh);
+      x = min(max(px0 - (P.sw[s] - bw) / 2, 0), P.W - P.sw[s]);
+      y = min(max(py0 - (P.sh[s] - bh) / 2, 0), P.H - P.sh[s]);
+    }
+    int rank = 0;
+    for (int kk = 0; kk < P.k; kk++) {
+      const uint32_t mk = __ballot_sync(0xffffffffu, s == kk);
+      if (s == kk) rank = S.run[kk] + __popc(mk & lanemask_lt());
+      __syncwarp();
+      if (lane == 0) S.run[kk] += __popc(mk);
+      __syncwarp();
+    }
+    if (q < n) out[q] = make_int4(x, y, s, rank);
+  }
+  __syncwarp();
+  if (lane == 0) ws_count[f] = n;
+  for (int kk = lane; kk < P.k; kk += 32) ws_cls[(size_t)f * P.k + kk] = S.run[kk];
+}
+
+__global__ void __launch_bounds__(1024) plan_scan_kernel(int F, int k, int* __restrict__ ws_count,
+                                                         int* __restrict__ ws_cls, int* __restrict__ frame_off,
+                                                         int* __restrict__ class_count, int max_windows,
+                                                         int* __restrict__ d_status) {
+  __shared__ int tmp[40];
+  // frame CSR: copy counts then scan in place in frame_off
+  for (int f = threadIdx.x; f < F; f += blockDim.x) frame_off[f] = ws_count[f];
+  __syncthreads();
+  const int total = block_scan_global(frame_off, F, 1, tmp);
+  if (threadIdx.x == 0) {
+    frame_off[F] = total;
+    if (total > max_windows) set_status(d_status, MP_ERR_CAPACITY);
+  }
+  for (int kk = 0; kk < k; kk++) {
+    const int tot = block_scan_global(ws_cls + kk, F, k, tmp);
+    if (threadIdx.x == 0) class_count[kk] = tot;
+  }
+}
+
+__global__ void __launch_bounds__(256) plan_scatter_kernel(PlanArgs P, int F, const int4* __restrict__ ws_win,
+                                                           const int* __restrict__ ws_count,
+                                                           const int* __restrict__ ws_cls,
+                                                           const int* __restrict__ frame_off,
+                                                           mp_window* __restrict__ windows, int max_windows) {
+  const int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (f >= F) return;
+  const int n = ws_count[f];
+  const int base = frame_off[f];
+  for (int q = lane; q < n; q += 32) {
+    const int4 v = ws_win[(size_t)f * P.maxc + q];
+    const int idx = base + q;
+    if (idx >= max_windows) continue;
+    mp_window w;
+    w.frame = f;
+    w.x = v.x;
+    w.y = v.y;
+    w.w = P.sw[v.z];
+    w.h = P.sh[v.z];
+    w.size_idx = v.z;
+    w.slot = ws_cls[(size_t)f * P.k + v.z] + v.w;
+    windows[idx] = w;
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static bool build_plan_args(const mp_plan_params* p, PlanArgs* A, mp_status* err) {
+  *err = MP_ERR_INVALID;
+  if (!p || !p->sizes || !p->cost) return false;
+  if (p->W < 1 || p->H < 1 || p->W > 16384 || p->H > 16384) return false;
+  if (p->cell_w < 1 || p->cell_h < 1 || p->k < 1 || p->k > kMaxClasses) return false;
+  if (!(p->b_proxy == p->b_proxy)) return false;   // NaN threshold
+  int full = -1;
+  for (int i = 0; i < p->k; i++) {
+    const mp_size s = p->sizes[i];
+    if (s.w < 1 || s.h < 1 || s.w > p->W || s.h > p->H || p->cost[i] <= 0) return false;
+    if (s.w == p->W && s.h == p->H) full = i;
+    for (int j = 0; j < p->k; j++) {
+      if (j == i) continue;
+      if (p->sizes[j].w == s.w && p->sizes[j].h == s.h) return false;
+      const long long ai = (long long)s.w * s.h, aj = (long long)p->sizes[j].w * p->sizes[j].h;
+      if (ai < aj && !(p->cost[i] < p->cost[j])) return false;
+    }
+  }
+  if (full < 0) return false;   // the full frame is always in S (R14)
+  A->W = p->W;
+  A->H = p->H;
+  A->cw = p->cell_w;
+  A->ch = p->cell_h;
+  A->R = (p->H + p->cell_h - 1) / p->cell_h;
+  A->C = (p->W + p->cell_w - 1) / p->cell_w;
+  A->words = (A->C + 31) / 32;
+  A->k = p->k;
+  A->full = full;
+  A->b = p->b_proxy;
+  if ((long long)A->R * A->C > 16384) {
+    *err = MP_ERR_UNSUPPORTED;
+    return false;
+  }
+  A->maxc = A->R * ((A->C + 1) / 2);
+  for (int i = 0; i < kMaxClasses; i++) {
+    A->order[i] = i;
+    A->sw[i] = i < p->k ? p->sizes[i].w : 0;
+    A->sh[i] = i < p->k ? p->sizes[i].h : 0;
+    A->cost[i] = i < p->k ? p->cost[i] : 0;
+  }
+  // insertion sort of size indices by (area, w, h)
+  for (int a = 1; a < p->k; a++) {
+    int v = A->order[a], b = a - 1;
+    auto less = [&](int x, int y) {
+      long long ax = (long long)A->sw[x] * A->sh[x], ay = (long long)A->sw[y] * A->sh[y];
+      if (ax != ay) return ax < ay;
+      if (A->sw[x] != A->sw[y]) return A->sw[x] < A->sw[y];
+      return A->sh[x] < A->sh[y];
+    };
+    while (b >= 0 && less(v, A->order[b])) {
+      A->order[b + 1] = A->order[b];
+      b--;
+    }
+    A->order[b + 1] = v;
+  }
+  *err = MP_OK;
+  return true;
+}
+
+struct PlanWs {
+  size_t win_off, count_off, cls_off, total;
+};
+
+static PlanWs plan_ws_layout(const PlanArgs& A, int F) {
+  PlanWs L;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  L.win_off = 0;
+  L.count_off = al(L.win_off + sizeof(int4) * (size_t)F * A.maxc);
+  L.cls_off = al(L.count_off + sizeof(int) * (size_t)F);
+  L.total = al(L.cls_off + sizeof(int) * (size_t)F * A.k) + 256;
+  return L;
+}
+
+}  // namespace mpk
+
+using namespace mpk;
+
+extern "C" size_t mp_plan_workspace_size(const mp_plan_params* p, int32_t F) {
+  PlanArgs A;
+  mp_status err;
+  if (F < 0 || !build_plan_args(p, &A, &err)) return 0;
+  return plan_ws_layout(A, F).total;
+}
+
+extern "C" mp_status mp_plan_windows(const mp_plan_params* p, const float* d_scores, int32_t F,
+                                     uint32_t* d_mask, mp_window* d_windows, int32_t max_windows,
+                                     int32_t* d_frame_off, int32_t* d_class_count, int32_t* d_status,
+                                     void* d_ws, size_t ws_bytes, void* stream) {
+  PlanArgs A;
+  mp_status err;
+  if (!build_plan_args(p, &A, &err)) return err;
+  if (F < 0 || max_windows < 0 || !d_frame_off || !d_class_count || !d_status) return MP_ERR_INVALID;
+  if (F > 0 && !d_scores) return MP_ERR_INVALID;
+  if (max_windows > 0 && !d_windows) return MP_ERR_INVALID;
+  const PlanWs L = plan_ws_layout(A, F);
+  if (ws_bytes < L.total || (!d_ws && L.total > 0)) return MP_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned char* ws = (unsigned char*)d_ws;
+  int4* ws_win = (int4*)(ws + L.win_off);
+  int* ws_count = (int*)(ws + L.count_off);
+  int* ws_cls = (int*)(ws + L.cls_off);
+  if (F > 0) {
+    const size_t smem = plan_smem_bytes(A.R, A.words, A.maxc, nullptr, nullptr);
+    if (smem > 227 * 1024) return MP_ERR_UNSUPPORTED;
+    MP_CUDA_TRY(cudaFuncSetAttribute(plan_frames_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    plan_frames_kernel<<<F, kPlanThreads, smem, s>>>(A, d_scores, d_mask, ws_win, ws_count, ws_cls);
+    MP_CUDA_TRY(cudaGetLastError());
+  }
+  plan_scan_kernel<<<1, 1024, 0, s>>>(F, A.k, ws_count, ws_cls, d_frame_off, d_class_count, max_windows,
+                                      d_status);
+  MP_CUDA_TRY(cudaGetLastError());
+  if (F > 0) {
+    plan_scatter_kernel<<<(F + 7) / 8, 256, 0, s>>>(A, F, ws_win, ws_count, ws_cls, d_frame_off, d_windows,
+                                                    max_windows);
+    MP_CUDA_TRY(cudaGetLastError());
+  }
+  return MP_OK;
+}

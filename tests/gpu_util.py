@@ -1,0 +1,85 @@
+"""Helpers for the -m gpu parity tests: run the CUDA path (through the C-ABI
+binding) on numpy inputs and bring the results back as numpy."""
+import numpy as np
+import torch
+
+import paper_2103_14695_b200 as mp
+from paper_2103_14695_b200 import _binding as B
+
+DEV = torch.device("cuda:0")
+
+
+def gpu_plan(W, H, cw, ch, b, sizes, cost, scores, max_windows=None, want_mask=True):
+    scores = np.ascontiguousarray(scores, np.float32)
+    F = scores.shape[0]
+    p = B.PlanParams(W, H, sizes, cost, b, cw, ch)
+    R, C = p.grid
+    if max_windows is None:
+        max_windows = max(F * ((R * C + 1) // 2 + 1), 1)
+    win = torch.full((max(max_windows, 1), 7), -7, dtype=torch.int32, device=DEV)
+    fo = torch.full((F + 1,), -7, dtype=torch.int32, device=DEV)
+    cc = torch.full((len(sizes),), -7, dtype=torch.int32, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    mask = torch.full((max(F, 1), R, (C + 31) // 32), -7, dtype=torch.int32, device=DEV) if want_mask else None
+    ws = torch.empty(max(B.mp_plan_workspace_size(p, F), 1), dtype=torch.uint8, device=DEV)
+    sc = torch.from_numpy(scores).to(DEV) if F else torch.zeros((1, R, C), device=DEV)
+    B.mp_plan_windows(p, sc, F, mask if F else None, win if max_windows else None, fo, cc, st, ws)
+    torch.cuda.synchronize()
+    n = int(fo[F].item())
+    return dict(status=int(st.item()), windows=win[:min(n, max_windows)].cpu().numpy(), frame_off=fo.cpu().numpy(),
+                class_count=cc.cpu().numpy(),
+                mask=(mask[:F].cpu().numpy().view(np.uint32) if want_mask else None))
+
+
+def gpu_gather(frames_np_or_t, pitch, W, H, windows, sizes, out_dims, caps, fmt=mp.MP_OUT_F32_NCHW):
+    if isinstance(frames_np_or_t, torch.Tensor):
+        fr = frames_np_or_t
+    else:
+        fr = torch.from_numpy(np.stack(frames_np_or_t)).to(DEV)
+    F = fr.shape[0]
+    win = np.asarray(windows, np.int32).reshape(-1, 7)
+    # a CSR over frames consistent with the (frame-sorted) window list
+    fo = np.searchsorted(win[:, 0], np.arange(F + 1), side="left").astype(np.int32) if len(win) else \
+        np.zeros(F + 1, np.int32)
+    fo[F] = len(win)
+    wt = torch.from_numpy(win if len(win) else np.zeros((1, 7), np.int32)).to(DEV)
+    fot = torch.from_numpy(fo).to(DEV)
+    outs = []
+    for q, (ow, oh) in enumerate(out_dims):
+        if fmt == mp.MP_OUT_F32_NCHW:
+            outs.append(torch.full((caps[q], 3, oh, ow), -1.0, dtype=torch.float32, device=DEV))
+        else:
+            outs.append(torch.zeros((caps[q], oh, ow, 3), dtype=torch.uint8, device=DEV))
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ws = torch.empty(B.mp_gather_workspace_size(caps), dtype=torch.uint8, device=DEV)
+    ptrs = mp.WindowPipeline.frame_ptrs(fr)
+    B.mp_gather_resize(ptrs, pitch, W, H, F, wt, fot, sizes, out_dims, outs, fmt, st, ws)
+    torch.cuda.synchronize()
+    return int(st.item()), [o.cpu().numpy() for o in outs]
+
+
+def boxes_to_t(boxes):
+    if len(boxes) == 0:
+        return torch.zeros((1, 6), dtype=torch.float32, device=DEV)
+    return torch.from_numpy(np.ascontiguousarray(boxes).view(np.float32).reshape(-1, 6).copy()).to(DEV)
+
+
+def gpu_remap_nms(boxes, win_box_off, windows, frame_off, out_dims, W, H, score_thr, iou_thr, max_out=None):
+    F = len(frame_off) - 1
+    n_box = len(boxes)
+    max_out = max(n_box, 1) if max_out is None else max_out
+    win = np.asarray(windows, np.int32).reshape(-1, 7)
+    wt = torch.from_numpy(win if len(win) else np.zeros((1, 7), np.int32)).to(DEV)
+    out = torch.full((max(max_out, 1), 6), -3.0, dtype=torch.float32, device=DEV)
+    src = torch.full((max(max_out, 1),), -3, dtype=torch.int32, device=DEV)
+    ofo = torch.full((F + 1,), -3, dtype=torch.int32, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    bx = boxes_to_t(boxes)
+    ws = torch.empty(B.mp_remap_nms_workspace_size(F, max(n_box, 1)), dtype=torch.uint8, device=DEV)
+    B.mp_remap_nms(bx, torch.from_numpy(np.asarray(win_box_off, np.int32)).to(DEV), wt,
+                   torch.from_numpy(np.asarray(frame_off, np.int32)).to(DEV), F, out_dims, W, H, score_thr,
+                   iou_thr, out[:max(max_out, 1)] if max_out else out, src, ofo, st, ws)
+    torch.cuda.synchronize()
+    n = min(int(ofo[F].item()), max_out)
+    return dict(status=int(st.item()), boxes=out[:n].cpu().numpy(), src=src[:n].cpu().numpy(),
+                frame_off=ofo.cpu().numpy())

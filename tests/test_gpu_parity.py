@@ -1,0 +1,335 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs.  Bit-exact for masks, windows, slots, CSR offsets, NMS
+keep-lists and remapped coordinates; f32 pixels within 1e-3 absolute; u8
+pixels within 1 LSB (SURVEY.md §8(c) tolerances, BASELINE.json north_star)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle as O  # noqa: E402
+from workloads import synth as S  # noqa: E402
+
+F32_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def G():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import gpu_util
+    return gpu_util
+
+
+def _plan_both(G, W, H, cw, ch, b, sizes, cost, scores, max_windows=None):
+    ref = O.plan_windows(W, H, cw, ch, b, sizes, cost, scores, max_windows=max_windows)
+    got = G.gpu_plan(W, H, cw, ch, b, sizes, cost, scores, max_windows=max_windows)
+    return ref, got
+
+
+def _assert_plan_equal(ref, got):
+    assert got["status"] == ref["status"]
+    assert np.array_equal(got["frame_off"], ref["frame_off"])
+    assert np.array_equal(got["class_count"], ref["class_count"])
+    assert np.array_equal(got["windows"], ref["windows"])
+    assert np.array_equal(got["mask"], ref["mask"])
+
+
+# --------------------------------------------------------------------------- a1-a4
+@pytest.mark.parametrize("name,frames", [("c1_540p", 30), ("c2_1080p_sparse", 240), ("c3_1080p_dense", 120),
+                                         ("c4_4k_drone", 24)])
+def test_plan_parity_configs(G, name, frames):
+    cfg = S.CONFIGS[name]
+    scene = S.make_scene(cfg, 1, frames)
+    scores = S.score_grids(cfg, 1, scene)
+    ref, got = _plan_both(G, cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores)
+    _assert_plan_equal(ref, got)
+
+
+@pytest.mark.parametrize("b", S.B_SWEEP)
+def test_plan_parity_threshold_sweep(G, b):
+    """configs[4]: 1080p clips of mixed density, B swept over 0.1..0.9."""
+    cfg = S.CONFIGS["c5_1080p_clips"]
+    for clip in (3, 17, 404):
+        scene = S.make_scene(cfg, clip, 40)
+        scores = S.score_grids(cfg, clip, scene)
+        ref, got = _plan_both(G, cfg.W, cfg.H, 32, 32, b, cfg.sizes, cfg.cost, scores)
+        _assert_plan_equal(ref, got)
+
+
+def _adversarial_grids(R, C):
+    g = {}
+    g["empty"] = np.zeros((R, C), np.float32)
+    g["full"] = np.ones((R, C), np.float32)
+    g["checker"] = ((np.add.outer(np.arange(R), np.arange(C)) % 2) == 0).astype(np.float32)
+    g["stripes_h"] = np.repeat((np.arange(R) % 2 == 0)[:, None], C, 1).astype(np.float32)
+    g["stripes_v"] = np.repeat((np.arange(C) % 2 == 0)[None, :], R, 0).astype(np.float32)
+    g["single_row"] = np.zeros((R, C), np.float32); g["single_row"][R // 2] = 1
+    g["single_col"] = np.zeros((R, C), np.float32); g["single_col"][:, C // 2] = 1
+    g["edges"] = np.zeros((R, C), np.float32); g["edges"][0, :] = 1; g["edges"][-1, :] = 1
+    g["edges"][:, 0] = 1; g["edges"][:, -1] = 1
+    g["corners"] = np.zeros((R, C), np.float32)
+    for r, c in ((0, 0), (0, C - 1), (R - 1, 0), (R - 1, C - 1)):
+        g["corners"][r, c] = 1
+    sp = np.zeros((R, C), np.float32)
+    sp[::2, :] = 1
+    sp[1::4, 0] = 1
+    sp[3::4, -1] = 1
+    g["spiral_snake"] = sp
+    rng = np.random.default_rng(11)
+    for d in (0.02, 0.1, 0.3, 0.5, 0.7, 0.95):
+        g[f"rand{d}"] = (rng.random((R, C)) < d).astype(np.float32)
+    return g
+
+
+@pytest.mark.parametrize("W,H,cw,ch,sizes", [
+    (1920, 1080, 32, 32, ((256, 256), (512, 512), (1920, 1080))),
+    (3840, 2160, 32, 32, ((128, 128), (256, 256), (512, 512), (3840, 2160))),
+    (200, 100, 20, 10, ((64, 32), (32, 64), (200, 100))),
+    (1000, 700, 37, 29, ((111, 87), (300, 200), (299, 201), (1000, 700))),
+    (3072, 3072, 32, 32, ((256, 256), (1024, 512), (3072, 3072))),       # 96 x 96 cells
+    (8192, 96, 16, 16, ((64, 32), (8192, 96))),                          # 512 columns x 6 rows
+    (40, 5000, 8, 8, ((16, 64), (40, 5000))),                            # 5 columns x 625 rows
+])
+def test_plan_parity_adversarial(G, W, H, cw, ch, sizes):
+    R, C = -(-H // ch), -(-W // cw)
+    cost = [-(-w // 32) * -(-h // 32) + 16 for (w, h) in sizes]
+    grids = _adversarial_grids(R, C)
+    scores = np.stack(list(grids.values())).astype(np.float32)
+    ref, got = _plan_both(G, W, H, cw, ch, 0.5, sizes, cost, scores)
+    _assert_plan_equal(ref, got)
+
+
+def test_plan_parity_nan_and_ties(G):
+    cfg = S.CONFIGS["c2_1080p_sparse"]
+    rng = np.random.default_rng(3)
+    s = rng.random((16, 34, 60)).astype(np.float32)
+    s[0, :3, :] = np.nan
+    s[1, :, :] = np.float32(0.5)          # exactly B: never positive (strict >)
+    s[2, 5:9, 10:20] = np.float32(0.5000001)
+    s[3] = np.inf
+    s[4] = -np.inf
+    ref, got = _plan_both(G, cfg.W, cfg.H, 32, 32, 0.5, cfg.sizes, cfg.cost, s)
+    _assert_plan_equal(ref, got)
+
+
+def test_plan_capacity_and_zero_frames(G):
+    cfg = S.CONFIGS["c2_1080p_sparse"]
+    scene = S.make_scene(cfg, 2, 20)
+    scores = S.score_grids(cfg, 2, scene)
+    ref, got = _plan_both(G, cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores, max_windows=5)
+    assert got["status"] == O.ERR_CAPACITY == ref["status"]
+    assert np.array_equal(got["frame_off"], ref["frame_off"])
+    assert np.array_equal(got["windows"], ref["windows"][:5])
+    z = G.gpu_plan(cfg.W, cfg.H, 32, 32, 0.5, cfg.sizes, cfg.cost, np.zeros((0, 34, 60), np.float32))
+    assert z["status"] == 0 and z["frame_off"].tolist() == [0] and z["class_count"].tolist() == [0, 0, 0]
+
+
+def test_plan_unsupported_grid(G):
+    import paper_2103_14695_b200 as mp
+    with pytest.raises(mp.MPError) as e:     # 128 x 128 cells: beyond one CTA's shared memory
+        G.gpu_plan(4096, 4096, 32, 32, 0.5, [(256, 256), (4096, 4096)], [80, 16400],
+                   np.zeros((1, 128, 128), np.float32))
+    assert e.value.code == mp.MP_ERR_UNSUPPORTED
+
+
+def test_plan_invalid_params_raise(G):
+    import paper_2103_14695_b200 as mp
+    s = np.zeros((1, 6, 8), np.float32)
+    with pytest.raises(mp.MPError) as e:
+        G.gpu_plan(256, 192, 32, 32, 0.5, [(64, 64)], [20], s)        # full frame missing (R14)
+    assert e.value.code == mp.MP_ERR_INVALID
+    with pytest.raises(mp.MPError):
+        G.gpu_plan(256, 192, 32, 32, 0.5, [(64, 64), (256, 192)], [90, 64], s)   # non-monotone cost
+
+
+# --------------------------------------------------------------------------- a5
+def _frames(cfg, clip, F):
+    return [S.frame_pixels_np(S.frame_seed(clip, f), cfg.H, cfg.pitch) for f in range(F)]
+
+
+def _gather_compare(G, frames, pitch, W, H, windows, sizes, out_dims, fmt):
+    win = np.asarray(windows, np.int32).reshape(-1, 7)
+    caps = [int((win[:, 5] == q).sum()) for q in range(len(sizes))]
+    st_r, ref = O.gather_resize(frames, pitch, W, H, win, sizes, out_dims, caps,
+                                O.F32_NCHW if fmt == 0 else O.U8_NHWC)
+    st_g, got = G.gpu_gather(frames, pitch, W, H, win, sizes, out_dims, caps, fmt)
+    assert st_g == st_r == 0
+    for q in range(len(sizes)):
+        if caps[q] == 0:
+            continue
+        if fmt == 0:
+            err = np.abs(got[q].astype(np.float64) - ref[q]).max()
+            assert err <= F32_TOL, (q, err)
+        else:
+            d = np.abs(got[q].astype(np.int32) - ref[q].astype(np.int32))
+            assert d.max() <= 1, (q, d.max())
+    return ref, got
+
+
+@pytest.mark.parametrize("fmt", [0, 1])
+@pytest.mark.parametrize("name,frames", [("c1_540p", 30), ("c2_1080p_sparse", 24), ("c4_4k_drone", 2)])
+def test_gather_parity_configs(G, name, frames, fmt):
+    cfg = S.CONFIGS[name]
+    scene = S.make_scene(cfg, 4, frames)
+    scores = S.score_grids(cfg, 4, scene)
+    plan = O.plan_windows(cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores)
+    _gather_compare(G, _frames(cfg, 4, frames), cfg.pitch, cfg.W, cfg.H, plan["windows"], cfg.sizes,
+                    cfg.out_dims, fmt)
+
+
+@pytest.mark.parametrize("fmt", [0, 1])
+@pytest.mark.parametrize("scale", [1.0, 0.5, 0.7, 1.37, 0.26, 0.9999])
+def test_gather_parity_scales_and_edges(G, scale, fmt):
+    """Odd output widths (scalar stores), upscale, dyadic, near-identity, strong
+    downscale, and windows touching every frame edge."""
+    W, H = 640, 360
+    pitch = (3 * W + 15) // 16 * 16
+    sizes = [(96, 64), (250, 130), (640, 360)]
+    out_dims = [(max(1, int(np.floor(scale * w + 0.5))), max(1, int(np.floor(scale * h + 0.5)))) for w, h in sizes]
+    frames = [S.frame_pixels_np(S.frame_seed(99, f), H, pitch) for f in range(3)]
+    rng = np.random.default_rng(int(scale * 1000))
+    win = []
+    for f in range(3):
+        for q, (w, h) in enumerate(sizes):
+            xs = sorted({0, W - w, int(rng.integers(0, W - w + 1))})
+            ys = sorted({0, H - h, int(rng.integers(0, H - h + 1))})
+            for x in xs:
+                for y in ys:
+                    win.append([f, x, y, w, h, q, 0])
+    win = np.array(win, np.int32)
+    for q in range(3):
+        sel = np.nonzero(win[:, 5] == q)[0]
+        win[sel, 6] = np.arange(len(sel))
+    ref, got = _gather_compare(G, frames, pitch, W, H, win, sizes, out_dims, fmt)
+    if scale == 1.0:   # exact crop copy, bit-exact
+        for q in range(3):
+            if fmt == 0:
+                assert np.array_equal(got[q], ref[q])
+            else:
+                assert np.array_equal(got[q], ref[q])
+
+
+def test_gather_capacity_and_invalid(G):
+    W, H = 256, 128
+    pitch = 3 * W
+    frames = [S.frame_pixels_np(5, H, pitch)]
+    win = np.array([[0, 0, 0, 64, 64, 0, 0], [0, 64, 0, 64, 64, 0, 1]], np.int32)
+    st, got = G.gpu_gather(frames, pitch, W, H, win, [(64, 64), (256, 128)], [(32, 32), (128, 64)], [1, 1])
+    assert st == O.ERR_CAPACITY
+    ref_st, ref = O.gather_resize(frames, pitch, W, H, win[:1], [(64, 64), (256, 128)], [(32, 32), (128, 64)],
+                                  [1, 1])
+    assert np.abs(got[0] - ref[0]).max() <= F32_TOL
+    bad = np.array([[0, 200, 0, 64, 64, 0, 0]], np.int32)     # outside the frame
+    st, _ = G.gpu_gather(frames, pitch, W, H, bad, [(64, 64), (256, 128)], [(32, 32), (128, 64)], [1, 1])
+    assert st == O.ERR_INVALID
+
+
+# --------------------------------------------------------------------------- a6-a7
+def _nms_compare(G, boxes, wbo, windows, frame_off, cfg_out_dims, W, H, score_thr, iou_thr):
+    ref = O.remap_nms(boxes, wbo, windows, frame_off, cfg_out_dims, W, H, score_thr, iou_thr)
+    got = G.gpu_remap_nms(boxes, wbo, windows, frame_off, cfg_out_dims, W, H, score_thr, iou_thr)
+    assert got["status"] == ref["status"] == 0
+    assert np.array_equal(got["frame_off"], ref["frame_off"])
+    assert np.array_equal(got["src"], ref["src"])
+    assert np.array_equal(got["boxes"].view(np.uint32), ref["boxes"].view(np.float32).reshape(-1, 6).view(np.uint32))
+    return ref, got
+
+
+@pytest.mark.parametrize("name,frames", [("c1_540p", 30), ("c2_1080p_sparse", 200), ("c3_1080p_dense", 60),
+                                         ("c4_4k_drone", 12)])
+def test_remap_nms_parity_configs(G, name, frames):
+    cfg = S.CONFIGS[name]
+    scene = S.make_scene(cfg, 5, frames)
+    scores = S.score_grids(cfg, 5, scene)
+    plan = O.plan_windows(cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores)
+    boxes, wbo = S.standin_boxes(cfg, 5, scene, plan["windows"], extra_edge_cases=True)
+    _nms_compare(G, boxes, wbo, plan["windows"], plan["frame_off"], cfg.out_dims, cfg.W, cfg.H, cfg.score_thr,
+                 cfg.iou_thr)
+
+
+@pytest.mark.parametrize("n", [0, 1, 63, 64, 65, 511, 512, 513, 1023, 1024, 1025, 2048])
+def test_nms_parity_frame_sizes(G, n):
+    """Tie-heavy single frames around every tier boundary (small <= 512,
+    bitmask <= 1024, on-the-fly <= 2048)."""
+    rng = np.random.default_rng(n)
+    rows = np.zeros(n, O.BOX_DTYPE)
+    xy = rng.integers(0, 300, (n, 2)).astype(np.float32)
+    wh = rng.integers(4, 60, (n, 2)).astype(np.float32)
+    rows["x1"], rows["y1"] = xy[:, 0], xy[:, 1]
+    rows["x2"], rows["y2"] = xy[:, 0] + wh[:, 0], xy[:, 1] + wh[:, 1]
+    rows["score"] = rng.choice(np.array([0.3, 0.5, 0.9], np.float32), n)
+    rows["cls"] = rng.integers(0, 3, n)
+    win = np.array([[0, 0, 0, 512, 512, 0, 0]], np.int32)
+    for thr in (0.5, 0.375):
+        _nms_compare(G, rows, [0, n], win, [0, 1], [(384, 384)], 512, 512, 0.25, thr)
+
+
+def test_nms_parity_empty_frames_and_windows(G):
+    cfg = S.CONFIGS["c2_1080p_sparse"]
+    win = np.array([[1, 0, 0, 256, 256, 0, 0], [1, 100, 100, 256, 256, 0, 1], [3, 0, 0, 512, 512, 1, 0]], np.int32)
+    frame_off = np.array([0, 0, 2, 2, 3, 3], np.int32)       # frames 0, 2, 4 have no windows
+    rows = np.zeros(4, O.BOX_DTYPE)
+    rows[0] = (1, 1, 50, 50, 0.9, 0)
+    rows[1] = (10, 10, 60, 60, 0.8, 0)
+    rows[2] = (0, 0, 100, 100, 0.7, 2)
+    rows[3] = (5, 5, 6, 6, 0.1, 1)
+    wbo = np.array([0, 2, 2, 4], np.int32)                     # window 1 has no boxes
+    _nms_compare(G, rows, wbo, win, frame_off, cfg.out_dims, cfg.W, cfg.H, 0.25, 0.5)
+
+
+def test_nms_capacity(G):
+    rows = np.zeros(5, O.BOX_DTYPE)
+    for i in range(5):
+        rows[i] = (i * 20, 0, i * 20 + 10, 10, 0.9, 0)
+    win = np.array([[0, 0, 0, 256, 256, 0, 0]], np.int32)
+    got = G.gpu_remap_nms(rows, [0, 5], win, [0, 1], [(256, 256)], 256, 256, 0.25, 0.5, max_out=3)
+    assert got["status"] == O.ERR_CAPACITY and got["frame_off"].tolist() == [0, 5]
+    ref = O.remap_nms(rows, [0, 5], win, [0, 1], [(256, 256)], 256, 256, 0.25, 0.5)
+    assert np.array_equal(got["src"], ref["src"][:3])
+
+
+# --------------------------------------------------------------------------- full size (bench launch config)
+def test_full_size_bench_config_parity(G):
+    """configs[1] at full size (1800 frames, 1080p), through WindowPipeline as
+    bench.py runs it: every window/mask/slot/kept box compared exactly; pixels
+    compared on a seeded sample of windows (the oracle computes each one)."""
+    import paper_2103_14695_b200 as mp
+    cfg = S.CONFIGS["c2_1080p_sparse"]
+    F = cfg.frames
+    scene = S.make_scene(cfg, 0, F)
+    scores = S.score_grids(cfg, 0, scene)
+    ref = O.plan_windows(cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores)
+    pipe = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
+                             cfg.iou_thr, device=G.DEV, want_mask=True)
+    caps = [int(c) for c in ref["class_count"]]
+    boxes, wbo = S.standin_boxes(cfg, 0, scene, ref["windows"])
+    pipe.reserve(F, len(ref["windows"]) + 64, caps=caps, max_boxes=len(boxes))
+    frames = S.frame_pixels_torch([S.frame_seed(0, f) for f in range(F)], cfg.H, cfg.pitch, device=G.DEV)
+    pipe.plan(torch.from_numpy(scores).to(G.DEV))
+    pipe.gather(mp.WindowPipeline.frame_ptrs(frames))
+    pipe.merge(G.boxes_to_t(boxes), torch.from_numpy(wbo).to(G.DEV))
+    torch.cuda.synchronize()
+    pipe.check_status()
+    n = len(ref["windows"])
+    assert np.array_equal(pipe.frame_off.cpu().numpy(), ref["frame_off"])
+    assert np.array_equal(pipe.windows[:n].cpu().numpy(), ref["windows"])
+    assert np.array_equal(pipe.mask.cpu().numpy().view(np.uint32), ref["mask"])
+    r = O.remap_nms(boxes, wbo, ref["windows"], ref["frame_off"], cfg.out_dims, cfg.W, cfg.H, cfg.score_thr,
+                    cfg.iou_thr)
+    nk = int(pipe.nms_frame_off[F].item())
+    assert np.array_equal(pipe.nms_src[:nk].cpu().numpy(), r["src"])
+    assert np.array_equal(pipe.nms_out[:nk].cpu().numpy().view(np.uint32),
+                          r["boxes"].view(np.float32).reshape(-1, 6).view(np.uint32))
+    rng = np.random.default_rng(1234)
+    sample = rng.choice(n, size=min(60, n), replace=False)
+    for wi in sample:
+        w = ref["windows"][wi].copy()
+        f, q, slot = int(w[0]), int(w[5]), int(w[6])
+        fr = S.frame_pixels_np(S.frame_seed(0, f), cfg.H, cfg.pitch)
+        one = w.copy(); one[0] = 0; one[6] = 0
+        caps1 = [1 if qq == q else 0 for qq in range(len(cfg.sizes))]
+        st, o = O.gather_resize([fr], cfg.pitch, cfg.W, cfg.H, one[None], cfg.sizes, cfg.out_dims, caps1)
+        got = pipe.outs[q][slot].cpu().numpy()
+        assert np.abs(got - o[q][0]).max() <= F32_TOL, (wi, np.abs(got - o[q][0]).max())
