@@ -22,9 +22,9 @@ constexpr int kGatherThreads = (kConsumerWarps + 1) * 32;
 constexpr int kStages = 3;
 constexpr int kHdrBytes = 64;
 constexpr int kMaxTW = 256;
-constexpr int kMaxTR = 64;
+constexpr int kMaxTR = 128;
 constexpr int kTapBytes = kMaxTW * 8 + kMaxTR * 16;
-constexpr int kStageDataBudget = 24 * 1024;
+constexpr int kStageDataBudget = 32 * 1024;
 
 struct GatherArgs {
   int k, W, H, pitch, F, fmt, stage_bytes;
@@ -203,6 +203,11 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(GatherArgs A, co
   }
 
   // ===================== consumer warps =====================
+  // Thread <-> one output column of the tile (consecutive lanes = consecutive
+  // columns: conflict-free byte loads, coalesced stores) and a contiguous block
+  // of rows.  Separable evaluation: the horizontal lerp of a staged source row
+  // is computed once and reused by the next output row that taps it.
+  const int ctid = tid;   // 0 .. 32*kConsumerWarps-1
   for (int i = 0;; i++) {
     const int t = blockIdx.x + i * G;
     if (t >= T) break;
@@ -215,52 +220,72 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(GatherArgs A, co
       const int4* yt = reinterpret_cast<const int4*>(stage + kHdrBytes + kMaxTW * 8);
       const unsigned char* data = stage + kHdrBytes + kTapBytes;
       const int q = hdr->k, rows = hdr->rows, cols = hdr->cols;
-      const int ow = A.ow[q], oh = A.oh[q];
-      const int nseg = (cols + 31) >> 5;
-      const int nitems = rows * nseg;
-      int row = wid / nseg, seg = wid - (wid / nseg) * nseg;
-      for (int it = wid; it < nitems; it += kConsumerWarps) {
-        const int col = seg * 32 + lane;
-        if (col < cols) {
-          const int2 x = xt[col];
-          const int off = x.x & 0xFFFFF, dx = x.x >> 20;
-          const float lx = __int_as_float(x.y);
-          const int4 y = yt[row];
-          const unsigned char* p0 = data + y.x + off;
-          const unsigned char* p1 = data + y.y + off;
-          const float ly = __int_as_float(y.z);
-          float v[3];
-#pragma unroll
-          for (int c = 0; c < 3; c++) {
-            const float a = u8f(p0[c]), b = u8f(p0[dx + c]);
-            const float e = u8f(p1[c]), g = u8f(p1[dx + c]);
-            const float top = fmaf(lx, b - a, a);
-            const float bot = fmaf(lx, g - e, e);
-            v[c] = fmaf(ly, bot - top, top);
-          }
-          const int oy = hdr->oy0 + row, ox = hdr->ox0 + col;
-          if (FMT == MP_OUT_F32_NCHW) {
-            float* o = reinterpret_cast<float*>(A.out[q]);
-            const size_t plane = (size_t)oh * ow;
-            const size_t base = (size_t)hdr->slot * 3 * plane + (size_t)oy * ow + ox;
-            __stcs(o + base, v[0]);
-            __stcs(o + base + plane, v[1]);
-            __stcs(o + base + 2 * plane, v[2]);
-          } else {
-            uint8_t* o = reinterpret_cast<uint8_t*>(A.out[q]);
-            const size_t base = (((size_t)hdr->slot * oh + oy) * ow + ox) * 3;
-#pragma unroll
-            for (int c = 0; c < 3; c++) {
-              int r = __float2int_rd(v[c] + 0.5f);   // R16 round half up
-              r = min(max(r, 0), 255);
-              o[base + c] = (uint8_t)r;
+      const int nph = max(1, (32 * kConsumerWarps) / cols);
+      const int ph = ctid / cols, c = ctid - ph * cols;
+      if (ph < nph) {
+        const int rpp = (rows + nph - 1) / nph;
+        const int rb0 = ph * rpp, rb1 = min(rows, rb0 + rpp);
+        const int2 x = xt[c];
+        const unsigned char* base = data + (x.x & 0xFFFFF);
+        const int dx = x.x >> 20;
+        const float lx = __int_as_float(x.y);
+        const int ow = A.ow[q], oh = A.oh[q];
+        int ra = -1, rb = -1;
+        float ha0 = 0.f, ha1 = 0.f, ha2 = 0.f, hb0 = 0.f, hb1 = 0.f, hb2 = 0.f;
+        auto hlerp = [&](int rowoff, float& h0, float& h1, float& h2) {
+          const unsigned char* p = base + rowoff;
+          const float a0 = u8f(p[0]), a1 = u8f(p[1]), a2 = u8f(p[2]);
+          const float b0 = u8f(p[dx]), b1 = u8f(p[dx + 1]), b2 = u8f(p[dx + 2]);
+          h0 = fmaf(lx, b0 - a0, a0);
+          h1 = fmaf(lx, b1 - a1, a1);
+          h2 = fmaf(lx, b2 - a2, a2);
+        };
+        if (FMT == MP_OUT_F32_NCHW) {
+          const size_t plane = (size_t)oh * ow;
+          float* o = reinterpret_cast<float*>(A.out[q]) + (size_t)hdr->slot * 3 * plane +
+                     (size_t)(hdr->oy0 + rb0) * ow + hdr->ox0 + c;
+          for (int r = rb0; r < rb1; r++) {
+            const int4 y = yt[r];
+            if (y.x != ra) {
+              if (y.x == rb) { ha0 = hb0; ha1 = hb1; ha2 = hb2; }
+              else hlerp(y.x, ha0, ha1, ha2);
+              ra = y.x;
             }
+            if (y.y != rb) {
+              if (y.y == ra) { hb0 = ha0; hb1 = ha1; hb2 = ha2; }
+              else hlerp(y.y, hb0, hb1, hb2);
+              rb = y.y;
+            }
+            const float ly = __int_as_float(y.z);
+            __stcs(o, fmaf(ly, hb0 - ha0, ha0));
+            __stcs(o + plane, fmaf(ly, hb1 - ha1, ha1));
+            __stcs(o + 2 * plane, fmaf(ly, hb2 - ha2, ha2));
+            o += ow;
           }
-        }
-        seg += kConsumerWarps;
-        while (seg >= nseg) {
-          seg -= nseg;
-          row++;
+        } else {
+          uint8_t* o = reinterpret_cast<uint8_t*>(A.out[q]) +
+                       (((size_t)hdr->slot * oh + hdr->oy0 + rb0) * ow + hdr->ox0 + c) * 3;
+          for (int r = rb0; r < rb1; r++) {
+            const int4 y = yt[r];
+            if (y.x != ra) {
+              if (y.x == rb) { ha0 = hb0; ha1 = hb1; ha2 = hb2; }
+              else hlerp(y.x, ha0, ha1, ha2);
+              ra = y.x;
+            }
+            if (y.y != rb) {
+              if (y.y == ra) { hb0 = ha0; hb1 = ha1; hb2 = ha2; }
+              else hlerp(y.y, hb0, hb1, hb2);
+              rb = y.y;
+            }
+            const float ly = __int_as_float(y.z);
+            const float v[3] = {fmaf(ly, hb0 - ha0, ha0), fmaf(ly, hb1 - ha1, ha1), fmaf(ly, hb2 - ha2, ha2)};
+#pragma unroll
+            for (int ch = 0; ch < 3; ch++) {
+              int rr = __float2int_rd(v[ch] + 0.5f);   // R16 round half up
+              o[ch] = (uint8_t)min(max(rr, 0), 255);
+            }
+            o += (size_t)ow * 3;
+          }
         }
       }
     }
@@ -325,13 +350,11 @@ static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_si
     A->h[q] = h;
     A->ow[q] = ow;
     A->oh[q] = oh;
-    // tile width: <= 256 output columns, split evenly; height ~3K pixels per tile
-    int nct = (ow + kMaxTW - 1) / kMaxTW;
-    int TW = (ow + nct - 1) / nct;
-    TW = (TW + 3) & ~3;
-    if (TW > kMaxTW) TW = kMaxTW;
-    int TR = 3072 / TW;
-    if (TR < 1) TR = 1;
+    // tile width: a power of two <= 256 (so 256 consumer threads split into
+    // whole column phases), height so a tile is ~4K output pixels
+    int TW = 256;
+    while (TW > 32 && TW > ow) TW >>= 1;
+    int TR = 4096 / TW;
     if (TR > kMaxTR) TR = kMaxTR;
     long long dat = class_stage_data(w, h, ow, oh, TW, TR);
     while (dat > kStageDataBudget && TR > 1) {
@@ -339,7 +362,7 @@ static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_si
       dat = class_stage_data(w, h, ow, oh, TW, TR);
     }
     while (dat > kStageDataBudget && TW > 32) {
-      TW = ((TW / 2) + 3) & ~3;
+      TW >>= 1;
       dat = class_stage_data(w, h, ow, oh, TW, TR);
     }
     if (dat > 4 * kStageDataBudget) return false;   // > 32x downscale: unsupported
