@@ -114,8 +114,9 @@ mp_status mp_plan_windows(const mp_plan_params* p, const float* d_scores, int32_
                           int32_t* d_frame_off, int32_t* d_class_count, int32_t* d_status,
                           void* d_ws, size_t ws_bytes, void* stream);
 
-/* Bytes of scratch mp_gather_resize needs (0 on invalid params). */
-size_t mp_gather_workspace_size(int32_t k, const int32_t* out_cap);
+/* Bytes of scratch mp_gather_resize needs for k size classes with output
+ * dims out_dims[k] and batch capacities out_cap[k] (0 on invalid params). */
+size_t mp_gather_workspace_size(int32_t k, const mp_size* out_dims, const int32_t* out_cap);
 
 /*
  * mp_gather_resize — step a5: gather every window's crop from its full

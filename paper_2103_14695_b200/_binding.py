@@ -56,7 +56,7 @@ def _load():
     L.mp_plan_windows.restype = C.c_int
     L.mp_plan_windows.argtypes = [C.POINTER(mp_plan_params), vp, i32, vp, vp, i32, vp, vp, vp, vp, sz, vp]
     L.mp_gather_workspace_size.restype = sz
-    L.mp_gather_workspace_size.argtypes = [i32, vp]
+    L.mp_gather_workspace_size.argtypes = [i32, vp, vp]
     L.mp_gather_resize.restype = C.c_int
     L.mp_gather_resize.argtypes = [vp, i32, i32, i32, i32, vp, vp, i32, vp, vp, vp, vp, C.c_int, vp, vp, sz, vp]
     L.mp_remap_nms_workspace_size.restype = sz
@@ -157,9 +157,9 @@ def mp_plan_windows(params: PlanParams, scores, F, mask, windows, frame_off, cla
         raise MPError(st, "mp_plan_windows")
 
 
-def mp_gather_workspace_size(out_cap: Sequence[int]) -> int:
+def mp_gather_workspace_size(out_dims: Sequence, out_cap: Sequence[int]) -> int:
     cap = (C.c_int32 * len(out_cap))(*[int(c) for c in out_cap])
-    return int(_lib.mp_gather_workspace_size(len(out_cap), cap))
+    return int(_lib.mp_gather_workspace_size(len(out_cap), _sizes(out_dims), cap))
 
 
 def mp_gather_resize(frame_ptrs, pitch, W, H, F, windows, frame_off, sizes, out_dims, outs, fmt, status, ws,

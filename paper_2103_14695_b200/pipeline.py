@@ -62,7 +62,7 @@ class WindowPipeline:
                     self.outs.append(torch.empty((self.caps[q], 3, oh, ow), dtype=torch.float32, device=dev))
                 else:
                     self.outs.append(torch.empty((self.caps[q], oh, ow, 3), dtype=torch.uint8, device=dev))
-            self.gather_ws = torch.empty(max(B.mp_gather_workspace_size(self.caps), 1), dtype=torch.uint8,
+            self.gather_ws = torch.empty(max(B.mp_gather_workspace_size(self.out_dims, self.caps), 1), dtype=torch.uint8,
                                          device=dev)
         if max_boxes and (max_boxes != self.max_boxes or F != getattr(self, "_nms_F", -1)):
             self.max_boxes = int(max_boxes)

@@ -51,7 +51,7 @@ def gpu_gather(frames_np_or_t, pitch, W, H, windows, sizes, out_dims, caps, fmt=
         else:
             outs.append(torch.zeros((caps[q], oh, ow, 3), dtype=torch.uint8, device=DEV))
     st = torch.zeros(1, dtype=torch.int32, device=DEV)
-    ws = torch.empty(B.mp_gather_workspace_size(caps), dtype=torch.uint8, device=DEV)
+    ws = torch.empty(B.mp_gather_workspace_size(out_dims, caps), dtype=torch.uint8, device=DEV)
     ptrs = mp.WindowPipeline.frame_ptrs(fr)
     B.mp_gather_resize(ptrs, pitch, W, H, F, wt, fot, sizes, out_dims, outs, fmt, st, ws)
     torch.cuda.synchronize()

@@ -59,7 +59,7 @@ def test_workspace_queries(lib):
     assert n >= 1800 * 34 * 30 * 16
     assert lib.mp_plan_workspace_size(lib.PlanParams(256, 192, [(64, 64)], [20]), 4) == 0      # no full frame
     assert lib.mp_plan_workspace_size(lib.PlanParams(256, 192, [(64, 64), (256, 192)], [70, 64]), 4) == 0
-    assert lib.mp_gather_workspace_size([10, 20, 5]) >= 35 * 4
+    assert lib.mp_gather_workspace_size([(192, 192), (384, 384), (1440, 810)], [10, 20, 5]) >= 35 * 16
     assert lib.mp_remap_nms_workspace_size(100, 1000) >= 1000 * 28
 
 
