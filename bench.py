@@ -253,7 +253,6 @@ def run_b200(args):
     scores_np = S.score_grids(cfg, clip, scene)
     scores = torch.from_numpy(scores_np).to(dev)
     frames = S.frame_pixels_torch([S.frame_seed(clip, f) for f in range(F)], cfg.H, cfg.pitch, device=dev)
-    ptrs = mp.WindowPipeline.frame_ptrs(frames)
     pipe = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
                              cfg.iou_thr, fmt=fmt, device=dev)
     R, C = cfg.grid
@@ -276,7 +275,7 @@ def run_b200(args):
         pipe.plan(scores)
         if ev is not None:
             ev[0].record(stream)
-        pipe.gather(ptrs)
+        pipe.gather(frames)
         if ev is not None:
             ev[1].record(stream)
         pipe.merge(boxes_t, wbo_t)
@@ -400,7 +399,6 @@ def run_e2e(cfg, clip, scene, scores_np, boxes, wbo, fmt, dev, args):
     scores = torch.empty_like(host_scores, device=dev)
     boxes_t = torch.empty_like(host_boxes, device=dev)
     wbo_t = torch.empty_like(host_wbo, device=dev)
-    ptrs = mp.WindowPipeline.frame_ptrs(frames)
     pipe = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
                              cfg.iou_thr, fmt=fmt, device=dev)
     R, C = cfg.grid
@@ -423,7 +421,7 @@ def run_e2e(cfg, clip, scene, scores_np, boxes, wbo, fmt, dev, args):
         boxes_t.copy_(host_boxes, non_blocking=True)
         wbo_t.copy_(host_wbo, non_blocking=True)
         pipe.plan(scores)
-        pipe.gather(ptrs)
+        pipe.gather(frames)
         pipe.merge(boxes_t, wbo_t)
         off_host.copy_(pipe.nms_frame_off, non_blocking=True)
         out_host.copy_(pipe.nms_out, non_blocking=True)

@@ -147,6 +147,24 @@ mp_status mp_gather_resize(const uint8_t* const* d_frame_ptrs, int32_t pitch, in
                            mp_out_format fmt, int32_t* d_status, void* d_ws, size_t ws_bytes,
                            void* stream);
 
+/*
+ * mp_gather_resize_strided — mp_gather_resize for the common case where the F
+ * frames live in one allocation at a constant stride (a decoded batch):
+ * frame f = d_frames + f * frame_stride.  Same results bit for bit; the source
+ * box of each tile is staged with ONE 3-D TMA tensor copy (per-class tensor
+ * map encoded on the host each call) instead of one bulk copy per row.
+ *
+ *  d_frames      device, 16-byte aligned.
+ *  frame_stride  bytes, multiple of 16, >= H * pitch, < 2^40.
+ *  Other arguments as mp_gather_resize.  The workspace is the same.
+ */
+mp_status mp_gather_resize_strided(const uint8_t* d_frames, int64_t frame_stride, int32_t pitch, int32_t W,
+                                   int32_t H, int32_t F, const mp_window* d_windows,
+                                   const int32_t* d_frame_off, int32_t k, const mp_size* sizes,
+                                   const mp_size* out_dims, void* const* d_out, const int32_t* out_cap,
+                                   mp_out_format fmt, int32_t* d_status, void* d_ws, size_t ws_bytes,
+                                   void* stream);
+
 /* Bytes of scratch mp_remap_nms needs for F frames and max_boxes raw boxes. */
 size_t mp_remap_nms_workspace_size(int32_t F, int32_t max_boxes);
 

@@ -59,6 +59,9 @@ def _load():
     L.mp_gather_workspace_size.argtypes = [i32, vp, vp]
     L.mp_gather_resize.restype = C.c_int
     L.mp_gather_resize.argtypes = [vp, i32, i32, i32, i32, vp, vp, i32, vp, vp, vp, vp, C.c_int, vp, vp, sz, vp]
+    L.mp_gather_resize_strided.restype = C.c_int
+    L.mp_gather_resize_strided.argtypes = [vp, C.c_int64, i32, i32, i32, i32, vp, vp, i32, vp, vp, vp, vp, C.c_int,
+                                           vp, vp, sz, vp]
     L.mp_remap_nms_workspace_size.restype = sz
     L.mp_remap_nms_workspace_size.argtypes = [i32, i32]
     L.mp_remap_nms.restype = C.c_int
@@ -70,6 +73,7 @@ def _load():
 _lib = _load()
 
 EXPORTED = ("mp_plan_workspace_size", "mp_plan_windows", "mp_gather_workspace_size", "mp_gather_resize",
+            "mp_gather_resize_strided",
             "mp_remap_nms_workspace_size", "mp_remap_nms", "mp_status_string", "mp_launches_per_call")
 
 
@@ -185,6 +189,34 @@ def mp_gather_resize(frame_ptrs, pitch, W, H, F, windows, frame_off, sizes, out_
                                ws.numel(), _stream(stream))
     if st != MP_OK:
         raise MPError(st, "mp_gather_resize")
+
+
+def mp_gather_resize_strided(frames, W, H, windows, frame_off, sizes, out_dims, outs, fmt, status, ws,
+                             stream=None) -> None:
+    """a5 on a frame batch: frames uint8 CUDA tensor [F, H, pitch] (rows
+    contiguous, pitch % 16 == 0); frame stride taken from the tensor."""
+    _dev(windows, torch.int32, "windows")
+    _dev(frame_off, torch.int32, "frame_off")
+    _dev(status, torch.int32, "status")
+    _dev(ws, torch.uint8, "ws")
+    if not frames.is_cuda or frames.dtype != torch.uint8 or frames.dim() != 3:
+        raise ValueError("frames must be a uint8 CUDA tensor [F, H, pitch]")
+    if frames.stride(2) != 1 or frames.stride(1) != frames.shape[2]:
+        raise ValueError("frames rows must be contiguous with pitch = shape[2]")
+    F, Hh, pitch = frames.shape
+    k = len(sizes)
+    if len(outs) != k or len(out_dims) != k:
+        raise ValueError("sizes, out_dims and outs must have one entry per size class")
+    odt = torch.float32 if fmt == MP_OUT_F32_NCHW else torch.uint8
+    for q, o in enumerate(outs):
+        _dev(o, odt, f"outs[{q}]")
+    ptrs = (C.c_void_p * k)(*[o.data_ptr() for o in outs])
+    cap = (C.c_int32 * k)(*[int(o.shape[0]) for o in outs])
+    st = _lib.mp_gather_resize_strided(_p(frames), int(frames.stride(0)), int(pitch), int(W), int(H), int(F),
+                                       _p(windows), _p(frame_off), k, _sizes(sizes), _sizes(out_dims), ptrs, cap,
+                                       int(fmt), _p(status), _p(ws), ws.numel(), _stream(stream))
+    if st != MP_OK:
+        raise MPError(st, "mp_gather_resize_strided")
 
 
 def mp_remap_nms_workspace_size(F: int, max_boxes: int) -> int:

@@ -13,44 +13,58 @@
 //   gather_kernel<fmt>   persistent, warp-specialised, Grid = SMs x resident
 //                        CTAs.  Warps 8-9 = producers (alternate tiles): one
 //                        descriptor + 4 tap loads per tile, copy the tile's tap
-//                        slices into the stage header, then 1-D bulk copies
-//                        (TMA engine, cp.async.bulk) of the tile's source rows
-//                        into a 4-deep shared-memory stage ring completing on an
-//                        mbarrier (complete_tx).  Warps 0-7 = consumers: two
-//                        output columns per thread (packed f32x2 math),
-//                        separable lerps reusing staged rows, streaming stores.
+//                        slices into the stage header, then stage the tile's
+//                        source box into a 4-deep shared-memory ring completing
+//                        on an mbarrier (complete_tx): ONE 3-D TMA tensor copy
+//                        (cp.async.bulk.tensor, per-class tensor map over the
+//                        frame batch) on the strided entry point, or one 1-D
+//                        bulk copy per source row on the pointer-array entry
+//                        point.  Warps 0-7 = consumers: two output columns per
+//                        thread (packed f32x2 math), separable lerps reusing
+//                        staged rows, streaming stores.
+#include <cuda.h>
+#include <stdlib.h>
+
 #include "mp_internal.cuh"
 
 namespace mpk {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kProducerWarps = 2;
-constexpr int kGatherThreads = (kConsumerWarps + kProducerWarps) * 32;
+constexpr int kProducerWarps = 1;
+constexpr int kCW = 4;   // consumer warps per CTA; each owns a block of TR/kCW output rows
 constexpr int kStages = 4;
 constexpr int kHdrBytes = 64;
 constexpr int kMaxTW = 256;
 constexpr int kMaxTR = 64;
-constexpr int kTapBytes = kMaxTW * 8 + kMaxTR * 16;
+constexpr int kXtapBytes = (kMaxTW + 2) * 8, kYtapBytes = (kMaxTR + 2) * 8;
+constexpr int kTapBytes = kXtapBytes + kYtapBytes;
 constexpr int kStageDataBudget = 24 * 1024;
+constexpr int kDataOff = (kHdrBytes + kTapBytes + 127) / 128 * 128;   // TMA destination: 128-B aligned
 
 struct GatherArgs {
-  int k, W, H, pitch, F, fmt, stage_bytes;
+  int k, W, H, pitch, F, fmt, stage_bytes, debug, tensor;
+  int ncol[kMaxClasses];
+  int box_w[kMaxClasses], box_h[kMaxClasses];
   int w[kMaxClasses], h[kMaxClasses], ow[kMaxClasses], oh[kMaxClasses];
   int TW[kMaxClasses], TR[kMaxClasses], nct[kMaxClasses], tpw[kMaxClasses];
   int cap[kMaxClasses], list_off[kMaxClasses], xtab_off[kMaxClasses], ytab_off[kMaxClasses];
   void* out[kMaxClasses];
 };
 
-// Per listed window: pointer to the crop's first row (frame + y*pitch), x, slot.
+// Per listed window (indexed by class list offset + slot): frame, x, y, valid.
 struct WinDesc {
-  const uint8_t* row0;
-  int x, valid;
+  int frame, x, y, valid;
 };
 static_assert(sizeof(WinDesc) == 16, "desc");
 
+// One TMA tensor map per size class (box = the class's staged tile footprint).
+struct TmapArray {
+  CUtensorMap m[kMaxClasses];
+};
+
 struct TileHdr {
   int valid, k, slot, oy0, ox0, rows, cols, stride;
-  int pad[8];
+  int x, b0, r_lo, xs, ys;   // window x, staged byte origin, first staged row, tap slice shifts
+  int pad[3];
 };
 static_assert(sizeof(TileHdr) <= kHdrBytes, "header");
 
@@ -90,15 +104,14 @@ __device__ __forceinline__ int tiles_total(const GatherArgs& A, const int* cnt) 
   return T;
 }
 
-__global__ void __launch_bounds__(1024) gather_prep_kernel(GatherArgs A, const uint8_t* const* __restrict__ frames,
-                                                           const mp_window* __restrict__ win,
+__global__ void __launch_bounds__(1024) gather_prep_kernel(GatherArgs A, const mp_window* __restrict__ win,
                                                            const int* __restrict__ frame_off,
                                                            int* __restrict__ ws_cnt, WinDesc* __restrict__ ws_desc,
                                                            int2* __restrict__ ws_tap, int desc_total,
                                                            int* __restrict__ d_status) {
   __shared__ int cnt[kMaxClasses];
   if (threadIdx.x < kMaxClasses) cnt[threadIdx.x] = 0;
-  for (int i = threadIdx.x; i < desc_total; i += blockDim.x) ws_desc[i] = WinDesc{nullptr, 0, 0};
+  for (int i = threadIdx.x; i < desc_total; i += blockDim.x) ws_desc[i] = WinDesc{0, 0, 0, 0};
   // tap tables: x taps of class q at xtab_off[q] (ow entries), y taps at ytab_off[q]
   for (int q = 0; q < A.k; q++) {
     for (int d = threadIdx.x; d < A.ow[q]; d += blockDim.x) {
@@ -127,18 +140,162 @@ __global__ void __launch_bounds__(1024) gather_prep_kernel(GatherArgs A, const u
       set_status(d_status, MP_ERR_CAPACITY);
       continue;
     }
-    ws_desc[A.list_off[q] + w.slot] = WinDesc{frames[w.frame] + (size_t)w.y * A.pitch, w.x, 1};
+    ws_desc[A.list_off[q] + w.slot] = WinDesc{w.frame, w.x, w.y, 1};
   }
   __syncthreads();
   if (threadIdx.x < kMaxClasses) ws_cnt[threadIdx.x] = cnt[threadIdx.x];
 }
 
+// Consumer: warp `wid` owns output rows [wid*R, (wid+1)*R) of the tile
+// (R = ceil(rows / kCW)); lane owns output columns lane + 32*j, j < NCOL
+// (consecutive lanes = consecutive columns: conflict-free byte loads from the
+// staged box, 128-B coalesced stores; pairs of columns share one packed f32x2
+// datapath).  Separable evaluation in source-row order: each staged source row
+// is lerped horizontally once (ping-pong register sets) and an output row is
+// emitted as soon as its lower source row is ready.  The right/bottom taps
+// are always +1 pixel / +1 row: where R15 clamps (i0 = in-1) lambda is 0, so
+// the extra (finite) staged byte has no effect.
+extern __shared__ __align__(128) unsigned char smem[];
+
+template <int FMT, int NCOL>
+__device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr* hdr, unsigned int soff, int wid,
+                                             int lane) {
+  constexpr int NP = NCOL / 2;
+  const int2* xt = reinterpret_cast<const int2*>(&smem[soff + kHdrBytes]);
+  const int2* yt = reinterpret_cast<const int2*>(&smem[soff + kHdrBytes + kXtapBytes]) + hdr->ys;
+  const unsigned int doff = soff + kDataOff;
+  const int q = hdr->k, rows = hdr->rows, cols = hdr->cols;
+  const int x0 = 3 * hdr->x - hdr->b0, r_lo = hdr->r_lo;
+  xt += hdr->xs;
+  const unsigned int stride = (unsigned int)hdr->stride;
+  const int R = (rows + kCW - 1) / kCW;
+  const int rb0 = wid * R, rb1 = min(rows, rb0 + R);
+  if (rb0 >= rb1 || lane >= cols) return;
+  const float2 M2 = make_float2(8388608.0f, 8388608.0f);
+  unsigned int ba[NP], bb[NP];
+  float2 lx[NP];
+#pragma unroll
+  for (int p = 0; p < NP; p++) {
+    const int ca = lane + 64 * p, cb = ca + 32;
+    const int2 xa = xt[min(ca, cols - 1)];
+    const int2 xb = xt[min(cb, cols - 1)];
+    ba[p] = doff + x0 + 3 * xa.x;
+    bb[p] = doff + x0 + 3 * xb.x;
+    lx[p] = make_float2(__int_as_float(xa.y), __int_as_float(xb.y));
+  }
+  float2 P[NP][3], N[NP][3];   // ping-pong horizontal lerps (3 channels x column pair)
+#define MP_H(ROW, H)                                                                            \
+  {                                                                                             \
+    const unsigned int o_ = (unsigned int)(ROW) * stride;                                      \
+    _Pragma("unroll") for (int p = 0; p < NP; p++) {                                            \
+      const unsigned int pa_ = ba[p] + o_, pb_ = bb[p] + o_;                                    \
+      _Pragma("unroll") for (int ch = 0; ch < 3; ch++) {                                        \
+        const float2 m_ = make_float2(u8m(smem[pa_ + ch]), u8m(smem[pb_ + ch]));                 \
+        const float2 n_ = make_float2(u8m(smem[pa_ + 3 + ch]), u8m(smem[pb_ + 3 + ch]));         \
+        H[p][ch] = __ffma2_rn(lx[p], fsub2(n_, m_), fsub2(m_, M2));                              \
+      }                                                                                         \
+    }                                                                                           \
+  }
+  const int ow = A.ow[q], oh = A.oh[q];
+  int orow = rb0;
+  int2 y = yt[orow];
+  y.x -= r_lo;
+  int r = y.x;
+  const int rlast = yt[rb1 - 1].x - r_lo + 1;
+  MP_H(r, P)
+  if (FMT == MP_OUT_F32_NCHW) {
+    const size_t plane = (size_t)oh * ow;
+    float* o0 = reinterpret_cast<float*>(A.out[q]) + (size_t)hdr->slot * 3 * plane +
+                (size_t)(hdr->oy0 + rb0) * ow + hdr->ox0 + lane;
+    float* o1 = o0 + plane;
+    float* o2 = o1 + plane;
+    bool ok[NCOL];
+#pragma unroll
+    for (int j = 0; j < NCOL; j++) ok[j] = lane + 32 * j < cols;
+#define MP_EMIT(T, B)                                                                           \
+  while (orow < rb1 && y.x == r) {                                                              \
+    const float2 ly = make_float2(__int_as_float(y.y), __int_as_float(y.y));                    \
+    _Pragma("unroll") for (int p = 0; p < NP; p++) {                                            \
+      const float2 v0 = __ffma2_rn(ly, fsub2(B[p][0], T[p][0]), T[p][0]);                        \
+      const float2 v1 = __ffma2_rn(ly, fsub2(B[p][1], T[p][1]), T[p][1]);                        \
+      const float2 v2 = __ffma2_rn(ly, fsub2(B[p][2], T[p][2]), T[p][2]);                        \
+      if (ok[2 * p]) {                                                                          \
+        __stcs(o0 + 64 * p, v0.x);                                                              \
+        __stcs(o1 + 64 * p, v1.x);                                                              \
+        __stcs(o2 + 64 * p, v2.x);                                                              \
+      }                                                                                         \
+      if (ok[2 * p + 1]) {                                                                      \
+        __stcs(o0 + 64 * p + 32, v0.y);                                                         \
+        __stcs(o1 + 64 * p + 32, v1.y);                                                         \
+        __stcs(o2 + 64 * p + 32, v2.y);                                                         \
+      }                                                                                         \
+    }                                                                                           \
+    o0 += ow;                                                                                   \
+    o1 += ow;                                                                                   \
+    o2 += ow;                                                                                   \
+    orow++;                                                                                     \
+    if (orow < rb1) { y = yt[orow]; y.x -= r_lo; }                                              \
+  }
+    while (r < rlast) {
+      MP_H(r + 1, N)
+      MP_EMIT(P, N)
+      r++;
+      if (r >= rlast) break;
+      MP_H(r + 1, P)
+      MP_EMIT(N, P)
+      r++;
+    }
+#undef MP_EMIT
+  } else {
+    uint8_t* o = reinterpret_cast<uint8_t*>(A.out[q]) +
+                 (((size_t)hdr->slot * oh + hdr->oy0 + rb0) * ow + hdr->ox0 + lane) * 3;
+    bool ok[NCOL];
+#pragma unroll
+    for (int j = 0; j < NCOL; j++) ok[j] = lane + 32 * j < cols;
+#define MP_EMIT(T, B)                                                                           \
+  while (orow < rb1 && y.x == r) {                                                              \
+    const float2 ly = make_float2(__int_as_float(y.y), __int_as_float(y.y));                    \
+    _Pragma("unroll") for (int p = 0; p < NP; p++) {                                            \
+      const float2 v0 = __ffma2_rn(ly, fsub2(B[p][0], T[p][0]), T[p][0]);                        \
+      const float2 v1 = __ffma2_rn(ly, fsub2(B[p][1], T[p][1]), T[p][1]);                        \
+      const float2 v2 = __ffma2_rn(ly, fsub2(B[p][2], T[p][2]), T[p][2]);                        \
+      if (ok[2 * p]) {                                                                          \
+        o[192 * p + 0] = u8_round(v0.x);                                                        \
+        o[192 * p + 1] = u8_round(v1.x);                                                        \
+        o[192 * p + 2] = u8_round(v2.x);                                                        \
+      }                                                                                         \
+      if (ok[2 * p + 1]) {                                                                      \
+        o[192 * p + 96 + 0] = u8_round(v0.y);                                                   \
+        o[192 * p + 96 + 1] = u8_round(v1.y);                                                   \
+        o[192 * p + 96 + 2] = u8_round(v2.y);                                                   \
+      }                                                                                         \
+    }                                                                                           \
+    o += (size_t)ow * 3;                                                                        \
+    orow++;                                                                                     \
+    if (orow < rb1) { y = yt[orow]; y.x -= r_lo; }                                              \
+  }
+    while (r < rlast) {
+      MP_H(r + 1, N)
+      MP_EMIT(P, N)
+      r++;
+      if (r >= rlast) break;
+      MP_H(r + 1, P)
+      MP_EMIT(N, P)
+      r++;
+    }
+#undef MP_EMIT
+  }
+#undef MP_H
+}
+
 template <int FMT>
-__global__ void __launch_bounds__(kGatherThreads) gather_kernel(GatherArgs A, const int* __restrict__ ws_cnt,
+__global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(const __grid_constant__ GatherArgs A,
+                                                                 const __grid_constant__ TmapArray tm,
+                                                                 const uint8_t* const* __restrict__ frames,
+                                                                 const int* __restrict__ ws_cnt,
                                                                  const WinDesc* __restrict__ ws_desc,
                                                                  const int2* __restrict__ ws_tap,
                                                                  int* __restrict__ d_status) {
-  extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * A.stage_bytes);
   uint64_t* empty = full + kStages;
   __shared__ int cnt[kMaxClasses];
@@ -147,7 +304,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(GatherArgs A, co
   if (tid == 0) {
     for (int s = 0; s < kStages; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], kCW);
     }
     fence_mbar_init();
   }
@@ -155,190 +312,131 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(GatherArgs A, co
   const int T = tiles_total(A, cnt);
   const int G = gridDim.x;
 
-  if (wid >= kConsumerWarps) {
-    // ===================== producer warps (tiles i = p, p+2, ...) =====================
-    const int p = wid - kConsumerWarps;
-    for (int i = p;; i += kProducerWarps) {
-      const int t = blockIdx.x + i * G;
-      if (t >= T) break;
-      const int s = i % kStages;
-      if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
-      unsigned char* stage = smem + (size_t)s * A.stage_bytes;
-      TileHdr* hdr = reinterpret_cast<TileHdr*>(stage);
-      int2* xt = reinterpret_cast<int2*>(stage + kHdrBytes);
-      int4* yt = reinterpret_cast<int4*>(stage + kHdrBytes + kMaxTW * 8);
-      unsigned char* data = stage + kHdrBytes + kTapBytes;
-      // decode t -> (class, slot, row tile, col tile); tiles ordered by class,
-      // slot, then tile, so neighbouring CTAs share halo rows in L2.
+  if (wid >= kCW) {
+    // ===================== producer warp =====================
+    // The global loads a tile needs (its window descriptor and 3 tap bounds)
+    // are issued one tile ahead, so their latency overlaps the wait for a free
+    // stage; the tap slices themselves are staged by the copy engine.
+    struct TileInfo {
+      int q, slot, oy0, ox0, rows, cols;
+    };
+    auto decode = [&](int t, TileInfo& ti) {
       int q = 0, rel = t;
       while (rel >= min(cnt[q], A.cap[q]) * A.tpw[q]) {
         rel -= min(cnt[q], A.cap[q]) * A.tpw[q];
         q++;
       }
-      const int slot = rel / A.tpw[q];
-      const int tw = rel - slot * A.tpw[q];
+      // tiles ordered by class, slot, then tile: neighbouring CTAs share halo rows in L2
+      ti.q = q;
+      ti.slot = rel / A.tpw[q];
+      const int tw = rel - ti.slot * A.tpw[q];
       const int rt = tw / A.nct[q], ct = tw - rt * A.nct[q];
-      const int in_w = A.w[q], in_h = A.h[q];
-      const int oy0 = rt * A.TR[q], ox0 = ct * A.TW[q];
-      const int rows = min(A.TR[q], A.oh[q] - oy0), cols = min(A.TW[q], A.ow[q] - ox0);
-      const int2* xtab = ws_tap + A.xtab_off[q];
-      const int2* ytab = ws_tap + A.ytab_off[q];
-      const WinDesc d = ws_desc[A.list_off[q] + slot];
-      const int c_lo = __ldg(&xtab[ox0].x), c_hi = min(__ldg(&xtab[ox0 + cols - 1].x) + 1, in_w - 1);
-      const int r_lo = __ldg(&ytab[oy0].x), r_hi = min(__ldg(&ytab[oy0 + rows - 1].x) + 1, in_h - 1);
-      if (!d.valid) {   // slots of this class are not 0..count-1
-        if (lane == 0) {
+      ti.oy0 = rt * A.TR[q];
+      ti.ox0 = ct * A.TW[q];
+      ti.rows = min(A.TR[q], A.oh[q] - ti.oy0);
+      ti.cols = min(A.TW[q], A.ow[q] - ti.ox0);
+    };
+    TileInfo cur, nxt;
+    WinDesc dcur = WinDesc{0, 0, 0, 0}, dnxt = dcur;
+    int clo_cur = 0, rlo_cur = 0, rhi_cur = 0, clo_nxt = 0, rlo_nxt = 0, rhi_nxt = 0;
+    auto prefetch = [&](const TileInfo& ti, WinDesc& d, int& clo, int& rlo, int& rhi) {
+      d = ws_desc[A.list_off[ti.q] + ti.slot];
+      clo = __ldg(&ws_tap[A.xtab_off[ti.q] + ti.ox0].x);
+      rlo = __ldg(&ws_tap[A.ytab_off[ti.q] + ti.oy0].x);
+      rhi = __ldg(&ws_tap[A.ytab_off[ti.q] + ti.oy0 + ti.rows - 1].x);
+    };
+    if (blockIdx.x < T) {
+      decode(blockIdx.x, cur);
+      prefetch(cur, dcur, clo_cur, rlo_cur, rhi_cur);
+    }
+    for (int i = 0;; i++) {
+      const int t = blockIdx.x + i * G;
+      if (t >= T) break;
+      const int s = i % kStages;
+      if (t + G < T) {
+        decode(t + G, nxt);
+        prefetch(nxt, dnxt, clo_nxt, rlo_nxt, rhi_nxt);
+      }
+      if (i >= kStages) mbar_wait_sleep(&empty[s], ((i / kStages) - 1) & 1);
+      unsigned char* stage = smem + (size_t)s * A.stage_bytes;
+      TileHdr* hdr = reinterpret_cast<TileHdr*>(stage);
+      unsigned char* xt = stage + kHdrBytes;
+      unsigned char* yt = stage + kHdrBytes + kXtapBytes;
+      unsigned char* data = stage + kDataOff;
+      const int q = cur.q;
+      if (lane == 0) {
+        if (!dcur.valid) {   // slots of this class are not 0..count-1
           hdr->valid = 0;
           set_status(d_status, MP_ERR_INVALID);
           mbar_arrive(&full[s]);
+        } else {
+          const int b0 = (3 * (dcur.x + clo_cur)) & ~15;
+          const int stride = A.box_w[q];
+          const int xe = A.xtab_off[q] + cur.ox0, ye = A.ytab_off[q] + cur.oy0;   // first tap entries
+          const int xs = xe & 1, ys = ye & 1;                                       // 16-B aligned slices
+          const uint32_t xbytes = (uint32_t)((cur.cols + xs + 1) & ~1) * 8;
+          const uint32_t ybytes = (uint32_t)((cur.rows + ys + 1) & ~1) * 8;
+          hdr->valid = 1;
+          hdr->k = q;
+          hdr->slot = cur.slot;
+          hdr->oy0 = cur.oy0;
+          hdr->ox0 = cur.ox0;
+          hdr->rows = cur.rows;
+          hdr->cols = cur.cols;
+          hdr->stride = stride;
+          hdr->x = dcur.x;
+          hdr->b0 = b0;
+          hdr->r_lo = rlo_cur;
+          hdr->xs = xs;
+          hdr->ys = ys;
+          if (A.debug == 2) {   // experiment: no pixel copies (compute-only bound)
+            mbar_arrive_expect_tx(&full[s], xbytes + ybytes);
+            bulk_g2s(xt, ws_tap + (xe - xs), xbytes, &full[s]);
+            bulk_g2s(yt, ws_tap + (ye - ys), ybytes, &full[s]);
+          } else if (A.tensor) {
+            // one TMA box: [box_h rows][box_w bytes] from (b0, y + r_lo) of frame d.frame;
+            // rows past the frame bottom / bytes past the pitch are zero-filled.
+            mbar_arrive_expect_tx(&full[s], (uint32_t)(stride * A.box_h[q]) + xbytes + ybytes);
+            bulk_g2s(xt, ws_tap + (xe - xs), xbytes, &full[s]);
+            bulk_g2s(yt, ws_tap + (ye - ys), ybytes, &full[s]);
+            tma_load_3d(data, &tm.m[q], b0 >> 3, dcur.y + rlo_cur, dcur.frame, &full[s]);
+          } else {
+            // one 1-D bulk copy per source row (rows r_lo .. min(i0(last)+1, h-1) of the crop)
+            const int nrows = min(rhi_cur + 1, A.h[q] - 1) - rlo_cur + 1;
+            const int bytes = min(stride, A.pitch - b0);
+            mbar_arrive_expect_tx(&full[s], (uint32_t)(nrows * bytes) + xbytes + ybytes);
+            bulk_g2s(xt, ws_tap + (xe - xs), xbytes, &full[s]);
+            bulk_g2s(yt, ws_tap + (ye - ys), ybytes, &full[s]);
+            const uint8_t* src = frames[dcur.frame] + (size_t)(dcur.y + rlo_cur) * A.pitch + b0;
+            for (int r = 0; r < nrows; r++)
+              bulk_g2s(data + (size_t)r * stride, src + (size_t)r * A.pitch, (uint32_t)bytes, &full[s]);
+          }
         }
-        __syncwarp();
-        continue;
-      }
-      const int b0 = (3 * (d.x + c_lo)) & ~15;
-      const int b1 = (3 * (d.x + c_hi + 1) + 15) & ~15;
-      const int stride = b1 - b0;
-      const int nrows = r_hi - r_lo + 1;
-      for (int c = lane; c < cols; c += 32) {
-        const int2 e = __ldg(&xtab[ox0 + c]);
-        const int di = (e.x < in_w - 1) ? 3 : 0;
-        xt[c] = make_int2((3 * (d.x + e.x) - b0) | (di << 20), e.y);
-      }
-      for (int r = lane; r < rows; r += 32) {
-        const int2 e = __ldg(&ytab[oy0 + r]);
-        const int i1 = min(e.x + 1, in_h - 1);
-        yt[r] = make_int4((e.x - r_lo) * stride, (i1 - r_lo) * stride, e.y, 0);
-      }
-      if (lane == 0) {
-        hdr->valid = 1;
-        hdr->k = q;
-        hdr->slot = slot;
-        hdr->oy0 = oy0;
-        hdr->ox0 = ox0;
-        hdr->rows = rows;
-        hdr->cols = cols;
-        hdr->stride = stride;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(nrows * stride));
-      __syncwarp();
-      const uint8_t* src = d.row0 + (size_t)r_lo * A.pitch + b0;
-      for (int r = lane; r < nrows; r += 32)
-        bulk_g2s(data + (size_t)r * stride, src + (size_t)r * A.pitch, (uint32_t)stride, &full[s]);
+      cur = nxt;
+      dcur = dnxt;
+      clo_cur = clo_nxt;
+      rlo_cur = rlo_nxt;
+      rhi_cur = rhi_nxt;
     }
     return;
   }
 
   // ===================== consumer warps =====================
-  // Thread <-> two output columns of the tile, c and c + half (consecutive
-  // lanes = consecutive columns: conflict-free byte loads, coalesced stores;
-  // the pair shares one packed f32x2 datapath), and a contiguous block of rows.
-  // Separable evaluation: the horizontal lerp of a staged source row is
-  // computed once and reused by the next output row that taps the same row.
-  const int ctid = tid;   // 0 .. 32*kConsumerWarps-1
-  const float2 M2 = make_float2(8388608.0f, 8388608.0f);
   for (int i = 0;; i++) {
     const int t = blockIdx.x + i * G;
     if (t >= T) break;
     const int s = i % kStages;
-    mbar_wait(&full[s], (i / kStages) & 1);
+    mbar_wait_sleep(&full[s], (i / kStages) & 1);
     const unsigned int soff = (unsigned int)s * (unsigned int)A.stage_bytes;
     const TileHdr* hdr = reinterpret_cast<const TileHdr*>(&smem[soff]);
-    if (hdr->valid) {
-      const int2* xt = reinterpret_cast<const int2*>(&smem[soff + kHdrBytes]);
-      const int4* yt = reinterpret_cast<const int4*>(&smem[soff + kHdrBytes + kMaxTW * 8]);
-      const unsigned int doff = soff + kHdrBytes + kTapBytes;
-      const int q = hdr->k, rows = hdr->rows, cols = hdr->cols;
-      const int half = (cols + 1) >> 1;
-      const int nph = max(1, (32 * kConsumerWarps) / half);
-      const int ph = ctid / half, c = ctid - ph * half;
-      if (ph < nph) {
-        const int rpp = (rows + nph - 1) / nph;
-        const int rb0 = ph * rpp, rb1 = min(rows, rb0 + rpp);
-        const bool two = (c + half) < cols;
-        const int2 xa = xt[c];
-        const int2 xb = two ? xt[c + half] : xa;
-        const unsigned int ba = doff + (xa.x & 0xFFFFF), bb = doff + (xb.x & 0xFFFFF);
-        const unsigned int da = ba + (xa.x >> 20), db = bb + (xb.x >> 20);
-        const float2 lx = make_float2(__int_as_float(xa.y), __int_as_float(xb.y));
-        const int ow = A.ow[q], oh = A.oh[q];
-        int ra = -1, rb = -1;
-        float2 ha0, ha1, ha2, hb0, hb1, hb2;
-#define MP_HLERP(ROWOFF, H0, H1, H2)                                                          \
-  {                                                                                           \
-    const unsigned int o_ = (unsigned int)(ROWOFF);                                           \
-    float2 m_, n_;                                                                            \
-    m_ = make_float2(u8m(smem[ba + o_ + 0]), u8m(smem[bb + o_ + 0]));                          \
-    n_ = make_float2(u8m(smem[da + o_ + 0]), u8m(smem[db + o_ + 0]));                          \
-    H0 = __ffma2_rn(lx, fsub2(n_, m_), fsub2(m_, M2));                               \
-    m_ = make_float2(u8m(smem[ba + o_ + 1]), u8m(smem[bb + o_ + 1]));                          \
-    n_ = make_float2(u8m(smem[da + o_ + 1]), u8m(smem[db + o_ + 1]));                          \
-    H1 = __ffma2_rn(lx, fsub2(n_, m_), fsub2(m_, M2));                               \
-    m_ = make_float2(u8m(smem[ba + o_ + 2]), u8m(smem[bb + o_ + 2]));                          \
-    n_ = make_float2(u8m(smem[da + o_ + 2]), u8m(smem[db + o_ + 2]));                          \
-    H2 = __ffma2_rn(lx, fsub2(n_, m_), fsub2(m_, M2));                               \
-  }
-        if (FMT == MP_OUT_F32_NCHW) {
-          const int plane = oh * ow;
-          float* o = reinterpret_cast<float*>(A.out[q]) + (size_t)hdr->slot * 3 * plane +
-                     (size_t)(hdr->oy0 + rb0) * ow + hdr->ox0 + c;
-          for (int r = rb0; r < rb1; r++) {
-            const int4 y = yt[r];
-            if (y.x != ra) {
-              if (y.x == rb) { ha0 = hb0; ha1 = hb1; ha2 = hb2; }
-              else MP_HLERP(y.x, ha0, ha1, ha2)
-              ra = y.x;
-            }
-            if (y.y != rb) {
-              if (y.y == ra) { hb0 = ha0; hb1 = ha1; hb2 = ha2; }
-              else MP_HLERP(y.y, hb0, hb1, hb2)
-              rb = y.y;
-            }
-            const float2 ly = make_float2(__int_as_float(y.z), __int_as_float(y.z));
-            const float2 v0 = __ffma2_rn(ly, fsub2(hb0, ha0), ha0);
-            const float2 v1 = __ffma2_rn(ly, fsub2(hb1, ha1), ha1);
-            const float2 v2 = __ffma2_rn(ly, fsub2(hb2, ha2), ha2);
-            __stcs(o, v0.x);
-            __stcs(o + plane, v1.x);
-            __stcs(o + 2 * plane, v2.x);
-            if (two) {
-              __stcs(o + half, v0.y);
-              __stcs(o + plane + half, v1.y);
-              __stcs(o + 2 * plane + half, v2.y);
-            }
-            o += ow;
-          }
-        } else {
-          uint8_t* o = reinterpret_cast<uint8_t*>(A.out[q]) +
-                       (((size_t)hdr->slot * oh + hdr->oy0 + rb0) * ow + hdr->ox0 + c) * 3;
-          for (int r = rb0; r < rb1; r++) {
-            const int4 y = yt[r];
-            if (y.x != ra) {
-              if (y.x == rb) { ha0 = hb0; ha1 = hb1; ha2 = hb2; }
-              else MP_HLERP(y.x, ha0, ha1, ha2)
-              ra = y.x;
-            }
-            if (y.y != rb) {
-              if (y.y == ra) { hb0 = ha0; hb1 = ha1; hb2 = ha2; }
-              else MP_HLERP(y.y, hb0, hb1, hb2)
-              rb = y.y;
-            }
-            const float2 ly = make_float2(__int_as_float(y.z), __int_as_float(y.z));
-            const float2 v0 = __ffma2_rn(ly, fsub2(hb0, ha0), ha0);
-            const float2 v1 = __ffma2_rn(ly, fsub2(hb1, ha1), ha1);
-            const float2 v2 = __ffma2_rn(ly, fsub2(hb2, ha2), ha2);
-            o[0] = u8_round(v0.x);   // R16 round half up, clamp
-            o[1] = u8_round(v1.x);
-            o[2] = u8_round(v2.x);
-            if (two) {
-              o[3 * half + 0] = u8_round(v0.y);
-              o[3 * half + 1] = u8_round(v1.y);
-              o[3 * half + 2] = u8_round(v2.y);
-            }
-            o += (size_t)ow * 3;
-          }
-        }
-#undef MP_HLERP
+    if (hdr->valid && A.debug != 1) {
+      switch (A.ncol[hdr->k]) {
+        case 2: consume_tile<FMT, 2>(A, hdr, soff, wid, lane); break;
+        case 4: consume_tile<FMT, 4>(A, hdr, soff, wid, lane); break;
+        case 6: consume_tile<FMT, 6>(A, hdr, soff, wid, lane); break;
+        default: consume_tile<FMT, 8>(A, hdr, soff, wid, lane); break;
       }
     }
     __syncwarp();
@@ -355,26 +453,27 @@ static void host_tap(int in, int out, int d, int* i0, int* i1) {
   *i1 = (int)(a + 1 < in - 1 ? a + 1 : in - 1);
 }
 
-// Largest staged footprint (bytes) of any tile of a class with tile dims (TW, TR).
-static long long class_stage_data(int in_w, int in_h, int ow, int oh, int TW, int TR) {
-  long long best = 0;
+// Staged box of a class with tile dims (TW, TR): every tile reads source
+// columns c_lo .. i0(last)+1 (the +1 pixel is the always-present right tap)
+// starting at a 16-B aligned byte b0 >= 3*(x+c_lo)-15, and source rows
+// r_lo .. i0(last)+1.  Returns the box (bytes x rows) that covers any tile.
+static void class_box(int in_w, int in_h, int ow, int oh, int TW, int TR, int* box_w, int* box_h) {
   int nct = (ow + TW - 1) / TW, nrt = (oh + TR - 1) / TR;
   int max_rows = 0, max_cols = 0, a, b, c, d;
   for (int rt = 0; rt < nrt; rt++) {
     int oy0 = rt * TR, rows = (TR < oh - oy0 ? TR : oh - oy0);
     host_tap(in_h, oh, oy0, &a, &b);
     host_tap(in_h, oh, oy0 + rows - 1, &c, &d);
-    if (d - a + 1 > max_rows) max_rows = d - a + 1;
+    if (c - a + 2 > max_rows) max_rows = c - a + 2;
   }
   for (int ct = 0; ct < nct; ct++) {
     int ox0 = ct * TW, cols = (TW < ow - ox0 ? TW : ow - ox0);
     host_tap(in_w, ow, ox0, &a, &b);
     host_tap(in_w, ow, ox0 + cols - 1, &c, &d);
-    if (d - a + 1 > max_cols) max_cols = d - a + 1;
+    if (c - a + 2 > max_cols) max_cols = c - a + 2;
   }
-  long long stride = ((3LL * max_cols + 30) + 15) / 16 * 16;
-  best = stride * max_rows;
-  return best;
+  *box_w = (3 * max_cols + 15 + 15) / 16 * 16;
+  *box_h = max_rows;
 }
 
 static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_size* sizes,
@@ -393,6 +492,7 @@ static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_si
   A->fmt = fmt;
   long long data_max = 0;
   int list = 0, taps = 0;
+  const long long budget = kStageDataBudget;
   for (int q = 0; q < k; q++) {
     const int w = sizes[q].w, h = sizes[q].h, ow = out_dims[q].w, oh = out_dims[q].h;
     if (w < 1 || h < 1 || w > W || h > H || ow < 1 || oh < 1 || ow > 16384 || oh > 16384) return false;
@@ -402,24 +502,38 @@ static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_si
     A->h[q] = h;
     A->ow[q] = ow;
     A->oh[q] = oh;
-    // tile width: a power of two <= 256 (so 256 consumer threads split into
-    // whole column phases), height so a tile is ~4K output pixels
-    int TW = 256;
-    while (TW > 32 && TW > ow) TW >>= 1;
-    int TR = 4096 / TW;
-    if (TR > kMaxTR) TR = kMaxTR;
-    long long dat = class_stage_data(w, h, ow, oh, TW, TR);
-    while (dat > kStageDataBudget && TR > 1) {
-      TR = TR - 1;
-      dat = class_stage_data(w, h, ow, oh, TW, TR);
+    // column tiles of equal width TW <= 256 (so every tile's TMA box is the
+    // class box, no over-fetch), NCOL = TW/32 rounded up to even columns per
+    // lane; rows: kCW warps x Rw rows each, Rw as large as the stage budget
+    // and the TMA box limits (256 rows, 256 x 8 bytes) allow (<= 8).
+    // Prefer the widest tiles whose box fits with >= 4 rows per warp; strong
+    // downscales of wide windows fall back to narrower column tiles.
+    int TW = 0, TR = 0, bw = 0, bh = 0, best_area = 0;
+    for (int nct = (ow + kMaxTW - 1) / kMaxTW; nct <= (ow + 31) / 32; nct++) {
+      const int tw = (ow + nct - 1) / nct;
+      int Rw = 8, cbw = 0, cbh = 0;
+      for (; Rw >= 1; Rw--) {
+        class_box(w, h, ow, oh, tw, kCW * Rw, &cbw, &cbh);
+        if ((long long)cbw * cbh <= budget && cbw <= 2048 && cbh <= 256) break;
+      }
+      if (Rw < 1) continue;
+      if (tw * Rw > best_area) {
+        best_area = tw * Rw;
+        TW = tw;
+        TR = kCW * Rw;
+        bw = cbw;
+        bh = cbh;
+      }
+      if (Rw >= 4) break;
     }
-    while (dat > kStageDataBudget && TW > 32) {
-      TW >>= 1;
-      dat = class_stage_data(w, h, ow, oh, TW, TR);
-    }
-    if (dat > 4 * kStageDataBudget) return false;   // > 32x downscale: unsupported
+    if (TW == 0) return false;   // too strong a downscale of too wide a window: unsupported
+    int ncol = (TW + 31) / 32;
+    ncol += ncol & 1;
+    A->ncol[q] = ncol;
     A->TW[q] = TW;
     A->TR[q] = TR;
+    A->box_w[q] = bw;
+    A->box_h[q] = bh;
     A->nct[q] = (ow + TW - 1) / TW;
     A->tpw[q] = A->nct[q] * ((oh + TR - 1) / TR);
     A->cap[q] = out_cap[q];
@@ -430,9 +544,9 @@ static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_si
     taps += ow;
     A->ytab_off[q] = taps;
     taps += oh;
-    if (dat > data_max) data_max = dat;
+    if ((long long)bw * bh > data_max) data_max = (long long)bw * bh;
   }
-  A->stage_bytes = (int)(((kHdrBytes + kTapBytes + data_max) + 127) / 128 * 128);
+  A->stage_bytes = (int)((kDataOff + data_max + 64 + 127) / 128 * 128);
   return true;
 }
 
@@ -465,14 +579,14 @@ extern "C" size_t mp_gather_workspace_size(int32_t k, const mp_size* out_dims, c
   return gather_ws_layout(k, out_dims, out_cap, &L) ? L.total : 0;
 }
 
-extern "C" mp_status mp_gather_resize(const uint8_t* const* d_frame_ptrs, int32_t pitch, int32_t W, int32_t H,
-                                      int32_t F, const mp_window* d_windows, const int32_t* d_frame_off,
-                                      int32_t k, const mp_size* sizes, const mp_size* out_dims,
-                                      void* const* d_out, const int32_t* out_cap, mp_out_format fmt,
-                                      int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
-  GatherArgs A;
-  if (!build_gather_args(pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A)) return MP_ERR_INVALID;
-  if (!d_frame_off || !d_status || (F > 0 && (!d_frame_ptrs || !d_windows))) return MP_ERR_INVALID;
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t* const* d_frame_ptrs,
+                               const mp_window* d_windows, const int32_t* d_frame_off, int32_t k,
+                               const mp_size* out_dims, const int32_t* out_cap, mp_out_format fmt,
+                               int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
   GatherWs L;
   if (!gather_ws_layout(k, out_dims, out_cap, &L) || !d_ws || ws_bytes < L.total) return MP_ERR_INVALID;
   int desc_total = 0;
@@ -482,22 +596,83 @@ extern "C" mp_status mp_gather_resize(const uint8_t* const* d_frame_ptrs, int32_
   int* ws_cnt = (int*)(ws + L.cnt_off);
   WinDesc* ws_desc = (WinDesc*)(ws + L.desc_off);
   int2* ws_tap = (int2*)(ws + L.tap_off);
-  gather_prep_kernel<<<1, 1024, 0, s>>>(A, d_frame_ptrs, d_windows, d_frame_off, ws_cnt, ws_desc, ws_tap, desc_total,
-                                        d_status);
+  gather_prep_kernel<<<1, 1024, 0, s>>>(A, d_windows, d_frame_off, ws_cnt, ws_desc, ws_tap, desc_total, d_status);
   MP_CUDA_TRY(cudaGetLastError());
-  if (F == 0) return MP_OK;
+  if (A.F == 0) return MP_OK;
   const size_t smem = (size_t)kStages * A.stage_bytes + 2 * kStages * sizeof(uint64_t);
   if (smem > 227 * 1024) return MP_ERR_UNSUPPORTED;
   int dev = 0, sms = 0, per_sm = 0;
   MP_CUDA_TRY(cudaGetDevice(&dev));
   MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // Diagnostic only (profiling the two halves of the pipeline): MP_GATHER_DEBUG=1
+  // skips the consumer math, =2 skips the pixel copies.  Unset in production.
+  const char* dbg = getenv("MP_GATHER_DEBUG");
+  A.debug = dbg ? atoi(dbg) : 0;
+  const int threads = (kCW + kProducerWarps) * 32;
   auto launch = [&](auto kern) -> mp_status {
     MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGatherThreads, smem));
+    MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
     if (per_sm < 1) per_sm = 1;
-    kern<<<sms * per_sm, kGatherThreads, smem, s>>>(A, ws_cnt, ws_desc, ws_tap, d_status);
+    kern<<<sms * per_sm, threads, smem, s>>>(A, tm, d_frame_ptrs, ws_cnt, ws_desc, ws_tap, d_status);
     MP_CUDA_TRY(cudaGetLastError());
     return MP_OK;
   };
   return fmt == MP_OUT_F32_NCHW ? launch(gather_kernel<MP_OUT_F32_NCHW>) : launch(gather_kernel<MP_OUT_U8_NHWC>);
+}
+
+extern "C" mp_status mp_gather_resize(const uint8_t* const* d_frame_ptrs, int32_t pitch, int32_t W, int32_t H,
+                                      int32_t F, const mp_window* d_windows, const int32_t* d_frame_off,
+                                      int32_t k, const mp_size* sizes, const mp_size* out_dims,
+                                      void* const* d_out, const int32_t* out_cap, mp_out_format fmt,
+                                      int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+  GatherArgs A;
+  if (!build_gather_args(pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A)) return MP_ERR_INVALID;
+  if (!d_frame_off || !d_status || (F > 0 && (!d_frame_ptrs || !d_windows))) return MP_ERR_INVALID;
+  TmapArray tm;
+  memset(&tm, 0, sizeof(tm));
+  A.tensor = 0;
+  return gather_launch(A, tm, d_frame_ptrs, d_windows, d_frame_off, k, out_dims, out_cap, fmt, d_status, d_ws,
+                       ws_bytes, stream);
+}
+
+extern "C" mp_status mp_gather_resize_strided(const uint8_t* d_frames, int64_t frame_stride, int32_t pitch,
+                                              int32_t W, int32_t H, int32_t F, const mp_window* d_windows,
+                                              const int32_t* d_frame_off, int32_t k, const mp_size* sizes,
+                                              const mp_size* out_dims, void* const* d_out, const int32_t* out_cap,
+                                              mp_out_format fmt, int32_t* d_status, void* d_ws, size_t ws_bytes,
+                                              void* stream) {
+  GatherArgs A;
+  if (!build_gather_args(pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A)) return MP_ERR_INVALID;
+  if (!d_frame_off || !d_status || (F > 0 && (!d_frames || !d_windows))) return MP_ERR_INVALID;
+  if (F > 0 && (((uintptr_t)d_frames) & 15)) return MP_ERR_INVALID;
+  if (frame_stride < (int64_t)H * pitch || (frame_stride & 15) || frame_stride >= (int64_t(1) << 40))
+    return MP_ERR_INVALID;
+  TmapArray tm;
+  memset(&tm, 0, sizeof(tm));
+  A.tensor = 1;
+  if (F > 0) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess || !fn) {
+      (void)cudaGetLastError();
+      return MP_ERR_CUDA;
+    }
+    EncodeTiledFn encode = (EncodeTiledFn)fn;
+    // measured on B200: 64-B L2 promotion beats none / 128 B / 256 B for these ~0.8 KB box rows
+    const CUtensorMapL2promotion l2promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    for (int q = 0; q < k; q++) {
+      // the frame batch as a 3-D tensor of 8-byte elements: [F][H][pitch/8]
+      const cuuint64_t gdim[3] = {(cuuint64_t)(pitch / 8), (cuuint64_t)H, (cuuint64_t)F};
+      const cuuint64_t gstride[2] = {(cuuint64_t)pitch, (cuuint64_t)frame_stride};
+      const cuuint32_t box[3] = {(cuuint32_t)(A.box_w[q] / 8), (cuuint32_t)A.box_h[q], 1};
+      const cuuint32_t estr[3] = {1, 1, 1};
+      if (encode(&tm.m[q], CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, (void*)d_frames, gdim, gstride, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2promo,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return MP_ERR_UNSUPPORTED;
+    }
+  }
+  return gather_launch(A, tm, nullptr, d_windows, d_frame_off, k, out_dims, out_cap, fmt, d_status, d_ws,
+                       ws_bytes, stream);
 }

@@ -144,6 +144,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Same, but the waiting thread is suspended in hardware (up to ~1 ms per try)
+// instead of spinning, so waiting consumer warps take no issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAITS_%=;\n}" ::"r"(addr),
+      "r"(parity), "r"(0x100000u)
+      : "memory");
+}
+
 // 1-D bulk copy global -> shared through the TMA engine (SASS UBLKCP);
 // completion is signalled as tx bytes on `bar`.  src/dst 16-B aligned,
 // bytes a multiple of 16.
@@ -153,6 +166,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst_smem)),
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// 3-D TMA tensor copy global -> shared (SASS UTMALDG), completion as tx bytes
+// on `bar`.  c0 is the innermost coordinate (in tensor elements).
+__device__ __forceinline__ void tma_load_3d(void* dst_smem, const void* tmap, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
 

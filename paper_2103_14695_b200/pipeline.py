@@ -80,9 +80,16 @@ class WindowPipeline:
         B.mp_plan_windows(self.params, scores, F, self.mask, self.windows, self.frame_off, self.class_count,
                           self.status, self.plan_ws, stream)
 
-    def gather(self, frame_ptrs: torch.Tensor, stream=None):
-        B.mp_gather_resize(frame_ptrs, self.pitch, self.W, self.H, self.F, self.windows, self.frame_off,
-                           self.sizes, self.out_dims, self.outs, self.fmt, self.status, self.gather_ws, stream)
+    def gather(self, frames: torch.Tensor, stream=None):
+        """frames: either a uint8 [F, H, pitch] batch tensor (TMA tensor path,
+        mp_gather_resize_strided) or an int64 [F] tensor of frame addresses
+        (pointer-array path, mp_gather_resize)."""
+        if frames.dtype == torch.uint8:
+            B.mp_gather_resize_strided(frames, self.W, self.H, self.windows, self.frame_off, self.sizes,
+                                       self.out_dims, self.outs, self.fmt, self.status, self.gather_ws, stream)
+        else:
+            B.mp_gather_resize(frames, self.pitch, self.W, self.H, self.F, self.windows, self.frame_off,
+                               self.sizes, self.out_dims, self.outs, self.fmt, self.status, self.gather_ws, stream)
 
     def merge(self, boxes: torch.Tensor, win_box_off: torch.Tensor, stream=None):
         B.mp_remap_nms(boxes, win_box_off, self.windows, self.frame_off, self.F, self.out_dims, self.W, self.H,

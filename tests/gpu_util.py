@@ -31,7 +31,8 @@ def gpu_plan(W, H, cw, ch, b, sizes, cost, scores, max_windows=None, want_mask=T
                 mask=(mask[:F].cpu().numpy().view(np.uint32) if want_mask else None))
 
 
-def gpu_gather(frames_np_or_t, pitch, W, H, windows, sizes, out_dims, caps, fmt=mp.MP_OUT_F32_NCHW):
+def gpu_gather(frames_np_or_t, pitch, W, H, windows, sizes, out_dims, caps, fmt=mp.MP_OUT_F32_NCHW,
+               strided=True):
     if isinstance(frames_np_or_t, torch.Tensor):
         fr = frames_np_or_t
     else:
@@ -52,8 +53,11 @@ def gpu_gather(frames_np_or_t, pitch, W, H, windows, sizes, out_dims, caps, fmt=
             outs.append(torch.zeros((caps[q], oh, ow, 3), dtype=torch.uint8, device=DEV))
     st = torch.zeros(1, dtype=torch.int32, device=DEV)
     ws = torch.empty(B.mp_gather_workspace_size(out_dims, caps), dtype=torch.uint8, device=DEV)
-    ptrs = mp.WindowPipeline.frame_ptrs(fr)
-    B.mp_gather_resize(ptrs, pitch, W, H, F, wt, fot, sizes, out_dims, outs, fmt, st, ws)
+    if strided:
+        B.mp_gather_resize_strided(fr, W, H, wt, fot, sizes, out_dims, outs, fmt, st, ws)
+    else:
+        ptrs = mp.WindowPipeline.frame_ptrs(fr)
+        B.mp_gather_resize(ptrs, pitch, W, H, F, wt, fot, sizes, out_dims, outs, fmt, st, ws)
     torch.cuda.synchronize()
     return int(st.item()), [o.cpu().numpy() for o in outs]
 

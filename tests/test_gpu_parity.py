@@ -149,12 +149,12 @@ def _frames(cfg, clip, F):
     return [S.frame_pixels_np(S.frame_seed(clip, f), cfg.H, cfg.pitch) for f in range(F)]
 
 
-def _gather_compare(G, frames, pitch, W, H, windows, sizes, out_dims, fmt):
+def _gather_compare(G, frames, pitch, W, H, windows, sizes, out_dims, fmt, strided=True):
     win = np.asarray(windows, np.int32).reshape(-1, 7)
     caps = [int((win[:, 5] == q).sum()) for q in range(len(sizes))]
     st_r, ref = O.gather_resize(frames, pitch, W, H, win, sizes, out_dims, caps,
                                 O.F32_NCHW if fmt == 0 else O.U8_NHWC)
-    st_g, got = G.gpu_gather(frames, pitch, W, H, win, sizes, out_dims, caps, fmt)
+    st_g, got = G.gpu_gather(frames, pitch, W, H, win, sizes, out_dims, caps, fmt, strided)
     assert st_g == st_r == 0
     for q in range(len(sizes)):
         if caps[q] == 0:
@@ -168,20 +168,22 @@ def _gather_compare(G, frames, pitch, W, H, windows, sizes, out_dims, fmt):
     return ref, got
 
 
+@pytest.mark.parametrize("strided", [True, False], ids=["tma_tensor", "ptr_array"])
 @pytest.mark.parametrize("fmt", [0, 1])
 @pytest.mark.parametrize("name,frames", [("c1_540p", 30), ("c2_1080p_sparse", 24), ("c4_4k_drone", 2)])
-def test_gather_parity_configs(G, name, frames, fmt):
+def test_gather_parity_configs(G, name, frames, fmt, strided):
     cfg = S.CONFIGS[name]
     scene = S.make_scene(cfg, 4, frames)
     scores = S.score_grids(cfg, 4, scene)
     plan = O.plan_windows(cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores)
     _gather_compare(G, _frames(cfg, 4, frames), cfg.pitch, cfg.W, cfg.H, plan["windows"], cfg.sizes,
-                    cfg.out_dims, fmt)
+                    cfg.out_dims, fmt, strided)
 
 
+@pytest.mark.parametrize("strided", [True, False], ids=["tma_tensor", "ptr_array"])
 @pytest.mark.parametrize("fmt", [0, 1])
 @pytest.mark.parametrize("scale", [1.0, 0.5, 0.7, 1.37, 0.26, 0.9999])
-def test_gather_parity_scales_and_edges(G, scale, fmt):
+def test_gather_parity_scales_and_edges(G, scale, fmt, strided):
     """Odd output widths (scalar stores), upscale, dyadic, near-identity, strong
     downscale, and windows touching every frame edge."""
     W, H = 640, 360
@@ -202,7 +204,7 @@ def test_gather_parity_scales_and_edges(G, scale, fmt):
     for q in range(3):
         sel = np.nonzero(win[:, 5] == q)[0]
         win[sel, 6] = np.arange(len(sel))
-    ref, got = _gather_compare(G, frames, pitch, W, H, win, sizes, out_dims, fmt)
+    ref, got = _gather_compare(G, frames, pitch, W, H, win, sizes, out_dims, fmt, strided)
     if scale == 1.0:   # exact crop copy, bit-exact
         for q in range(3):
             if fmt == 0:
@@ -308,7 +310,7 @@ def test_full_size_bench_config_parity(G):
     pipe.reserve(F, len(ref["windows"]) + 64, caps=caps, max_boxes=len(boxes))
     frames = S.frame_pixels_torch([S.frame_seed(0, f) for f in range(F)], cfg.H, cfg.pitch, device=G.DEV)
     pipe.plan(torch.from_numpy(scores).to(G.DEV))
-    pipe.gather(mp.WindowPipeline.frame_ptrs(frames))
+    pipe.gather(frames)
     pipe.merge(G.boxes_to_t(boxes), torch.from_numpy(wbo).to(G.DEV))
     torch.cuda.synchronize()
     pipe.check_status()
