@@ -30,14 +30,14 @@
 namespace mpk {
 
 constexpr int kProducerWarps = 1;
-constexpr int kCW = 4;   // consumer warps per CTA; each owns a block of TR/kCW output rows
-constexpr int kStages = 4;
+constexpr int kCW = 8;   // consumer warps per CTA; each owns a block of TR/kCW output rows
+constexpr int kStages = 2;
 constexpr int kHdrBytes = 64;
 constexpr int kMaxTW = 256;
-constexpr int kMaxTR = 64;
+constexpr int kMaxTR = 96;
 constexpr int kXtapBytes = (kMaxTW + 2) * 8, kYtapBytes = (kMaxTR + 2) * 8;
 constexpr int kTapBytes = kXtapBytes + kYtapBytes;
-constexpr int kStageDataBudget = 24 * 1024;
+constexpr int kStageDataBudget = 44 * 1024;
 constexpr int kDataOff = (kHdrBytes + kTapBytes + 127) / 128 * 128;   // TMA destination: 128-B aligned
 
 struct GatherArgs {
