@@ -1,7 +1,4 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-cp paper_2103_14695_b200/libmp_b200.so /tmp/base.so
-for f in .variants/lib_*.so; do v=$(basename $f .so); cp $f paper_2103_14695_b200/libmp_b200.so
-  timeout -s KILL 600 python bench.py --steps 100 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/bench_$v.log 2>&1
-done
-cp /tmp/base.so paper_2103_14695_b200/libmp_b200.so
+timeout -s KILL 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1
+for d in 1 2 3; do timeout -s KILL 600 python bench.py --steps 200 --warmup 10 --no-e2e --no-cpu-baseline --depth $d > gpurun_out/bench_d$d.log 2>&1; done

@@ -108,3 +108,60 @@ class WindowPipeline:
         F = frames.shape[0]
         step = frames.stride(0) * frames.element_size()
         return (torch.arange(F, dtype=torch.int64, device=frames.device) * step + frames.data_ptr()).contiguous()
+
+
+class PipelinedRunner:
+    """Software pipeline over consecutive batches on three CUDA streams:
+    plan(i+1) and remap/NMS(i-1) run while gather/resize(i) streams through HBM.
+
+    Each in-flight batch owns one WindowPipeline (double buffering: `depth`
+    sets of plan/gather/NMS buffers), so no stage of batch i+1 overwrites a
+    buffer a later stage of batch i still reads.  Ordering is enforced only
+    with CUDA events (no host synchronisation):
+        plan(i) -> gather(i) -> [detector] -> merge(i);  plan(i) waits merge(i-depth).
+    """
+
+    def __init__(self, pipes, device="cuda"):
+        self.pipes = list(pipes)
+        self.depth = len(self.pipes)
+        dev = torch.device(device)
+        self.s_plan = torch.cuda.Stream(dev)
+        self.s_gather = torch.cuda.Stream(dev)
+        self.s_merge = torch.cuda.Stream(dev)
+        self.done = [None] * self.depth
+        self.i = 0
+
+    def step(self, scores, frames, boxes=None, win_box_off=None, gather_events=None):
+        """Enqueue one batch.  `boxes`/`win_box_off` are the detector's output
+        for this batch (None skips the merge).  gather_events: optional
+        (start, end) CUDA events recorded around the gather on its stream."""
+        k = self.i % self.depth
+        p = self.pipes[k]
+        if self.done[k] is not None:
+            self.s_plan.wait_event(self.done[k])
+        p.plan(scores, stream=self.s_plan)
+        planned = torch.cuda.Event()
+        planned.record(self.s_plan)
+        self.s_gather.wait_event(planned)
+        if gather_events is not None:
+            gather_events[0].record(self.s_gather)
+        p.gather(frames, stream=self.s_gather)
+        if gather_events is not None:
+            gather_events[1].record(self.s_gather)
+        gathered = torch.cuda.Event()
+        gathered.record(self.s_gather)
+        self.s_merge.wait_event(gathered)
+        if boxes is not None:
+            p.merge(boxes, win_box_off, stream=self.s_merge)
+        done = torch.cuda.Event()
+        done.record(self.s_merge)
+        self.done[k] = done
+        self.i += 1
+        return p
+
+    def wait_all(self, stream=None):
+        """Make `stream` (default: current) wait for everything enqueued."""
+        s = torch.cuda.current_stream() if stream is None else stream
+        for e in self.done:
+            if e is not None:
+                s.wait_event(e)
