@@ -4,14 +4,16 @@
 // with class-aware greedy NMS over a shared-memory IoU bitmask.
 //
 // Launches:
-//   memset                      large-frame counter
-//   nms_small_kernel   F CTAs   frames with <= 512 raw boxes: remap, ordered
-//                               compaction, bitonic sort of (score desc, index)
-//                               keys, n x ceil(n/64) IoU bitmask, warp-0
-//                               greedy scan; larger frames are queued
-//   nms_large_kernel   #SM CTAs queued frames (<= 2048 raw boxes; bitmask up
-//                               to 1024 candidates, on-the-fly suppression
-//                               beyond)
+//   memset                      tier queue counters
+//   nms_tiny_kernel    F warps  one warp per frame with <= 64 raw boxes: remap,
+//                               ballot compaction, rank sort of the (score
+//                               desc, index) keys, 64-bit IoU row masks, greedy
+//                               scan; larger frames are queued
+//   nms_small_kernel   4/SM     queued frames with <= 512 raw boxes, one CTA each:
+//                               block compaction, bitonic sort, n x ceil(n/64)
+//                               IoU bitmask, warp-0 greedy scan
+//   nms_large_kernel   1/SM     queued frames (<= 2048 raw boxes; bitmask up to
+//                               1024 candidates, on-the-fly suppression beyond)
 //   nms_scan_kernel    1 CTA    kept-box CSR per frame, capacity check
 //   nms_scatter_kernel          compact kept boxes into the caller's buffers
 #include "mp_internal.cuh"
@@ -257,31 +259,155 @@ __device__ __forceinline__ bool frame_range(const NmsArgs& A, int f, const int* 
   return b_lo >= 0 && b_hi >= b_lo && b_hi <= A.max_boxes;
 }
 
-__global__ void __launch_bounds__(kSmallThreads) nms_small_kernel(NmsArgs A, const mp_box* __restrict__ boxes,
-                                                                  const int* __restrict__ win_box_off,
-                                                                  const mp_window* __restrict__ windows,
-                                                                  const int* __restrict__ frame_off,
-                                                                  mp_box* __restrict__ ws_box, int* __restrict__ ws_src,
-                                                                  int* __restrict__ ws_kept, int* __restrict__ large_cnt,
-                                                                  int* __restrict__ large_list, int* __restrict__ d_status) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int f = blockIdx.x;
+constexpr int kTinyCap = 64, kTinyWarps = 8;
+
+struct TinyWarpSmem {
+  float4 bx[kTinyCap];
+  unsigned long long key[kTinyCap];
+  unsigned long long mask[kTinyCap];
+  int cls[kTinyCap];
+  float score[kTinyCap];
+  int src[kTinyCap];
+  int order[kTinyCap];
+  int keep[kTinyCap];
+};
+
+// One warp per frame (frames with <= 64 raw boxes; the typical case).  Same
+// semantics and arithmetic as nms_frame (R18-R20); candidate index = position
+// in input order, rank sort by unique (score desc, index) keys.
+__global__ void __launch_bounds__(32 * kTinyWarps) nms_tiny_kernel(NmsArgs A, const mp_box* __restrict__ boxes,
+                                                                   const int* __restrict__ win_box_off,
+                                                                   const mp_window* __restrict__ windows,
+                                                                   const int* __restrict__ frame_off,
+                                                                   mp_box* __restrict__ ws_box, int* __restrict__ ws_src,
+                                                                   int* __restrict__ ws_kept, int* __restrict__ mid_cnt,
+                                                                   int* __restrict__ mid_list, int* __restrict__ d_status) {
+  __shared__ TinyWarpSmem sm_all[kTinyWarps];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int f = blockIdx.x * kTinyWarps + wid;
+  if (f >= A.F) return;
+  TinyWarpSmem& S = sm_all[wid];
   int w_lo, w_hi, b_lo, b_hi;
   if (!frame_range(A, f, frame_off, win_box_off, w_lo, w_hi, b_lo, b_hi)) {
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
       ws_kept[f] = 0;
       set_status(d_status, MP_ERR_INVALID);
     }
     return;
   }
-  if (b_hi - b_lo > kSmallCap) {
-    if (threadIdx.x == 0) large_list[atomicAdd(large_cnt, 1)] = f;
+  if (b_hi - b_lo > kTinyCap) {
+    if (lane == 0) mid_list[atomicAdd(mid_cnt, 1)] = f;
     return;
   }
+  // ---- a6: remap + ordered ballot compaction
+  int n = 0;
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const int b = b_lo + h * 32 + lane;
+    bool ok = false;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    mp_box bb;
+    if (b < b_hi) {
+      const int wi = window_of(win_box_off, w_lo, w_hi, b);
+      const mp_window w = windows[wi];
+      bb = boxes[b];
+      const int q = w.size_idx;
+      ok = (q >= 0 && q < A.k) && remap(bb, w, A.ow[q], A.oh[q], A.score_thr, o);
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, ok);
+    if (ok) {
+      const int p = n + __popc(m & lanemask_lt());
+      S.bx[p] = o;
+      S.cls[p] = bb.cls;
+      S.score[p] = bb.score;
+      S.src[p] = b;
+      S.key[p] = ((unsigned long long)score_desc_bits(bb.score) << 32) | (unsigned)p;
+    }
+    n += __popc(m);
+  }
+  __syncwarp();
+  // ---- rank sort (keys are unique)
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const int p = h * 32 + lane;
+    if (p < n) {
+      const unsigned long long kp = S.key[p];
+      int rank = 0;
+      for (int q2 = 0; q2 < n; q2++) rank += (S.key[q2] < kp) ? 1 : 0;
+      S.order[rank] = p;
+    }
+  }
+  __syncwarp();
+  // ---- a7: IoU row masks over later candidates of the same class
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const int i = h * 32 + lane;
+    if (i < n) {
+      const int qi = S.order[i];
+      const float4 bi = S.bx[qi];
+      const int ci = S.cls[qi];
+      unsigned long long bits = 0;
+      for (int j = i + 1; j < n; j++) {
+        const int qj = S.order[j];
+        if (S.cls[qj] == ci && iou_rn(bi, S.bx[qj]) > A.iou_thr) bits |= 1ull << j;
+      }
+      S.mask[i] = bits;
+    }
+  }
+  __syncwarp();
+  int nk = 0;
+  if (lane == 0) {
+    unsigned long long removed = 0;
+    for (int i = 0; i < n; i++) {
+      if (!((removed >> i) & 1ull)) {
+        S.keep[nk++] = i;
+        removed |= S.mask[i];
+      }
+    }
+  }
+  nk = __shfl_sync(0xffffffffu, nk, 0);
+  __syncwarp();
+  for (int r = lane; r < nk; r += 32) {
+    const int q = S.order[S.keep[r]];
+    const float4 o = S.bx[q];
+    mp_box ob;
+    ob.x1 = o.x;
+    ob.y1 = o.y;
+    ob.x2 = o.z;
+    ob.y2 = o.w;
+    ob.score = S.score[q];
+    ob.cls = S.cls[q];
+    ws_box[b_lo + r] = ob;
+    ws_src[b_lo + r] = S.src[q];
+  }
+  if (lane == 0) ws_kept[f] = nk;
+}
+
+// Queued frames with 65..512 raw boxes, one CTA per frame (persistent).
+__global__ void __launch_bounds__(kSmallThreads) nms_small_kernel(NmsArgs A, const mp_box* __restrict__ boxes,
+                                                                  const int* __restrict__ win_box_off,
+                                                                  const mp_window* __restrict__ windows,
+                                                                  const int* __restrict__ frame_off,
+                                                                  mp_box* __restrict__ ws_box, int* __restrict__ ws_src,
+                                                                  int* __restrict__ ws_kept, const int* __restrict__ mid_cnt,
+                                                                  const int* __restrict__ mid_list, int* __restrict__ large_cnt,
+                                                                  int* __restrict__ large_list, int* __restrict__ d_status) {
+  extern __shared__ __align__(16) unsigned char smem[];
   NmsSmem S;
   nms_smem_bytes(kSmallCap, kSmallCap, &S, smem);
-  nms_frame(A, f, b_lo, b_hi, w_lo, w_hi, S, kSmallCap, kSmallCap, boxes, win_box_off, windows, ws_box, ws_src,
-            ws_kept);
+  const int nm = *mid_cnt;
+  for (int li = blockIdx.x; li < nm; li += gridDim.x) {
+    const int f = mid_list[li];
+    int w_lo, w_hi, b_lo, b_hi;
+    frame_range(A, f, frame_off, win_box_off, w_lo, w_hi, b_lo, b_hi);
+    if (b_hi - b_lo > kSmallCap) {
+      if (threadIdx.x == 0) large_list[atomicAdd(large_cnt, 1)] = f;
+      continue;
+    }
+    nms_frame(A, f, b_lo, b_hi, w_lo, w_hi, S, kSmallCap, kSmallCap, boxes, win_box_off, windows, ws_box, ws_src,
+              ws_kept);
+    __syncthreads();
+  }
 }
 
 __global__ void __launch_bounds__(kLargeThreads) nms_large_kernel(NmsArgs A, const mp_box* __restrict__ boxes,
@@ -346,7 +472,7 @@ __global__ void __launch_bounds__(256) nms_scatter_kernel(int F, const int* __re
 }
 
 struct NmsWs {
-  size_t box_off, src_off, kept_off, lcnt_off, llist_off, total;
+  size_t box_off, src_off, kept_off, lcnt_off, llist_off, mlist_off, total;
 };
 
 static NmsWs nms_ws_layout(int F, int max_boxes) {
@@ -355,9 +481,10 @@ static NmsWs nms_ws_layout(int F, int max_boxes) {
   L.box_off = 0;
   L.src_off = al(sizeof(mp_box) * (size_t)max_boxes);
   L.kept_off = al(L.src_off + sizeof(int) * (size_t)max_boxes);
-  L.lcnt_off = al(L.kept_off + sizeof(int) * (size_t)F);
-  L.llist_off = al(L.lcnt_off + sizeof(int));
-  L.total = al(L.llist_off + sizeof(int) * (size_t)F) + 256;
+  L.lcnt_off = al(L.kept_off + sizeof(int) * (size_t)F);   // [0] large count, [1] mid count
+  L.llist_off = al(L.lcnt_off + 2 * sizeof(int));
+  L.mlist_off = al(L.llist_off + sizeof(int) * (size_t)F);
+  L.total = al(L.mlist_off + sizeof(int) * (size_t)F) + 256;
   return L;
 }
 
@@ -402,19 +529,25 @@ extern "C" mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_bo
   int* ws_kept = (int*)(ws + L.kept_off);
   int* lcnt = (int*)(ws + L.lcnt_off);
   int* llist = (int*)(ws + L.llist_off);
+  int* mcnt = lcnt + 1;
+  int* mlist = (int*)(ws + L.mlist_off);
   cudaStream_t s = (cudaStream_t)stream;
   if (F > 0) {
-    MP_CUDA_TRY(cudaMemsetAsync(lcnt, 0, sizeof(int), s));
+    MP_CUDA_TRY(cudaMemsetAsync(lcnt, 0, 2 * sizeof(int), s));
     const size_t sm_small = nms_smem_bytes(kSmallCap, kSmallCap, nullptr, nullptr);
     const size_t sm_large = nms_smem_bytes(kLargeCap, kLargeMaskCap, nullptr, nullptr);
     MP_CUDA_TRY(cudaFuncSetAttribute(nms_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_small));
     MP_CUDA_TRY(cudaFuncSetAttribute(nms_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_large));
-    nms_small_kernel<<<F, kSmallThreads, sm_small, s>>>(A, d_boxes, d_win_box_off, d_windows, d_frame_off, ws_box,
-                                                        ws_src, ws_kept, lcnt, llist, d_status);
+    nms_tiny_kernel<<<(F + kTinyWarps - 1) / kTinyWarps, 32 * kTinyWarps, 0, s>>>(
+        A, d_boxes, d_win_box_off, d_windows, d_frame_off, ws_box, ws_src, ws_kept, mcnt, mlist, d_status);
     MP_CUDA_TRY(cudaGetLastError());
     int dev = 0, sms = 0;
     MP_CUDA_TRY(cudaGetDevice(&dev));
     MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    nms_small_kernel<<<sms * 4, kSmallThreads, sm_small, s>>>(A, d_boxes, d_win_box_off, d_windows, d_frame_off,
+                                                             ws_box, ws_src, ws_kept, mcnt, mlist, lcnt, llist,
+                                                             d_status);
+    MP_CUDA_TRY(cudaGetLastError());
     nms_large_kernel<<<sms, kLargeThreads, sm_large, s>>>(A, d_boxes, d_win_box_off, d_windows, d_frame_off,
                                                           ws_box, ws_src, ws_kept, lcnt, llist, d_status);
     MP_CUDA_TRY(cudaGetLastError());

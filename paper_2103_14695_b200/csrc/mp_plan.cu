@@ -122,15 +122,30 @@ __global__ void __launch_bounds__(kPlanThreads) plan_frames_kernel(PlanArgs P, c
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
   const float* sc = scores + (size_t)f * R * C;
 
-  // ---- a1: threshold, one warp-ballot per 32 cells of a row (R2)
-  for (int rw = wid; rw < R * words; rw += nwarps) {
-    const int r = rw / words, w = rw - r * words, c = w * 32 + lane;
-    bool pos = false;
-    if (c < C) pos = __ldg(sc + (size_t)r * C + c) > P.b;   // NaN -> false
-    const uint32_t m = __ballot_sync(0xffffffffu, pos);
-    if (lane == 0) {
-      S.bits[rw] = m;
-      if (mask_out) mask_out[(size_t)f * R * words + rw] = m;
+  // ---- a1: threshold, one warp-ballot per 32 cells of a row (R2);
+  // four (row, word) loads per warp in flight before the ballots.
+  const int RW = R * words;
+  for (int base = wid; base < RW; base += 4 * nwarps) {
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int rw = base + u * nwarps;
+      v[u] = -INFINITY;
+      if (rw < RW) {
+        const int r = rw / words, c = (rw - r * words) * 32 + lane;
+        if (c < C) v[u] = __ldg(sc + (size_t)r * C + c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int rw = base + u * nwarps;
+      if (rw < RW) {
+        const uint32_t m = __ballot_sync(0xffffffffu, v[u] > P.b);   // NaN -> false
+        if (lane == 0) {
+          S.bits[rw] = m;
+          if (mask_out) mask_out[(size_t)f * RW + rw] = m;
+        }
+      }
     }
   }
   __syncthreads();
