@@ -18,6 +18,7 @@ bounded sample of the same workload (rank 0 only).
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import math
 import os
@@ -334,13 +335,15 @@ def run_b200(args):
     if not args.no_e2e:
         e2e = run_e2e(cfg, clip, scene, scores_np, boxes, wbo, fmt, dev, args)
 
-    frames_done = torch.tensor([F * args.steps], dtype=torch.int64, device=dev)
-    tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(frames_done, op=dist.ReduceOp.SUM)
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    total_frames = int(frames_done.item())
-    tmax_ms = float(tmax.item())
+    # the only cross-GPU traffic: int64 counters (SUM) and elapsed time (MAX) over NCCL
+    from paper_2103_14695_b200.sharding import Counters, reduce_counters
+    full = len(cfg.sizes) - 1
+    mine = Counters(frames=F * args.steps, windows=n_win * args.steps,
+                    fallback_frames=int((windows[:, 5] == full).sum()) * args.steps,
+                    crop_bytes=int(ab["read_union"]) * args.steps, out_bytes=int(ab["out"]) * args.steps,
+                    boxes_in=len(boxes) * args.steps, boxes_kept=n_kept * args.steps, clips=1)
+    glob, tmax_ms = reduce_counters(mine, elapsed_ms, device=dev)
+    total_frames = glob.frames
     value = total_frames / (tmax_ms * 1e-3)
 
     if rank == 0:
@@ -376,6 +379,7 @@ def run_b200(args):
             "e2e": e2e,
             "gpu_launches": args.steps * (mp.launches_per_call(0) + mp.launches_per_call(1) +
                                           mp.launches_per_call(2)),
+            "counters": dataclasses.asdict(glob),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
