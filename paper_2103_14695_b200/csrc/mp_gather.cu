@@ -5,23 +5,23 @@
 // carries ~99% of the path's bytes.
 //
 // Launches:
-//   gather_prep_kernel   one CTA: validate windows (n_win read on device),
-//                        count windows per class, build per-class slot ->
-//                        window descriptors (crop origin pointer, x), and the
-//                        per-class exact integer tap tables (i0, lambda) for
-//                        both axes (R15).
-//   gather_kernel<fmt>   persistent, warp-specialised, Grid = SMs x resident
-//                        CTAs.  Warps 8-9 = producers (alternate tiles): one
-//                        descriptor + 4 tap loads per tile, copy the tile's tap
-//                        slices into the stage header, then stage the tile's
-//                        source box into a 4-deep shared-memory ring completing
-//                        on an mbarrier (complete_tx): ONE 3-D TMA tensor copy
-//                        (cp.async.bulk.tensor, per-class tensor map over the
-//                        frame batch) on the strided entry point, or one 1-D
+//   memset               per-class window counters
+//   gather_prep_kernel   grid-stride over the windows (n_win read on device):
+//                        validate, count per class (shared then one global
+//                        atomic per CTA), per-class slot -> window index lists,
+//                        and the per-class exact integer tap tables (i0,
+//                        lambda) for both axes (R15).
+//   gather_kernel<fmt>   persistent, warp-specialised, one CTA per SM.
+//                        Warp 8 = producer: the next tile's window record and
+//                        tap bounds are prefetched while it waits for a free
+//                        stage; then the tile's tap slices (two 1-D bulk copies)
+//                        and its source box (ONE 3-D TMA tensor copy over the
+//                        frame batch on the strided entry point, or one 1-D
 //                        bulk copy per source row on the pointer-array entry
-//                        point.  Warps 0-7 = consumers: two output columns per
-//                        thread (packed f32x2 math), separable lerps reusing
-//                        staged rows, streaming stores.
+//                        point) land in a 2-stage shared-memory ring completing
+//                        on an mbarrier (complete_tx).  Warps 0-7 = consumers:
+//                        output columns lane + 32j (packed f32x2 math),
+//                        separable lerps reusing staged rows, streaming stores.
 #include <cuda.h>
 #include <stdlib.h>
 
@@ -50,11 +50,6 @@ struct GatherArgs {
   void* out[kMaxClasses];
 };
 
-// Per listed window (indexed by class list offset + slot): frame, x, y, valid.
-struct WinDesc {
-  int frame, x, y, valid;
-};
-static_assert(sizeof(WinDesc) == 16, "desc");
 
 // One TMA tensor map per size class (box = the class's staged tile footprint).
 struct TmapArray {
@@ -104,30 +99,31 @@ __device__ __forceinline__ int tiles_total(const GatherArgs& A, const int* cnt) 
   return T;
 }
 
-__global__ void __launch_bounds__(1024) gather_prep_kernel(GatherArgs A, const mp_window* __restrict__ win,
-                                                           const int* __restrict__ frame_off,
-                                                           int* __restrict__ ws_cnt, WinDesc* __restrict__ ws_desc,
-                                                           int2* __restrict__ ws_tap, int desc_total,
-                                                           int* __restrict__ d_status) {
+constexpr int kPrepThreads = 256;
+
+__global__ void __launch_bounds__(kPrepThreads) gather_prep_kernel(GatherArgs A, const mp_window* __restrict__ win,
+                                                                   const int* __restrict__ frame_off,
+                                                                   int* __restrict__ ws_cnt, int* __restrict__ ws_list,
+                                                                   int2* __restrict__ ws_tap, int n_taps,
+                                                                   int* __restrict__ d_status) {
   __shared__ int cnt[kMaxClasses];
   if (threadIdx.x < kMaxClasses) cnt[threadIdx.x] = 0;
-  for (int i = threadIdx.x; i < desc_total; i += blockDim.x) ws_desc[i] = WinDesc{0, 0, 0, 0};
-  // tap tables: x taps of class q at xtab_off[q] (ow entries), y taps at ytab_off[q]
-  for (int q = 0; q < A.k; q++) {
-    for (int d = threadIdx.x; d < A.ow[q]; d += blockDim.x) {
-      int i0; float lam;
-      tap(A.w[q], A.ow[q], d, i0, lam);
-      ws_tap[A.xtab_off[q] + d] = make_int2(i0, __float_as_int(lam));
-    }
-    for (int d = threadIdx.x; d < A.oh[q]; d += blockDim.x) {
-      int i0; float lam;
-      tap(A.h[q], A.oh[q], d, i0, lam);
-      ws_tap[A.ytab_off[q] + d] = make_int2(i0, __float_as_int(lam));
-    }
-  }
   __syncthreads();
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  // tap tables: entry e -> (class, axis, d); x taps of class q at xtab_off[q], y taps at ytab_off[q]
+  for (int e = gtid; e < n_taps; e += gstride) {
+    int q = 0;
+    while (q + 1 < A.k && e >= A.xtab_off[q + 1]) q++;
+    const bool xaxis = e < A.ytab_off[q];
+    const int d = xaxis ? e - A.xtab_off[q] : e - A.ytab_off[q];
+    int i0;
+    float lam;
+    if (xaxis) tap(A.w[q], A.ow[q], d, i0, lam);
+    else tap(A.h[q], A.oh[q], d, i0, lam);
+    ws_tap[e] = make_int2(i0, __float_as_int(lam));
+  }
   const int n_win = frame_off[A.F];
-  for (int i = threadIdx.x; i < n_win; i += blockDim.x) {
+  for (int i = gtid; i < n_win; i += gstride) {
     const mp_window w = win[i];
     const int q = w.size_idx;
     if (q < 0 || q >= A.k || w.frame < 0 || w.frame >= A.F || w.w != A.w[q] || w.h != A.h[q] || w.x < 0 ||
@@ -140,10 +136,10 @@ __global__ void __launch_bounds__(1024) gather_prep_kernel(GatherArgs A, const m
       set_status(d_status, MP_ERR_CAPACITY);
       continue;
     }
-    ws_desc[A.list_off[q] + w.slot] = WinDesc{w.frame, w.x, w.y, 1};
+    ws_list[A.list_off[q] + w.slot] = i;
   }
   __syncthreads();
-  if (threadIdx.x < kMaxClasses) ws_cnt[threadIdx.x] = cnt[threadIdx.x];
+  if (threadIdx.x < A.k && cnt[threadIdx.x]) atomicAdd(&ws_cnt[threadIdx.x], cnt[threadIdx.x]);
 }
 
 // Consumer: warp `wid` owns output rows [wid*R, (wid+1)*R) of the tile
@@ -293,7 +289,9 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
                                                                  const __grid_constant__ TmapArray tm,
                                                                  const uint8_t* const* __restrict__ frames,
                                                                  const int* __restrict__ ws_cnt,
-                                                                 const WinDesc* __restrict__ ws_desc,
+                                                                 const int* __restrict__ ws_list,
+                                                                 const mp_window* __restrict__ windows,
+                                                                 const int* __restrict__ frame_off,
                                                                  const int2* __restrict__ ws_tap,
                                                                  int* __restrict__ d_status) {
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * A.stage_bytes);
@@ -336,11 +334,27 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
       ti.rows = min(A.TR[q], A.oh[q] - ti.oy0);
       ti.cols = min(A.TW[q], A.ow[q] - ti.ox0);
     };
+    struct WinRef {
+      int frame, x, y, valid;
+    };
+    const int n_win = frame_off[A.F];
     TileInfo cur, nxt;
-    WinDesc dcur = WinDesc{0, 0, 0, 0}, dnxt = dcur;
+    WinRef dcur = WinRef{0, 0, 0, 0}, dnxt = dcur;
     int clo_cur = 0, rlo_cur = 0, rhi_cur = 0, clo_nxt = 0, rlo_nxt = 0, rhi_nxt = 0;
-    auto prefetch = [&](const TileInfo& ti, WinDesc& d, int& clo, int& rlo, int& rhi) {
-      d = ws_desc[A.list_off[ti.q] + ti.slot];
+    auto prefetch = [&](const TileInfo& ti, WinRef& d, int& clo, int& rlo, int& rhi) {
+      // the class list entry must point at a window of this class and slot
+      // (catches slots that are not 0..count-1 without zero-filling the list)
+      const int wi = ws_list[A.list_off[ti.q] + ti.slot];
+      d.valid = 0;
+      if (wi >= 0 && wi < n_win) {
+        const mp_window w = windows[wi];
+        d.frame = w.frame;
+        d.x = w.x;
+        d.y = w.y;
+        d.valid = (w.size_idx == ti.q && w.slot == ti.slot && w.frame >= 0 && w.frame < A.F && w.x >= 0 &&
+                   w.y >= 0 && w.w == A.w[ti.q] && w.h == A.h[ti.q] && w.x + w.w <= A.W && w.y + w.h <= A.H)
+                      ? 1 : 0;
+      }
       clo = __ldg(&ws_tap[A.xtab_off[ti.q] + ti.ox0].x);
       rlo = __ldg(&ws_tap[A.ytab_off[ti.q] + ti.oy0].x);
       rhi = __ldg(&ws_tap[A.ytab_off[ti.q] + ti.oy0 + ti.rows - 1].x);
@@ -555,7 +569,7 @@ static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_si
 using namespace mpk;
 
 struct GatherWs {
-  size_t cnt_off, desc_off, tap_off, total;
+  size_t cnt_off, list_off, tap_off, total;
 };
 
 static bool gather_ws_layout(int32_t k, const mp_size* out_dims, const int32_t* out_cap, GatherWs* L) {
@@ -568,8 +582,8 @@ static bool gather_ws_layout(int32_t k, const mp_size* out_dims, const int32_t* 
   }
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   L->cnt_off = 0;
-  L->desc_off = 256;
-  L->tap_off = al(L->desc_off + desc * sizeof(WinDesc));
+  L->list_off = 256;
+  L->tap_off = al(L->list_off + desc * sizeof(int));
   L->total = al(L->tap_off + taps * sizeof(int2));
   return true;
 }
@@ -589,14 +603,15 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
                                int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
   GatherWs L;
   if (!gather_ws_layout(k, out_dims, out_cap, &L) || !d_ws || ws_bytes < L.total) return MP_ERR_INVALID;
-  int desc_total = 0;
-  for (int q = 0; q < k; q++) desc_total += out_cap[q];
+  int n_taps = 0;
+  for (int q = 0; q < k; q++) n_taps += out_dims[q].w + out_dims[q].h;
   cudaStream_t s = (cudaStream_t)stream;
   unsigned char* ws = (unsigned char*)d_ws;
   int* ws_cnt = (int*)(ws + L.cnt_off);
-  WinDesc* ws_desc = (WinDesc*)(ws + L.desc_off);
+  int* ws_list = (int*)(ws + L.list_off);
   int2* ws_tap = (int2*)(ws + L.tap_off);
-  gather_prep_kernel<<<1, 1024, 0, s>>>(A, d_windows, d_frame_off, ws_cnt, ws_desc, ws_tap, desc_total, d_status);
+  MP_CUDA_TRY(cudaMemsetAsync(ws_cnt, 0, kMaxClasses * sizeof(int), s));
+  gather_prep_kernel<<<256, kPrepThreads, 0, s>>>(A, d_windows, d_frame_off, ws_cnt, ws_list, ws_tap, n_taps, d_status);
   MP_CUDA_TRY(cudaGetLastError());
   if (A.F == 0) return MP_OK;
   const size_t smem = (size_t)kStages * A.stage_bytes + 2 * kStages * sizeof(uint64_t);
@@ -613,7 +628,8 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
     MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
     if (per_sm < 1) per_sm = 1;
-    kern<<<sms * per_sm, threads, smem, s>>>(A, tm, d_frame_ptrs, ws_cnt, ws_desc, ws_tap, d_status);
+    kern<<<sms * per_sm, threads, smem, s>>>(A, tm, d_frame_ptrs, ws_cnt, ws_list, d_windows, d_frame_off, ws_tap,
+                                             d_status);
     MP_CUDA_TRY(cudaGetLastError());
     return MP_OK;
   };
