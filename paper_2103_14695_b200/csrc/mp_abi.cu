@@ -13,12 +13,12 @@ extern "C" const char* mp_status_string(mp_status st) {
 }
 
 // Kernel launches per call (for bench.py's gpu_launches count):
-//   plan: plan_frames + plan_scan + plan_scatter
+//   plan: memset (not a kernel) + plan_fast + plan_full + plan_scan + plan_scatter
 //   gather: gather_prep + gather_kernel
 //   remap_nms: memset (not a kernel) + tiny + small + large + scan + scatter
 extern "C" int32_t mp_launches_per_call(int32_t which) {
   switch (which) {
-    case 0: return 3;
+    case 0: return 4;
     case 1: return 2;
     case 2: return 5;
   }

@@ -4,10 +4,15 @@
 // window per cluster.  Readings R1-R14 are in DESIGN.md §3.
 //
 // Launches (all on the caller's stream, no host sync):
-//   K1-K3 plan_frames_kernel   one CTA per frame: ballot threshold -> run
-//                              extraction -> shared-memory union-find over
-//                              runs -> component bboxes -> warp-0 greedy merge
-//                              -> placement into per-frame scratch
+//   memset                     tier queue counter
+//   K1-K3 plan_fast_kernel     one 128-thread CTA per frame (shared memory for
+//                              <= 256 runs): ballot threshold -> run extraction
+//                              -> shared-memory union-find over runs ->
+//                              component bboxes -> warp-0 greedy merge ->
+//                              placement into per-frame scratch; frames with
+//                              more runs are queued
+//         plan_full_kernel     persistent over the queue, shared memory for
+//                              R*ceil(C/2) runs (checkerboard worst case)
 //   K4a   plan_scan_kernel     one CTA: frame CSR + per-class slot bases
 //   K4b   plan_scatter_kernel  warp per frame: final window records + slots
 #include <climits>
@@ -106,18 +111,21 @@ __host__ __device__ inline size_t plan_smem_bytes(int R, int words, int maxc, Pl
   return off;
 }
 
-constexpr int kPlanThreads = 256;
+constexpr int kPlanThreads = 256;      // full-capacity tier
+constexpr int kFastThreads = 128;      // fast tier: frames with <= kFastCap runs
+constexpr int kFastCap = 256;
 
-__global__ void __launch_bounds__(kPlanThreads) plan_frames_kernel(PlanArgs P, const float* __restrict__ scores,
-                                                                   uint32_t* __restrict__ mask_out,
-                                                                   int4* __restrict__ ws_win,
-                                                                   int* __restrict__ ws_count,
-                                                                   int* __restrict__ ws_cls) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+extern __shared__ __align__(16) unsigned char smem_raw[];
+
+// The whole per-frame plan (a1-a4) with the CTA; `cap` = run/component
+// capacity of the shared-memory layout.  Returns false (having queued the
+// frame) if the frame has more runs than `cap`.
+__device__ __forceinline__ bool plan_frame(const PlanArgs& P, int f, int cap, const float* __restrict__ scores,
+                                           uint32_t* __restrict__ mask_out, int4* __restrict__ ws_win,
+                                           int* __restrict__ ws_count, int* __restrict__ ws_cls,
+                                           int* __restrict__ q_cnt, int* __restrict__ q_list) {
   PlanSmem S;
-  plan_smem_bytes(P.R, P.words, P.maxc, &S, smem_raw);
-
-  const int f = blockIdx.x;
+  plan_smem_bytes(P.R, P.words, cap, &S, smem_raw);
   const int R = P.R, C = P.C, words = P.words;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
   const float* sc = scores + (size_t)f * R * C;
@@ -163,6 +171,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_frames_kernel(PlanArgs P, c
   }
   __syncthreads();
   const int nruns = block_excl_scan_smem(S.row_off, R, S.tmp);
+  if (nruns > cap) {   // too many runs for this tier's shared memory: queue for the full tier
+    if (tid == 0) q_list[atomicAdd(q_cnt, 1)] = f;
+    return false;
+  }
   for (int r = tid; r < R; r += blockDim.x) {
     const int base = S.row_off[r];
     int ns = 0, ne = 0;
@@ -235,7 +247,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_frames_kernel(PlanArgs P, c
   }
   if (tid < kMaxClasses) S.run[tid] = 0;
   __syncthreads();
-  if (wid != 0) return;
+  if (wid != 0) return true;
 
   // ---- a3: greedy agglomerative merge, warp 0 ------------
   const long long* T = P.cost;
@@ -352,7 +364,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_frames_kernel(PlanArgs P, c
       ws_count[f] = 1;
       for (int kk = 0; kk < P.k; kk++) ws_cls[(size_t)f * P.k + kk] = (kk == P.full) ? 1 : 0;
     }
-    return;
+    return true;
   }
   for (int base = 0; base < n; base += 32) {
     const int q = base + lane;
@@ -377,6 +389,28 @@ __global__ void __launch_bounds__(kPlanThreads) plan_frames_kernel(PlanArgs P, c
   __syncwarp();
   if (lane == 0) ws_count[f] = n;
   for (int kk = lane; kk < P.k; kk += 32) ws_cls[(size_t)f * P.k + kk] = S.run[kk];
+  return true;
+}
+
+__global__ void __launch_bounds__(kFastThreads) plan_fast_kernel(PlanArgs P, const float* __restrict__ scores,
+                                                                  uint32_t* __restrict__ mask_out,
+                                                                  int4* __restrict__ ws_win, int* __restrict__ ws_count,
+                                                                  int* __restrict__ ws_cls, int* __restrict__ q_cnt,
+                                                                  int* __restrict__ q_list) {
+  plan_frame(P, blockIdx.x, min(kFastCap, P.maxc), scores, mask_out, ws_win, ws_count, ws_cls, q_cnt, q_list);
+}
+
+// Persistent over the frames the fast tier queued (dense / checkerboard grids).
+__global__ void __launch_bounds__(kPlanThreads) plan_full_kernel(PlanArgs P, const float* __restrict__ scores,
+                                                                 uint32_t* __restrict__ mask_out,
+                                                                 int4* __restrict__ ws_win, int* __restrict__ ws_count,
+                                                                 int* __restrict__ ws_cls, const int* __restrict__ q_cnt,
+                                                                 const int* __restrict__ q_list) {
+  const int nq = *q_cnt;
+  for (int qi = blockIdx.x; qi < nq; qi += gridDim.x) {
+    plan_frame(P, q_list[qi], P.maxc, scores, mask_out, ws_win, ws_count, ws_cls, nullptr, nullptr);
+    __syncthreads();
+  }
 }
 
 __global__ void __launch_bounds__(1024) plan_scan_kernel(int F, int k, int* __restrict__ ws_count,
@@ -485,7 +519,7 @@ static bool build_plan_args(const mp_plan_params* p, PlanArgs* A, mp_status* err
 }
 
 struct PlanWs {
-  size_t win_off, count_off, cls_off, total;
+  size_t win_off, count_off, cls_off, q_off, total;
 };
 
 static PlanWs plan_ws_layout(const PlanArgs& A, int F) {
@@ -494,7 +528,8 @@ static PlanWs plan_ws_layout(const PlanArgs& A, int F) {
   L.win_off = 0;
   L.count_off = al(L.win_off + sizeof(int4) * (size_t)F * A.maxc);
   L.cls_off = al(L.count_off + sizeof(int) * (size_t)F);
-  L.total = al(L.cls_off + sizeof(int) * (size_t)F * A.k) + 256;
+  L.q_off = al(L.cls_off + sizeof(int) * (size_t)F * A.k);   // [0] queue count, [1..F] queued frames
+  L.total = al(L.q_off + sizeof(int) * (size_t)(F + 1)) + 256;
   return L;
 }
 
@@ -526,12 +561,25 @@ extern "C" mp_status mp_plan_windows(const mp_plan_params* p, const float* d_sco
   int4* ws_win = (int4*)(ws + L.win_off);
   int* ws_count = (int*)(ws + L.count_off);
   int* ws_cls = (int*)(ws + L.cls_off);
+  int* q_cnt = (int*)(ws + L.q_off);
+  int* q_list = q_cnt + 1;
   if (F > 0) {
     const size_t smem = plan_smem_bytes(A.R, A.words, A.maxc, nullptr, nullptr);
     if (smem > 227 * 1024) return MP_ERR_UNSUPPORTED;
-    MP_CUDA_TRY(cudaFuncSetAttribute(plan_frames_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-    plan_frames_kernel<<<F, kPlanThreads, smem, s>>>(A, d_scores, d_mask, ws_win, ws_count, ws_cls);
+    const size_t smem_fast = plan_smem_bytes(A.R, A.words, kFastCap < A.maxc ? kFastCap : A.maxc, nullptr, nullptr);
+    MP_CUDA_TRY(cudaMemsetAsync(q_cnt, 0, sizeof(int), s));
+    MP_CUDA_TRY(cudaFuncSetAttribute(plan_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_fast));
+    MP_CUDA_TRY(cudaFuncSetAttribute(plan_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PlanArgs Af = A;   // the fast tier lays out shared memory for min(kFastCap, maxc) runs
+    plan_fast_kernel<<<F, kFastThreads, smem_fast, s>>>(Af, d_scores, d_mask, ws_win, ws_count, ws_cls, q_cnt,
+                                                         q_list);
+    MP_CUDA_TRY(cudaGetLastError());
+    int dev = 0, sms = 0;
+    MP_CUDA_TRY(cudaGetDevice(&dev));
+    MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    plan_full_kernel<<<sms * 2, kPlanThreads, smem, s>>>(A, d_scores, d_mask, ws_win, ws_count, ws_cls, q_cnt,
+                                                         q_list);
     MP_CUDA_TRY(cudaGetLastError());
   }
   plan_scan_kernel<<<1, 1024, 0, s>>>(F, A.k, ws_count, ws_cls, d_frame_off, d_class_count, max_windows,

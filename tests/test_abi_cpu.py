@@ -50,7 +50,7 @@ def test_library_is_sm100a(lib):
 def test_status_strings(lib):
     for code in range(5):
         assert lib.status_string(code).startswith("MP_")
-    assert lib.launches_per_call(0) == 3 and lib.launches_per_call(1) == 2 and lib.launches_per_call(2) == 5
+    assert lib.launches_per_call(0) == 4 and lib.launches_per_call(1) == 2 and lib.launches_per_call(2) == 5
 
 
 def test_workspace_queries(lib):
