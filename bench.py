@@ -279,6 +279,8 @@ def run_b200(args):
         pipes.append(p2)
     runner = mp.PipelinedRunner(pipes, device=dev)
     stream = torch.cuda.current_stream(dev)
+    if args.graphs:
+        runner.capture_graphs(scores, boxes_t, wbo_t)
 
     for _ in range(max(args.warmup, 0)):
         runner.step(scores, frames, boxes_t, wbo_t)
@@ -366,7 +368,8 @@ def run_b200(args):
                        "raw_boxes_per_step": int(len(boxes)), "kept_boxes_per_step": n_kept,
                        "l2": "inputs (%.1f GB frames) exceed L2; no flush" % (frames.numel() / 1e9),
                        "parallelism": f"clip-sharded x{world}",
-                       "pipeline": f"plan/gather/merge on 3 CUDA streams, {args.depth} buffer sets"},
+                       "pipeline": f"plan/gather/merge on 3 CUDA streams, {args.depth} buffer sets, "
+                                   f"plan/merge as CUDA graphs: {bool(args.graphs)}"},
             "roofline": {"bound": "hbm", "kernel": "gather_resize (prep + gather_kernel)",
                          "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -461,6 +464,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=2, help="batches in flight (buffer sets) in the stream pipeline")
+    ap.add_argument("--graphs", type=int, default=1, help="replay plan/merge as CUDA graphs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

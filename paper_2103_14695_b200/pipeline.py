@@ -131,6 +131,24 @@ class PipelinedRunner:
         self.done = [None] * self.depth
         self.i = 0
 
+    def capture_graphs(self, scores, boxes=None, win_box_off=None):
+        """Capture each pipeline's plan and merge calls (4 + 5 launches, all
+        latency-bound) as CUDA graphs over fixed input tensors; `step` then
+        replays them.  The gather stays a plain launch (2 kernels) so its
+        duration can be timed with events on its stream."""
+        self.g_plan, self.g_merge = [], []
+        for p in self.pipes:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.s_plan):
+                p.plan(scores, stream=self.s_plan)
+            self.g_plan.append(g)
+            if boxes is not None:
+                g2 = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g2, stream=self.s_merge):
+                    p.merge(boxes, win_box_off, stream=self.s_merge)
+                self.g_merge.append(g2)
+        torch.cuda.synchronize()
+
     def step(self, scores, frames, boxes=None, win_box_off=None, gather_events=None):
         """Enqueue one batch.  `boxes`/`win_box_off` are the detector's output
         for this batch (None skips the merge).  gather_events: optional
@@ -139,7 +157,11 @@ class PipelinedRunner:
         p = self.pipes[k]
         if self.done[k] is not None:
             self.s_plan.wait_event(self.done[k])
-        p.plan(scores, stream=self.s_plan)
+        if getattr(self, "g_plan", None):
+            with torch.cuda.stream(self.s_plan):
+                self.g_plan[k].replay()
+        else:
+            p.plan(scores, stream=self.s_plan)
         planned = torch.cuda.Event()
         planned.record(self.s_plan)
         self.s_gather.wait_event(planned)
@@ -152,7 +174,11 @@ class PipelinedRunner:
         gathered.record(self.s_gather)
         self.s_merge.wait_event(gathered)
         if boxes is not None:
-            p.merge(boxes, win_box_off, stream=self.s_merge)
+            if getattr(self, "g_merge", None):
+                with torch.cuda.stream(self.s_merge):
+                    self.g_merge[k].replay()
+            else:
+                p.merge(boxes, win_box_off, stream=self.s_merge)
         done = torch.cuda.Event()
         done.record(self.s_merge)
         self.done[k] = done
