@@ -364,8 +364,8 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
       prefetch(cur, dcur, clo_cur, rlo_cur, rhi_cur);
     }
     for (int i = 0;; i++) {
-      const int t = blockIdx.x + i * G;
-      if (t >= T) break;
+      const int t = blockIdx.x + i * G;   // round-robin: concurrently processed tiles are
+      if (t >= T) break;                   // neighbours in the frames and in the outputs
       const int s = i % kStages;
       if (t + G < T) {
         decode(t + G, nxt);
@@ -484,9 +484,12 @@ static void class_box(int in_w, int in_h, int ow, int oh, int TW, int TR, int* b
     int ox0 = ct * TW, cols = (TW < ow - ox0 ? TW : ow - ox0);
     host_tap(in_w, ow, ox0, &a, &b);
     host_tap(in_w, ow, ox0 + cols - 1, &c, &d);
-    if (c - a + 2 > max_cols) max_cols = c - a + 2;
+    // the right tap of the last column is staged only when it lies inside the
+    // crop; at the crop edge lambda = 0 and the +1 read lands in stage slack
+    const int c_hi = (c + 1 < in_w - 1) ? c + 1 : in_w - 1;
+    if (c_hi - a + 1 > max_cols) max_cols = c_hi - a + 1;
   }
-  *box_w = (3 * max_cols + 15 + 15) / 16 * 16;
+  *box_w = (3 * max_cols + 15 + 15) / 16 * 16;   // + up to 15 B of 16-B start alignment
   *box_h = max_rows;
 }
 
@@ -525,6 +528,8 @@ static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_si
     int TW = 0, TR = 0, bw = 0, bh = 0, best_area = 0;
     for (int nct = (ow + kMaxTW - 1) / kMaxTW; nct <= (ow + 31) / 32; nct++) {
       const int tw = (ow + nct - 1) / nct;
+      // rows per warp: the tallest tile whose box fits (measured on B200:
+      // beats minimising halo/ragged rows, per-tile overhead dominates)
       int Rw = 8, cbw = 0, cbh = 0;
       for (; Rw >= 1; Rw--) {
         class_box(w, h, ow, oh, tw, kCW * Rw, &cbw, &cbh);
