@@ -392,6 +392,69 @@ def run_b200(args):
     return 0
 
 
+def run_sweep(args):
+    """NEXT-1 measurement: the proxy-module caching sweep
+    over one clip of configs[4] (1800 x 1080p frames) and the 9 thresholds
+    0.1..0.9 — one plan per (frame, threshold) plus the recall test against
+    the scene's detections.  Metric: planned frame-thresholds per second."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2103_14695_b200 as mp
+    from paper_2103_14695_b200.sharding import Counters, reduce_counters
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cfg = S.CONFIGS["c5_1080p_clips"]
+    F = cfg.frames
+    scene = S.make_scene(cfg, rank, F)
+    scores = torch.from_numpy(S.score_grids(cfg, rank, scene)).to(dev)
+    dets_np = np.concatenate(scene.boxes).astype(np.float32)
+    det_off = torch.from_numpy(np.concatenate([[0], np.cumsum([len(b) for b in scene.boxes])]).astype(np.int32)).to(dev)
+    dets = torch.from_numpy(dets_np).to(dev)
+    th = list(S.B_SWEEP)
+    p = mp.PlanParams(cfg.W, cfg.H, cfg.sizes, cfg.cost)
+    out = torch.zeros((len(th), 5), dtype=torch.int64, device=dev)
+    ws = torch.empty(mp.mp_proxy_sweep_workspace_size(p, F), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        mp.mp_proxy_sweep(p, scores, F, th, dets, det_off, out, ws)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for _ in range(args.steps):
+        mp.mp_proxy_sweep(p, scores, F, th, dets, det_off, out, ws)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    res = out.cpu().numpy()
+    glob, tmax = reduce_counters(Counters(frames=F * len(th) * args.steps, windows=int(res[:, 1].sum()) * args.steps,
+                                          clips=1), ms, device=dev)
+    if rank == 0:
+        recall = (res[:, 3] / max(len(dets_np), 1)).round(4).tolist()
+        print(json.dumps({
+            "metric": "frame-thresholds/sec of the proxy-module caching sweep (NEXT-1)",
+            "value": glob.frames / (tmax * 1e-3), "unit": "frame-thresholds/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tmax / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32/f32",
+            "data": "synthetic", "config": {"workload": cfg.name, "frames": F, "thresholds": th,
+                                            "detections": int(len(dets_np))},
+            "result": {"cost_sum": res[:, 0].tolist(), "windows": res[:, 1].tolist(), "recall": recall},
+            "gpu_launches": args.steps * mp.launches_per_call(3)}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def run_e2e(cfg, clip, scene, scores_np, boxes, wbo, fmt, dev, args):
     """Same metric through WindowPipeline with HOST inputs: each step copies the
     clip's frames (from a pinned host pool), scores and detector boxes H2D and
@@ -465,10 +528,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=2, help="batches in flight (buffer sets) in the stream pipeline")
     ap.add_argument("--graphs", type=int, default=1, help="replay plan/merge as CUDA graphs")
+    ap.add_argument("--mode", default="path", choices=["path", "sweep"],
+                    help="path: the hot path a1-a7 (default); sweep: NEXT-1 proxy-module sweep")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
+    if args.mode == "sweep":
+        return run_sweep(args)
     return run_b200(args)
 
 

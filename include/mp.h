@@ -196,12 +196,51 @@ mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_box_off,
                        int32_t max_out, int32_t* d_out_frame_off, int32_t* d_status,
                        int32_t max_boxes, void* d_ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * NEXT-1: proxy-module caching sweep (§3.5.2 "Proxy Model
+ * Module").  "for each threshold B_j, we compute rectangular windows using the
+ * cell grouping method ... on each frame.  ... our runtime estimate for this
+ * resolution and threshold is T_proxy,i + sum_k T_{r_k.w, r_k.h} ... The recall
+ * is the fraction of detections computed by theta_best that are covered by
+ * rectangles in R_{i,j}."
+ *
+ * One call = one proxy resolution i (one score-grid geometry) and J thresholds.
+ * For every threshold the frames are planned exactly as mp_plan_windows does
+ * (a1-a4, same readings) and the per-threshold totals are accumulated:
+ *   cost_sum      sum over frames and windows of T (the detector part of the
+ *                 runtime estimate; the caller adds T_proxy,i)
+ *   windows       number of windows
+ *   full_frames   frames whose plan is the single full-frame window
+ *   dets_covered  detections lying entirely inside some window of their frame
+ *                 (reading R21: "covered" = contained, the detector must see
+ *                 the whole object in one window)
+ *   dets_touched  detections overlapping some window with positive area
+ *                 (SPEC.md:251's looser reading, reported alongside)
+ * recall_j = dets_covered / n_det.
+ *
+ *  p             planner parameters; p->b_proxy is ignored.
+ *  d_scores      device float [F][R][C].
+ *  thresholds    host float [J], 1 <= J <= 64.
+ *  d_dets        device float [n_det][4] (x1, y1, x2, y2) frame px, the theta_best
+ *                detections, frame-major; d_det_off device int32 [F+1] CSR.
+ *  d_out         device mp_sweep_result [J] (overwritten).
+ */
+typedef struct {
+  int64_t cost_sum, windows, full_frames, dets_covered, dets_touched;
+} mp_sweep_result;
+
+size_t mp_proxy_sweep_workspace_size(const mp_plan_params* p, int32_t F);
+
+mp_status mp_proxy_sweep(const mp_plan_params* p, const float* d_scores, int32_t F, const float* thresholds,
+                         int32_t J, const float* d_dets, const int32_t* d_det_off, mp_sweep_result* d_out,
+                         void* d_ws, size_t ws_bytes, void* stream);
+
 /* Human-readable name of a status code (static string, never NULL). */
 const char* mp_status_string(mp_status st);
 
-/* Number of device kernels the last-built library launches per call
- * (diagnostic, used by bench.py to count launches): which = 0 plan,
- * 1 gather, 2 remap_nms. */
+/* Number of device kernels the library launches per call (diagnostic, used
+ * by bench.py to count launches): which = 0 plan, 1 gather, 2 remap_nms,
+ * 3 proxy_sweep. */
 int32_t mp_launches_per_call(int32_t which);
 
 #ifdef __cplusplus

@@ -67,6 +67,8 @@ def lib():
         L.mpo_iou.argtypes = [BoxC, BoxC]
         L.mpo_remap_box.restype = i32
         L.mpo_remap_box.argtypes = [BoxC, i32, i32, i32, i32, i32, i32, f32, p]
+        L.mpo_proxy_sweep.restype = i32
+        L.mpo_proxy_sweep.argtypes = [i32, i32, i32, i32, i32, p, p, p, i32, p, i32, p, p, p]
         L.mpo_remap_nms.restype = i32
         L.mpo_remap_nms.argtypes = [p, p, p, p, i32, i32, p, i32, i32, f32, f32, p, p, i32, p]
         _lib = L
@@ -215,3 +217,25 @@ def remap_nms(boxes, win_box_off, windows, frame_off, out_dims, W, H, score_thr,
                              _ptr(ofo))
     n = min(int(ofo[F]), max_out)
     return dict(status=st, boxes=out[:n].copy(), src=src[:n].copy(), frame_off=ofo)
+
+
+# --------------------------------------------------------------------------- NEXT-1
+SWEEP_FIELDS = ("cost_sum", "windows", "full_frames", "dets_covered", "dets_touched")
+
+
+def proxy_sweep(W, H, cell_w, cell_h, sizes, cost, scores, thresholds, dets, det_off):
+    """Per-threshold totals.  dets float32 [n,4] frame px,
+    det_off int32 [F+1].  Returns (status, int64 [J,5])."""
+    s = np.ascontiguousarray(scores, dtype=np.float32)
+    F = s.shape[0]
+    sz = _sizes_arr(sizes)
+    cs = np.ascontiguousarray(np.asarray(cost, dtype=np.int64))
+    th = np.ascontiguousarray(np.asarray(thresholds, dtype=np.float32))
+    d = np.ascontiguousarray(np.asarray(dets, dtype=np.float32).reshape(-1, 4))
+    if len(d) == 0:
+        d = np.zeros((1, 4), np.float32)
+    do = np.ascontiguousarray(np.asarray(det_off, dtype=np.int32))
+    out = np.zeros((len(th), 5), np.int64)
+    st = lib().mpo_proxy_sweep(W, H, cell_w, cell_h, len(sz), _ptr(sz), _ptr(cs), _ptr(s), F, _ptr(th), len(th),
+                               _ptr(d), _ptr(do), _ptr(out))
+    return st, out

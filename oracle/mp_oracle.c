@@ -565,3 +565,55 @@ int32_t mpo_remap_nms(const mpo_box* boxes, const int32_t* win_box_off, const mp
   out_frame_off[F] = total;
   return status;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-1: proxy-module caching sweep, PAPER.md:281-283 (§3.5.2 "Proxy Model
+ * Module"): "for each threshold B_j, we compute rectangular windows using the
+ * cell grouping method ... on each frame ... our runtime estimate for this
+ * resolution and threshold is T_proxy,i + sum_k T_{r_k.w,r_k.h} ... The recall
+ * is the fraction of detections computed by theta_best that are covered by
+ * rectangles in R_{i,j}."  Per threshold: plan all frames (mpo_plan_windows),
+ * then per frame and detection test the frame's windows.  Reading R21:
+ * covered = the detection lies inside a window; touched = positive-area
+ * overlap.  out[5*j + {0..4}] = cost_sum, windows, full_frames,
+ * dets_covered, dets_touched. */
+int32_t mpo_proxy_sweep(int32_t W, int32_t H, int32_t cw, int32_t ch, int32_t k, const mpo_size* sizes,
+                        const int64_t* cost, const float* scores, int32_t F, const float* thresholds,
+                        int32_t J, const float* dets, const int32_t* det_off, int64_t* out) {
+  int32_t R = (H + ch - 1) / ch, C = (W + cw - 1) / cw;
+  int64_t maxw = (int64_t)F * ((int64_t)R * ((C + 1) / 2) + 1) + 1;
+  mpo_window* win = (mpo_window*)malloc(sizeof(mpo_window) * maxw);
+  int32_t* frame_off = (int32_t*)malloc(sizeof(int32_t) * (F + 1));
+  int32_t* cc = (int32_t*)malloc(sizeof(int32_t) * (k > 0 ? k : 1));
+  int32_t full = -1;
+  for (int32_t q = 0; q < k; q++)
+    if (sizes[q].w == W && sizes[q].h == H) full = q;
+  int status = MPO_OK;
+  for (int32_t j = 0; j < J && status == MPO_OK; j++) {
+    int st = mpo_plan_windows(W, H, cw, ch, thresholds[j], k, sizes, cost, scores, F, NULL, win, (int32_t)maxw,
+                              frame_off, cc, NULL);
+    if (st != MPO_OK) { status = st; break; }
+    int64_t* o = out + 5 * j;
+    for (int32_t q = 0; q < 5; q++) o[q] = 0;
+    for (int32_t f = 0; f < F; f++) {
+      int32_t w0 = frame_off[f], w1 = frame_off[f + 1];
+      for (int32_t wi = w0; wi < w1; wi++) o[0] += cost[win[wi].size_idx];
+      o[1] += w1 - w0;
+      if (w1 - w0 == 1 && win[w0].size_idx == full) o[2] += 1;
+      for (int32_t d = det_off[f]; d < det_off[f + 1]; d++) {
+        float x1 = dets[4 * d], y1 = dets[4 * d + 1], x2 = dets[4 * d + 2], y2 = dets[4 * d + 3];
+        int in = 0, ov = 0;
+        for (int32_t wi = w0; wi < w1; wi++) {
+          float a0 = (float)win[wi].x, b0 = (float)win[wi].y;
+          float a1 = (float)(win[wi].x + win[wi].w), b1 = (float)(win[wi].y + win[wi].h);
+          if (x1 >= a0 && x2 <= a1 && y1 >= b0 && y2 <= b1) in = 1;
+          if (x1 < a1 && x2 > a0 && y1 < b1 && y2 > b0) ov = 1;
+        }
+        o[3] += in;
+        o[4] += ov;
+      }
+    }
+  }
+  free(win); free(frame_off); free(cc);
+  return status;
+}

@@ -62,6 +62,10 @@ def _load():
     L.mp_gather_resize_strided.restype = C.c_int
     L.mp_gather_resize_strided.argtypes = [vp, C.c_int64, i32, i32, i32, i32, vp, vp, i32, vp, vp, vp, vp, C.c_int,
                                            vp, vp, sz, vp]
+    L.mp_proxy_sweep_workspace_size.restype = sz
+    L.mp_proxy_sweep_workspace_size.argtypes = [C.POINTER(mp_plan_params), i32]
+    L.mp_proxy_sweep.restype = C.c_int
+    L.mp_proxy_sweep.argtypes = [C.POINTER(mp_plan_params), vp, i32, vp, i32, vp, vp, vp, vp, sz, vp]
     L.mp_remap_nms_workspace_size.restype = sz
     L.mp_remap_nms_workspace_size.argtypes = [i32, i32]
     L.mp_remap_nms.restype = C.c_int
@@ -73,7 +77,7 @@ def _load():
 _lib = _load()
 
 EXPORTED = ("mp_plan_workspace_size", "mp_plan_windows", "mp_gather_workspace_size", "mp_gather_resize",
-            "mp_gather_resize_strided",
+            "mp_gather_resize_strided", "mp_proxy_sweep_workspace_size", "mp_proxy_sweep",
             "mp_remap_nms_workspace_size", "mp_remap_nms", "mp_status_string", "mp_launches_per_call")
 
 
@@ -242,3 +246,24 @@ def mp_remap_nms(boxes, win_box_off, windows, frame_off, F, out_dims, W, H, scor
                            int(boxes.shape[0]), _p(ws), ws.numel(), _stream(stream))
     if st != MP_OK:
         raise MPError(st, "mp_remap_nms")
+
+
+def mp_proxy_sweep_workspace_size(params: PlanParams, F: int) -> int:
+    return int(_lib.mp_proxy_sweep_workspace_size(C.byref(params.c), int(F)))
+
+
+def mp_proxy_sweep(params: PlanParams, scores, F, thresholds, dets, det_off, out, ws, stream=None) -> None:
+    """NEXT-1 proxy-module sweep (PAPER.md:281-283).  scores float32 [F,R,C];
+    thresholds: host sequence of J floats; dets float32 [n,4] frame px;
+    det_off int32 [F+1]; out int64 [J,5] (cost_sum, windows, full_frames,
+    dets_covered, dets_touched)."""
+    _dev(scores, torch.float32, "scores")
+    _dev(dets, torch.float32, "dets")
+    _dev(det_off, torch.int32, "det_off")
+    _dev(out, torch.int64, "out")
+    _dev(ws, torch.uint8, "ws")
+    th = (C.c_float * len(thresholds))(*[float(t) for t in thresholds])
+    st = _lib.mp_proxy_sweep(C.byref(params.c), _p(scores), int(F), th, len(thresholds), _p(dets), _p(det_off),
+                             _p(out), _p(ws), ws.numel(), _stream(stream))
+    if st != MP_OK:
+        raise MPError(st, "mp_proxy_sweep")

@@ -16,11 +16,13 @@ extern "C" const char* mp_status_string(mp_status st) {
 //   plan: memset (not a kernel) + plan_fast + plan_full + plan_scan + plan_scatter
 //   gather: gather_prep + gather_kernel
 //   remap_nms: memset (not a kernel) + tiny + small + large + scan + scatter
+//   proxy_sweep: memset (not a kernel) + proxy_sweep_kernel
 extern "C" int32_t mp_launches_per_call(int32_t which) {
   switch (which) {
     case 0: return 4;
     case 1: return 2;
     case 2: return 5;
+    case 3: return 1;
   }
   return 0;
 }

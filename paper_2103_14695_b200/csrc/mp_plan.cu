@@ -458,6 +458,66 @@ __global__ void __launch_bounds__(256) plan_scatter_kernel(PlanArgs P, int F, co
   }
 }
 
+// ------------------------------------------------------------------ NEXT-1 proxy sweep
+constexpr int kSweepMaxJ = 64;
+constexpr int kSweepThreads = 256;
+struct SweepThr {
+  float v[kSweepMaxJ];
+};
+
+// One CTA per frame; for each threshold the frame is planned exactly as in
+// mp_plan_windows (plan_frame, full capacity), then the frame's detections are
+// tested against its windows; per-threshold totals are reduced in shared
+// memory and added to the output with one int64 atomic per field per CTA.
+__global__ void __launch_bounds__(kSweepThreads) proxy_sweep_kernel(PlanArgs P, const float* __restrict__ scores,
+                                                                    SweepThr thr, int J,
+                                                                    const float4* __restrict__ dets,
+                                                                    const int* __restrict__ det_off,
+                                                                    int4* __restrict__ ws_win, int* __restrict__ ws_count,
+                                                                    int* __restrict__ ws_cls,
+                                                                    unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long acc[5];
+  __shared__ float s_thr[kSweepMaxJ];
+  const int f = blockIdx.x, tid = threadIdx.x;
+  if (tid < J) s_thr[tid] = thr.v[tid];
+  const int d_lo = det_off[f], d_hi = det_off[f + 1];
+  for (int j = 0; j < J; j++) {
+    if (tid < 5) acc[tid] = 0;
+    __syncthreads();
+    PlanArgs Pj = P;
+    Pj.b = s_thr[j];
+    plan_frame(Pj, f, P.maxc, scores, nullptr, ws_win, ws_count, ws_cls, nullptr, nullptr);
+    __syncthreads();   // warp 0's scratch writes are visible to the CTA
+    const int n = ws_count[f];
+    const int4* wl = ws_win + (size_t)f * P.maxc;
+    unsigned long long cost = 0, cov = 0, touch = 0;
+    for (int q = tid; q < n; q += blockDim.x) cost += (unsigned long long)P.cost[wl[q].z];
+    for (int d = d_lo + tid; d < d_hi; d += blockDim.x) {
+      const float4 b = dets[d];
+      bool in = false, ov = false;
+      for (int q = 0; q < n; q++) {
+        const int4 w = wl[q];
+        const float x0 = (float)w.x, y0 = (float)w.y;
+        const float x1 = (float)(w.x + P.sw[w.z]), y1 = (float)(w.y + P.sh[w.z]);
+        in |= (b.x >= x0) && (b.z <= x1) && (b.y >= y0) && (b.w <= y1);
+        ov |= (b.x < x1) && (b.z > x0) && (b.y < y1) && (b.w > y0);
+      }
+      cov += in ? 1 : 0;
+      touch += ov ? 1 : 0;
+    }
+    if (cost) atomicAdd(&acc[0], cost);
+    if (cov) atomicAdd(&acc[3], cov);
+    if (touch) atomicAdd(&acc[4], touch);
+    if (tid == 0) {
+      acc[1] = n;
+      acc[2] = (n == 1 && wl[0].z == P.full) ? 1 : 0;
+    }
+    __syncthreads();
+    if (tid < 5 && acc[tid]) atomicAdd(&out[5 * j + tid], acc[tid]);
+    __syncthreads();   // scratch and acc are reused by the next threshold
+  }
+}
+
 // ------------------------------------------------------------------ host side
 static bool build_plan_args(const mp_plan_params* p, PlanArgs* A, mp_status* err) {
   *err = MP_ERR_INVALID;
@@ -590,5 +650,41 @@ extern "C" mp_status mp_plan_windows(const mp_plan_params* p, const float* d_sco
                                                     max_windows);
     MP_CUDA_TRY(cudaGetLastError());
   }
+  return MP_OK;
+}
+
+extern "C" size_t mp_proxy_sweep_workspace_size(const mp_plan_params* p, int32_t F) {
+  return mp_plan_workspace_size(p, F);
+}
+
+extern "C" mp_status mp_proxy_sweep(const mp_plan_params* p, const float* d_scores, int32_t F,
+                                    const float* thresholds, int32_t J, const float* d_dets,
+                                    const int32_t* d_det_off, mp_sweep_result* d_out, void* d_ws, size_t ws_bytes,
+                                    void* stream) {
+  PlanArgs A;
+  mp_status err;
+  if (!build_plan_args(p, &A, &err)) return err;
+  if (F < 0 || J < 1 || J > kSweepMaxJ || !thresholds || !d_out || !d_det_off) return MP_ERR_INVALID;
+  if (F > 0 && (!d_scores || !d_dets)) return MP_ERR_INVALID;
+  for (int j = 0; j < J; j++)
+    if (!(thresholds[j] == thresholds[j])) return MP_ERR_INVALID;
+  const PlanWs L = plan_ws_layout(A, F);
+  if (ws_bytes < L.total || !d_ws) return MP_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned char* ws = (unsigned char*)d_ws;
+  int4* ws_win = (int4*)(ws + L.win_off);
+  int* ws_count = (int*)(ws + L.count_off);
+  int* ws_cls = (int*)(ws + L.cls_off);
+  // thresholds travel in the (graph-capturable) kernel parameter block
+  SweepThr th;
+  for (int j = 0; j < kSweepMaxJ; j++) th.v[j] = j < J ? thresholds[j] : 0.0f;
+  MP_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(mp_sweep_result) * (size_t)J, s));
+  if (F == 0) return MP_OK;
+  const size_t smem = plan_smem_bytes(A.R, A.words, A.maxc, nullptr, nullptr);
+  if (smem > 227 * 1024) return MP_ERR_UNSUPPORTED;
+  MP_CUDA_TRY(cudaFuncSetAttribute(proxy_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  proxy_sweep_kernel<<<F, kSweepThreads, smem, s>>>(A, d_scores, th, J, (const float4*)d_dets, d_det_off, ws_win,
+                                                    ws_count, ws_cls, (unsigned long long*)d_out);
+  MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
