@@ -52,7 +52,9 @@ __device__ __forceinline__ int uf_find(volatile int* parent, int x) {
     int p = parent[x];
     if (p == x) return x;
     int gp = parent[p];
-    if (gp != p) parent[x] = gp;   // path halving (benign: gp is an ancestor)
+    // path halving; the store is an atomic CAS so concurrent finds/links never
+    // race on a plain write (gp is an ancestor either way)
+    if (gp != p) atomicCAS(const_cast<int*>(parent + x), p, gp);
     x = p;
   }
 }
