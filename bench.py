@@ -455,6 +455,53 @@ def run_sweep(args):
     return 0
 
 
+def run_wsel(args):
+    """NEXT-2 measurement: one greedy step of the window-size selection
+     on configs[1]-shaped training frames with a perfect
+    proxy: every multiple-of-32 candidate (1,980 at 1080p) x 600 frames planned
+    in one launch.  Metric: candidate-frame plans per second."""
+    import torch
+
+    import paper_2103_14695_b200 as mp
+    from paper_2103_14695_b200 import window_sets
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    cfg = S.CONFIGS["c2_1080p_sparse"]
+    F = 600
+    scene = S.make_scene(cfg, 0, F)
+    lab = torch.from_numpy(np.stack([S.cell_labels(cfg, b) for b in scene.boxes]).astype(np.float32)).to(dev)
+    cost = lambda w, h: -(-w // 32) * -(-h // 32) + 16
+    Sset = [(cfg.W, cfg.H)]
+    cand = window_sets.candidate_sizes(cfg.W, cfg.H, Sset)
+    p = mp.PlanParams(cfg.W, cfg.H, Sset, [cost(*x) for x in Sset])
+    tot = torch.empty(len(cand), dtype=torch.int64, device=dev)
+    ws = torch.empty(mp.mp_window_set_cost_workspace_size(len(cand)), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    cc = [cost(*c) for c in cand]
+    for _ in range(max(1, args.warmup)):
+        mp.mp_window_set_cost(p, lab, F, cand, cc, tot, ws)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        mp.mp_window_set_cost(p, lab, F, cand, cc, tot, ws)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    t = tot.cpu().tolist()
+    best = min(range(len(cand)), key=lambda i: (t[i], cand[i][0] * cand[i][1], cand[i][0]))
+    sel, hist = window_sets.select_window_sizes(lab, cfg.W, cfg.H, 3, cost)
+    print(json.dumps({
+        "metric": "candidate-frame plans/sec of the window-size selection step (NEXT-2)",
+        "value": len(cand) * F * args.steps / (ms * 1e-3), "unit": "plans/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": cfg.name, "training_frames": F, "candidates": len(cand)},
+        "result": {"first_pick": cand[best], "k3_selection": sel, "tot_per_step": hist},
+        "gpu_launches": args.steps * mp.launches_per_call(4)}), flush=True)
+    return 0
+
+
 def run_e2e(cfg, clip, scene, scores_np, boxes, wbo, fmt, dev, args):
     """Same metric through WindowPipeline with HOST inputs: each step copies the
     clip's frames (from a pinned host pool), scores and detector boxes H2D and
@@ -528,14 +575,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=2, help="batches in flight (buffer sets) in the stream pipeline")
     ap.add_argument("--graphs", type=int, default=1, help="replay plan/merge as CUDA graphs")
-    ap.add_argument("--mode", default="path", choices=["path", "sweep"],
-                    help="path: the hot path a1-a7 (default); sweep: NEXT-1 proxy-module sweep")
+    ap.add_argument("--mode", default="path", choices=["path", "sweep", "wsel"],
+                    help="path: the hot path a1-a7 (default); sweep: NEXT-1 proxy-module sweep; "
+                         "wsel: NEXT-2 window-size selection step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
     if args.mode == "sweep":
         return run_sweep(args)
+    if args.mode == "wsel":
+        return run_wsel(args)
     return run_b200(args)
 
 

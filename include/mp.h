@@ -235,12 +235,41 @@ mp_status mp_proxy_sweep(const mp_plan_params* p, const float* d_scores, int32_t
                          int32_t J, const float* d_dets, const int32_t* d_det_off, mp_sweep_result* d_out,
                          void* d_ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * NEXT-2: window-size set selection (§3.3 "Determining Fixed
+ * Set of Window Sizes").  "on each iteration, we select the size (w,h) that
+ * minimizes tot_time(S + {(w,h)})", tot_time(S) = sum_t im_time(S, I_t) and
+ * im_time = est(R(I_t; S)) with "the proxy model perform[ing] perfectly"
+ * (positive cells = cells of the theta_best detections).
+ *
+ * mp_window_set_cost evaluates, for every candidate c, tot[c] = sum over the F
+ * frames of est(R(I_f; S + {cand[c]})) — one greedy step's objective for all
+ * candidates in one launch (grid frames x candidate blocks); the caller takes
+ * the arg-min (ties: smaller area, then smaller w — reading R22) and repeats
+ * k-1 times (paper_2103_14695_b200.window_sets.select_window_sizes).
+ *
+ *  p          the current set S (must contain (W,H)); p->b_proxy thresholds
+ *             d_scores (pass a perfect-proxy 0/1 grid and e.g. 0.5).
+ *  cand       host [n_cand] candidate sizes; cand_cost host [n_cand] their T;
+ *             every S + {cand[c]} must be a valid set (R13, distinct sizes),
+ *             else MP_ERR_INVALID.  |S| <= 15.
+ *  d_tot      device int64 [n_cand] (overwritten).
+ *  d_ws       device scratch, mp_window_set_cost_workspace_size(n_cand) bytes.
+ *  This offline call copies the candidate table to the device and
+ *  synchronises the stream once (not graph-capturable).
+ */
+size_t mp_window_set_cost_workspace_size(int32_t n_cand);
+
+mp_status mp_window_set_cost(const mp_plan_params* p, const float* d_scores, int32_t F, const mp_size* cand,
+                             const int64_t* cand_cost, int32_t n_cand, int64_t* d_tot, void* d_ws,
+                             size_t ws_bytes, void* stream);
+
 /* Human-readable name of a status code (static string, never NULL). */
 const char* mp_status_string(mp_status st);
 
 /* Number of device kernels the library launches per call (diagnostic, used
  * by bench.py to count launches): which = 0 plan, 1 gather, 2 remap_nms,
- * 3 proxy_sweep. */
+ * 3 proxy_sweep, 4 window_set_cost. */
 int32_t mp_launches_per_call(int32_t which);
 
 #ifdef __cplusplus

@@ -69,6 +69,8 @@ def lib():
         L.mpo_remap_box.argtypes = [BoxC, i32, i32, i32, i32, i32, i32, f32, p]
         L.mpo_proxy_sweep.restype = i32
         L.mpo_proxy_sweep.argtypes = [i32, i32, i32, i32, i32, p, p, p, i32, p, i32, p, p, p]
+        L.mpo_window_set_cost.restype = i32
+        L.mpo_window_set_cost.argtypes = [i32, i32, i32, i32, f32, i32, p, p, p, i32, p, p, i32, p]
         L.mpo_remap_nms.restype = i32
         L.mpo_remap_nms.argtypes = [p, p, p, p, i32, i32, p, i32, i32, f32, f32, p, p, i32, p]
         _lib = L
@@ -239,3 +241,38 @@ def proxy_sweep(W, H, cell_w, cell_h, sizes, cost, scores, thresholds, dets, det
     st = lib().mpo_proxy_sweep(W, H, cell_w, cell_h, len(sz), _ptr(sz), _ptr(cs), _ptr(s), F, _ptr(th), len(th),
                                _ptr(d), _ptr(do), _ptr(out))
     return st, out
+
+
+# --------------------------------------------------------------------------- NEXT-2
+def window_set_cost(W, H, cell_w, cell_h, b_proxy, sizes, cost, scores, cand, cand_cost):
+    """tot[c] = sum_t est(R(I_t; S + {cand[c]}))."""
+    s = np.ascontiguousarray(scores, dtype=np.float32)
+    sz = _sizes_arr(sizes)
+    cs = np.ascontiguousarray(np.asarray(cost, dtype=np.int64))
+    cd = _sizes_arr(cand)
+    cc = np.ascontiguousarray(np.asarray(cand_cost, dtype=np.int64))
+    tot = np.zeros(max(len(cd), 1), np.int64)
+    st = lib().mpo_window_set_cost(W, H, cell_w, cell_h, float(b_proxy), len(sz), _ptr(sz), _ptr(cs), _ptr(s),
+                                   s.shape[0], _ptr(cd), _ptr(cc), len(cd), _ptr(tot))
+    return st, tot[:len(cd)].copy()
+
+
+def select_window_sizes(W, H, cell_w, cell_h, scores, k, cost_fn, b_proxy=0.5, step=32):
+    """The greedy of PAPER.md:193-195: S = {full frame}; k-1 times add the
+    candidate (w, h), multiples of `step` no larger than the frame (not the full
+    frame, not already in S), minimising tot_time(S + {(w,h)}); ties -> smaller
+    area, then smaller w (reading R22).  Returns (sizes, [tot per step])."""
+    S = [(W, H)]
+    hist = []
+    for _ in range(k - 1):
+        cand = [(w, h) for w in range(step, W + 1, step) for h in range(step, H + 1, step)
+                if (w, h) != (W, H) and (w, h) not in S]
+        if not cand:
+            break
+        st, tot = window_set_cost(W, H, cell_w, cell_h, b_proxy, S, [cost_fn(*s) for s in S], scores, cand,
+                                  [cost_fn(*c) for c in cand])
+        assert st == OK, st
+        best = min(range(len(cand)), key=lambda i: (int(tot[i]), cand[i][0] * cand[i][1], cand[i][0]))
+        S.append(cand[best])
+        hist.append(int(tot[best]))
+    return S, hist

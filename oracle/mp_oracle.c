@@ -617,3 +617,36 @@ int32_t mpo_proxy_sweep(int32_t W, int32_t H, int32_t cw, int32_t ch, int32_t k,
   free(win); free(frame_off); free(cc);
   return status;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-2: window-size selection objective, PAPER.md:190-195 ("Determining
+ * Fixed Set of Window Sizes"): tot_time(S) = sum_t im_time(S, I_t),
+ * im_time(S, I_t) = est(R(I_t; S)) with the cell grouping method of P:184 and
+ * a perfect proxy (the caller passes 0/1 label grids).  For each candidate
+ * (w,h): S' = S + {(w,h)}; tot[c] = sum over frames of est of the plan (after
+ * the R11 fallback).  Plain loops over candidates and frames. */
+int32_t mpo_window_set_cost(int32_t W, int32_t H, int32_t cw, int32_t ch, float b_proxy, int32_t k,
+                            const mpo_size* sizes, const int64_t* cost, const float* scores, int32_t F,
+                            const mpo_size* cand, const int64_t* cand_cost, int32_t n_cand, int64_t* tot) {
+  int32_t R = (H + ch - 1) / ch, C = (W + cw - 1) / cw;
+  int64_t maxw = (int64_t)F * ((int64_t)R * ((C + 1) / 2) + 1) + 1;
+  mpo_window* win = (mpo_window*)malloc(sizeof(mpo_window) * maxw);
+  int32_t* frame_off = (int32_t*)malloc(sizeof(int32_t) * (F + 1));
+  mpo_size* sz = (mpo_size*)malloc(sizeof(mpo_size) * (k + 1));
+  int64_t* cs = (int64_t*)malloc(sizeof(int64_t) * (k + 1));
+  int32_t cc[17];
+  int status = MPO_OK;
+  for (int32_t q = 0; q < k; q++) { sz[q] = sizes[q]; cs[q] = cost[q]; }
+  for (int32_t c = 0; c < n_cand; c++) {
+    sz[k] = cand[c];
+    cs[k] = cand_cost[c];
+    int st = mpo_plan_windows(W, H, cw, ch, b_proxy, k + 1, sz, cs, scores, F, NULL, win, (int32_t)maxw,
+                              frame_off, cc, NULL);
+    if (st != MPO_OK) { status = st; break; }
+    int64_t t = 0;
+    for (int32_t i = 0; i < frame_off[F]; i++) t += cs[win[i].size_idx];
+    tot[c] = t;
+  }
+  free(win); free(frame_off); free(sz); free(cs);
+  return status;
+}

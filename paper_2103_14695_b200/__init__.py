@@ -10,5 +10,5 @@ from ._binding import (MP_ERR_CAPACITY, MP_ERR_CUDA, MP_ERR_INVALID, MP_ERR_UNSU
                        MP_OUT_F32_NCHW, MP_OUT_U8_NHWC, LIB_PATH, MPError, PlanParams, launches_per_call,
                        mp_gather_resize, mp_gather_resize_strided, mp_gather_workspace_size, mp_plan_windows, mp_plan_workspace_size,
                        mp_proxy_sweep, mp_proxy_sweep_workspace_size, mp_remap_nms, mp_remap_nms_workspace_size,
-                       status_string)
+                       mp_window_set_cost, mp_window_set_cost_workspace_size, status_string)
 from .pipeline import PipelinedRunner, WindowPipeline  # noqa: F401

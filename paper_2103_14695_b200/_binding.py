@@ -66,6 +66,10 @@ def _load():
     L.mp_proxy_sweep_workspace_size.argtypes = [C.POINTER(mp_plan_params), i32]
     L.mp_proxy_sweep.restype = C.c_int
     L.mp_proxy_sweep.argtypes = [C.POINTER(mp_plan_params), vp, i32, vp, i32, vp, vp, vp, vp, sz, vp]
+    L.mp_window_set_cost_workspace_size.restype = sz
+    L.mp_window_set_cost_workspace_size.argtypes = [i32]
+    L.mp_window_set_cost.restype = C.c_int
+    L.mp_window_set_cost.argtypes = [C.POINTER(mp_plan_params), vp, i32, vp, vp, i32, vp, vp, sz, vp]
     L.mp_remap_nms_workspace_size.restype = sz
     L.mp_remap_nms_workspace_size.argtypes = [i32, i32]
     L.mp_remap_nms.restype = C.c_int
@@ -78,6 +82,7 @@ _lib = _load()
 
 EXPORTED = ("mp_plan_workspace_size", "mp_plan_windows", "mp_gather_workspace_size", "mp_gather_resize",
             "mp_gather_resize_strided", "mp_proxy_sweep_workspace_size", "mp_proxy_sweep",
+            "mp_window_set_cost_workspace_size", "mp_window_set_cost",
             "mp_remap_nms_workspace_size", "mp_remap_nms", "mp_status_string", "mp_launches_per_call")
 
 
@@ -267,3 +272,22 @@ def mp_proxy_sweep(params: PlanParams, scores, F, thresholds, dets, det_off, out
                              _p(out), _p(ws), ws.numel(), _stream(stream))
     if st != MP_OK:
         raise MPError(st, "mp_proxy_sweep")
+
+
+def mp_window_set_cost_workspace_size(n_cand: int) -> int:
+    return int(_lib.mp_window_set_cost_workspace_size(int(n_cand)))
+
+
+def mp_window_set_cost(params: PlanParams, scores, F, cand, cand_cost, tot, ws, stream=None) -> None:
+    """NEXT-2 greedy-step objective: tot[c] = sum_t
+    est(R(I_t; S + {cand[c]})).  cand: host list of (w, h); cand_cost: host
+    list of T; tot int64 CUDA tensor [n_cand]."""
+    _dev(scores, torch.float32, "scores")
+    _dev(tot, torch.int64, "tot")
+    _dev(ws, torch.uint8, "ws")
+    n = len(cand)
+    cs = (C.c_int64 * max(n, 1))(*[int(c) for c in cand_cost])
+    st = _lib.mp_window_set_cost(C.byref(params.c), _p(scores), int(F), _sizes(cand) if n else None, cs, n, _p(tot),
+                                 _p(ws), ws.numel(), _stream(stream))
+    if st != MP_OK:
+        raise MPError(st, "mp_window_set_cost")

@@ -23,6 +23,7 @@ extern "C" int32_t mp_launches_per_call(int32_t which) {
     case 1: return 2;
     case 2: return 5;
     case 3: return 1;
+    case 4: return 1;
   }
   return 0;
 }

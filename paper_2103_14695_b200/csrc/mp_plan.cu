@@ -125,7 +125,8 @@ extern __shared__ __align__(16) unsigned char smem_raw[];
 __device__ __forceinline__ bool plan_frame(const PlanArgs& P, int f, int cap, const float* __restrict__ scores,
                                            uint32_t* __restrict__ mask_out, int4* __restrict__ ws_win,
                                            int* __restrict__ ws_count, int* __restrict__ ws_cls,
-                                           int* __restrict__ q_cnt, int* __restrict__ q_list) {
+                                           int* __restrict__ q_cnt, int* __restrict__ q_list,
+                                           long long* est_out = nullptr) {
   PlanSmem S;
   plan_smem_bytes(P.R, P.words, cap, &S, smem_raw);
   const int R = P.R, C = P.C, words = P.words;
@@ -359,6 +360,10 @@ __device__ __forceinline__ bool plan_frame(const PlanArgs& P, int f, int cap, co
   long long est = 0;
   for (int q = lane; q < n; q += 32) est += T[S.csz[q]];
   est = warp_sum_i64(est);
+  if (!ws_win) {   // estimate-only mode (window-size selection): est(R_t) after the R11 fallback
+    if (lane == 0) *est_out = (n > 0 && est > T[P.full]) ? T[P.full] : est;
+    return true;
+  }
   int4* out = ws_win + (size_t)f * P.maxc;
   if (n > 0 && est > T[P.full]) {
     if (lane == 0) {
@@ -517,6 +522,47 @@ __global__ void __launch_bounds__(kSweepThreads) proxy_sweep_kernel(PlanArgs P, 
     __syncthreads();
     if (tid < 5 && acc[tid]) atomicAdd(&out[5 * j + tid], acc[tid]);
     __syncthreads();   // scratch and acc are reused by the next threshold
+  }
+}
+
+// ------------------------------------------------------------------ NEXT-2 window-size selection
+constexpr int kSelThreads = 128;
+constexpr int kSelCandPerBlock = 16;
+
+// grid (F, ceil(n_cand / kSelCandPerBlock)): the CTA plans frame f once per
+// candidate size, with S' = S + {candidate} (order re-derived by (area, w, h)),
+// in estimate-only mode, and adds est(R(I_f; S')) to tot[c].
+__global__ void __launch_bounds__(kSelThreads) window_set_cost_kernel(PlanArgs P, const float* __restrict__ scores,
+                                                                      const int4* __restrict__ cand, int n_cand,
+                                                                      unsigned long long* __restrict__ tot) {
+  __shared__ long long s_est;
+  const int f = blockIdx.x;
+  const int c0 = blockIdx.y * kSelCandPerBlock, c1 = min(n_cand, c0 + kSelCandPerBlock);
+  for (int c = c0; c < c1; c++) {
+    const int4 cd = cand[c];   // (w, h, cost lo, cost hi)
+    PlanArgs Q = P;
+    const int kk = P.k;
+    Q.sw[kk] = cd.x;
+    Q.sh[kk] = cd.y;
+    Q.cost[kk] = (long long)(((unsigned long long)(unsigned)cd.w << 32) | (unsigned)cd.z);
+    Q.k = kk + 1;
+    // insert the candidate into the (area, w, h) order
+    const long long ac = (long long)cd.x * cd.y;
+    int pos = kk;
+    for (int q = 0; q < kk; q++) {
+      const int i = P.order[q];
+      const long long ai = (long long)P.sw[i] * P.sh[i];
+      if (ac < ai || (ac == ai && (cd.x < P.sw[i] || (cd.x == P.sw[i] && cd.y < P.sh[i])))) {
+        pos = q;
+        break;
+      }
+    }
+    for (int q = kk; q > pos; q--) Q.order[q] = P.order[q - 1];
+    Q.order[pos] = kk;
+    plan_frame(Q, f, P.maxc, scores, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &s_est);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_est) atomicAdd(&tot[c], (unsigned long long)s_est);
+    __syncthreads();
   }
 }
 
@@ -687,6 +733,67 @@ extern "C" mp_status mp_proxy_sweep(const mp_plan_params* p, const float* d_scor
   MP_CUDA_TRY(cudaFuncSetAttribute(proxy_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   proxy_sweep_kernel<<<F, kSweepThreads, smem, s>>>(A, d_scores, th, J, (const float4*)d_dets, d_det_off, ws_win,
                                                     ws_count, ws_cls, (unsigned long long*)d_out);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+extern "C" size_t mp_window_set_cost_workspace_size(int32_t n_cand) {
+  return n_cand < 0 ? 0 : ((size_t)n_cand * sizeof(int4) + 255) / 256 * 256 + 256;
+}
+
+extern "C" mp_status mp_window_set_cost(const mp_plan_params* p, const float* d_scores, int32_t F,
+                                        const mp_size* cand, const int64_t* cand_cost, int32_t n_cand,
+                                        int64_t* d_tot, void* d_ws, size_t ws_bytes, void* stream) {
+  PlanArgs A;
+  mp_status err;
+  if (!build_plan_args(p, &A, &err)) return err;
+  if (A.k >= kMaxClasses) return MP_ERR_UNSUPPORTED;
+  if (F < 0 || n_cand < 0 || (n_cand > 0 && (!cand || !cand_cost || !d_tot))) return MP_ERR_INVALID;
+  if (F > 0 && !d_scores) return MP_ERR_INVALID;
+  if (n_cand == 0) return MP_OK;
+  if (!d_ws || ws_bytes < mp_window_set_cost_workspace_size(n_cand)) return MP_ERR_INVALID;
+  // every S + {candidate} must itself be a valid size set (R13/R14)
+  int4* h = (int4*)malloc(sizeof(int4) * (size_t)n_cand);
+  if (!h) return MP_ERR_INVALID;
+  for (int c = 0; c < n_cand; c++) {
+    mp_size sz[kMaxClasses];
+    int64_t cs[kMaxClasses];
+    for (int q = 0; q < p->k; q++) {
+      sz[q] = p->sizes[q];
+      cs[q] = p->cost[q];
+    }
+    sz[p->k] = cand[c];
+    cs[p->k] = cand_cost[c];
+    mp_plan_params pc = *p;
+    pc.k = p->k + 1;
+    pc.sizes = sz;
+    pc.cost = cs;
+    PlanArgs tmp;
+    if (!build_plan_args(&pc, &tmp, &err)) {
+      free(h);
+      return MP_ERR_INVALID;
+    }
+    h[c] = make_int4(cand[c].w, cand[c].h, (int)(uint32_t)((uint64_t)cand_cost[c] & 0xffffffffu),
+                     (int)(uint32_t)((uint64_t)cand_cost[c] >> 32));
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  int4* d_cand = (int4*)d_ws;
+  // host -> device copy of the candidate table: stream-ordered from pageable
+  // memory (the call is therefore not graph-capturable; it is an offline step)
+  cudaError_t e = cudaMemcpyAsync(d_cand, h, sizeof(int4) * (size_t)n_cand, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  free(h);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return MP_ERR_CUDA;
+  }
+  MP_CUDA_TRY(cudaMemsetAsync(d_tot, 0, sizeof(int64_t) * (size_t)n_cand, s));
+  if (F == 0) return MP_OK;
+  const size_t smem = plan_smem_bytes(A.R, A.words, A.maxc, nullptr, nullptr);
+  if (smem > 227 * 1024) return MP_ERR_UNSUPPORTED;
+  MP_CUDA_TRY(cudaFuncSetAttribute(window_set_cost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid(F, (n_cand + kSelCandPerBlock - 1) / kSelCandPerBlock);
+  window_set_cost_kernel<<<grid, kSelThreads, smem, s>>>(A, d_scores, d_cand, n_cand, (unsigned long long*)d_tot);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
