@@ -23,6 +23,7 @@
 //                        output columns lane + 32j (packed f32x2 math),
 //                        separable lerps reusing staged rows, streaming stores.
 #include <cuda.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "mp_internal.cuh"
@@ -523,27 +524,51 @@ static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_si
     // class box, no over-fetch), NCOL = TW/32 rounded up to even columns per
     // lane; rows: kCW warps x Rw rows each, Rw as large as the stage budget
     // and the TMA box limits (256 rows, 256 x 8 bytes) allow (<= 8).
-    // Prefer the widest tiles whose box fits with >= 4 rows per warp; strong
-    // downscales of wide windows fall back to narrower column tiles.
-    int TW = 0, TR = 0, bw = 0, bh = 0, best_area = 0;
-    for (int nct = (ow + kMaxTW - 1) / kMaxTW; nct <= (ow + 31) / 32; nct++) {
-      const int tw = (ow + nct - 1) / nct;
-      // rows per warp: the tallest tile whose box fits (measured on B200:
-      // beats minimising halo/ragged rows, per-tile overhead dominates)
-      int Rw = 8, cbw = 0, cbh = 0;
-      for (; Rw >= 1; Rw--) {
-        class_box(w, h, ow, oh, tw, kCW * Rw, &cbw, &cbh);
-        if ((long long)cbw * cbh <= budget && cbw <= 2048 && cbh <= 256) break;
+    // Tile width (measured on B200): stores must start on full 128-B lines —
+    // so prefer the largest TW <= 256 that is a multiple of 32 and divides ow
+    // (equal tiles: every tile's TMA box is the class box, no over-fetch);
+    // else equal tiles rounded up to a multiple of 8 (full 32-B sectors).
+    // Rows per warp: the tallest Rw whose box fits the stage budget and the
+    // TMA limits.  Narrower fallbacks only when nothing fits.
+    int TW = 0, TR = 0, bw = 0, bh = 0;
+    auto fit_rows = [&](int tw, int& rw, int& cbw, int& cbh) {
+      for (rw = 8; rw >= 1; rw--) {
+        class_box(w, h, ow, oh, tw, kCW * rw, &cbw, &cbh);
+        if ((long long)cbw * cbh <= budget && cbw <= 2048 && cbh <= 256) return true;
       }
-      if (Rw < 1) continue;
-      if (tw * Rw > best_area) {
-        best_area = tw * Rw;
+      return false;
+    };
+    for (int tw = kMaxTW; tw >= 32 && !TW; tw -= 32) {
+      if (ow % tw) continue;
+      int rw, cbw, cbh;
+      if (fit_rows(tw, rw, cbw, cbh) && rw >= 3) {
         TW = tw;
-        TR = kCW * Rw;
+        TR = kCW * rw;
         bw = cbw;
         bh = cbh;
       }
-      if (Rw >= 4) break;
+    }
+    for (int nct = (ow + kMaxTW - 1) / kMaxTW; nct <= (ow + 7) / 8 && !TW; nct++) {
+      int tw = (ow + nct - 1) / nct;
+      tw = (tw + 7) / 8 * 8;
+      if (tw > kMaxTW) continue;
+      int rw, cbw, cbh;
+      if (fit_rows(tw, rw, cbw, cbh) && (rw >= 3 || tw <= 32)) {
+        TW = tw;
+        TR = kCW * rw;
+        bw = cbw;
+        bh = cbh;
+      }
+    }
+    {
+      // experiment knob: MP_GATHER_TILE=ow,TW,Rw forces the tile of classes with that output width
+      const char* ft = getenv("MP_GATHER_TILE");
+      int fow = 0, ftw = 0, frw = 0;
+      if (ft && sscanf(ft, "%d,%d,%d", &fow, &ftw, &frw) == 3 && fow == ow) {
+        TW = ftw;
+        TR = kCW * frw;
+        class_box(w, h, ow, oh, TW, TR, &bw, &bh);
+      }
     }
     if (TW == 0) return false;   // too strong a downscale of too wide a window: unsupported
     int ncol = (TW + 31) / 32;
