@@ -13,7 +13,7 @@
 //                               block compaction, bitonic sort, n x ceil(n/64)
 //                               IoU bitmask, warp-0 greedy scan
 //   nms_large_kernel   1/SM     queued frames (<= 2048 raw boxes; bitmask up to
-//                               1024 candidates, on-the-fly suppression beyond)
+//                               1024 candidates, tiled 64-candidate blocks beyond)
 //   nms_scan_kernel    1 CTA    kept-box CSR per frame, capacity check
 //   nms_scatter_kernel          compact kept boxes into the caller's buffers
 #include "mp_internal.cuh"
@@ -37,8 +37,10 @@ struct NmsSmem {
   int* order;
   int* keep;
   unsigned long long* key;    // sort keys, then reused for the IoU bitmask
-  unsigned char* supp;        // on-the-fly suppression flags (overlaps key/mask)
+  unsigned char* supp;        // tiled-path suppression flags (overlaps key/mask)
   int* tmp;
+  unsigned long long* bmask;  // tiled path: one 64-candidate block's IoU masks
+  int* bkeep;                 // tiled path: candidates kept in the current block
 };
 
 __host__ __device__ inline int pow2_at_least(int n) {
@@ -62,6 +64,8 @@ __host__ __device__ inline size_t nms_smem_bytes(int cap, int mask_cap, NmsSmem*
   s.order = (int*)take(sizeof(int) * cap);
   s.keep = (int*)take(sizeof(int) * cap);
   s.tmp = (int*)take(sizeof(int) * 64);
+  s.bmask = (unsigned long long*)take(sizeof(unsigned long long) * 64);
+  s.bkeep = (int*)take(sizeof(int) * 64);
   const size_t keyb = sizeof(unsigned long long) * pow2_at_least(cap);
   const size_t maskb = sizeof(unsigned long long) * (size_t)mask_cap * ((mask_cap + 63) / 64);
   size_t u = keyb > maskb ? keyb : maskb;
@@ -96,7 +100,11 @@ __device__ __forceinline__ float iou_rn(const float4 a, const float4 b) {
   const float iw = fmaxf(__fsub_rn(fminf(a.z, b.z), fmaxf(a.x, b.x)), 0.0f);
   const float ih = fmaxf(__fsub_rn(fminf(a.w, b.w), fmaxf(a.y, b.y)), 0.0f);
   const float inter = __fmul_rn(iw, ih);
-  return __fdiv_rn(inter, __fsub_rn(__fadd_rn(area_a, area_b), inter));
+  const float uni = __fsub_rn(__fadd_rn(area_a, area_b), inter);
+  // disjoint boxes (most pairs): 0 / uni is exactly 0 for uni > 0 -- skip the
+  // IEEE division, whose slow path (FCHK) a zero dividend always takes
+  if (inter == 0.0f && uni > 0.0f) return 0.0f;
+  return __fdiv_rn(inter, uni);
 }
 
 __device__ __forceinline__ unsigned int score_desc_bits(float s) {
@@ -216,20 +224,57 @@ __device__ void nms_frame(const NmsArgs& A, int f, int b_lo, int b_hi, int w_lo,
     __syncthreads();
     nk = S.tmp[32];
   } else {
+    // Tiled greedy for large frames (identical result to the sequential scan):
+    // for each block of 64 sorted candidates, (a) the block's 64x64 IoU masks,
+    // (b) one thread resolves the block sequentially against those masks and
+    // the suppression flags left by earlier blocks, (c) the whole CTA
+    // suppresses every later candidate overlapping a box kept in this block.
     for (int p = tid; p < n; p += blockDim.x) S.supp[p] = 0;
     __syncthreads();
-    for (int i = 0; i < n; i++) {
-      if (!S.supp[i]) {   // uniform across the CTA (read after the barrier)
+    for (int b0 = 0; b0 < n; b0 += 64) {
+      const int b1 = min(n, b0 + 64);
+      for (int i = b0 + tid; i < b1; i += blockDim.x) {
         const int qi = S.order[i];
         const float4 bi = S.bx[qi];
         const int ci = S.cls[qi];
-        if (tid == 0) S.keep[nk] = i;
-        nk++;
-        for (int j = i + 1 + tid; j < n; j += blockDim.x) {
+        unsigned long long bits = 0;
+        for (int j = i + 1; j < b1; j++) {
           const int qj = S.order[j];
-          if (!S.supp[j] && S.cls[qj] == ci && iou_rn(bi, S.bx[qj]) > A.iou_thr) S.supp[j] = 1;
+          if (S.cls[qj] == ci && iou_rn(bi, S.bx[qj]) > A.iou_thr) bits |= 1ull << (j - b0);
+        }
+        S.bmask[i - b0] = bits;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long removed = 0;
+        for (int i = b0; i < b1; i++)
+          if (S.supp[i]) removed |= 1ull << (i - b0);
+        int nb = 0;
+        for (int i = b0; i < b1; i++) {
+          if (!((removed >> (i - b0)) & 1ull)) {
+            S.keep[nk + nb] = i;
+            S.bkeep[nb++] = i;
+            removed |= S.bmask[i - b0];
+          }
+        }
+        S.tmp[33] = nb;
+      }
+      __syncthreads();
+      const int nb = S.tmp[33];
+      for (int j = b1 + tid; j < n; j += blockDim.x) {
+        if (S.supp[j]) continue;
+        const int qj = S.order[j];
+        const float4 bj = S.bx[qj];
+        const int cj = S.cls[qj];
+        for (int r = 0; r < nb; r++) {
+          const int qk = S.order[S.bkeep[r]];
+          if (S.cls[qk] == cj && iou_rn(S.bx[qk], bj) > A.iou_thr) {
+            S.supp[j] = 1;
+            break;
+          }
         }
       }
+      nk += nb;
       __syncthreads();
     }
   }

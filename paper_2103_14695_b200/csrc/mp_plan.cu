@@ -117,7 +117,128 @@ constexpr int kPlanThreads = 256;      // full-capacity tier
 constexpr int kFastThreads = 128;      // fast tier: frames with <= kFastCap runs
 constexpr int kFastCap = 256;
 
+constexpr int kCoopMergeMin = 96;   // components above which the whole CTA runs the merge
+
+// Block-wide minimum of a 64-bit key; `red` = 2 x 32 shared slots used
+// alternately (par) so consecutive calls need one barrier each.
+__device__ __forceinline__ unsigned long long block_min_u64(unsigned long long v, unsigned long long* red,
+                                                            int& par) {
+  v = warp_min_u64(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned long long* r = red + 32 * par;
+  if (lane == 0) r[wid] = v;
+  __syncthreads();
+  unsigned long long m = ~0ull;
+  for (int w = 0; w < nw; w++) m = r[w] < m ? r[w] : m;
+  par ^= 1;
+  return m;
+}
+
 extern __shared__ __align__(16) unsigned char smem_raw[];
+
+// a3 with the whole CTA (exactly the P:184 greedy of the warp-0 path below:
+// same nearest-neighbour metric and ties, same ascending absorption, strict
+// acceptance, remove + append); used when a frame has many components.
+__device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n) {
+  __shared__ unsigned long long red[64];
+  int par = 0;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, BS = blockDim.x;
+  const long long* T = P.cost;
+  bool again = true;
+  while (again) {
+    again = false;
+    int i = 0;
+    while (i < n && n >= 2) {
+      const int ic0 = S.bc0[i], ir0 = S.br0[i], ic1 = S.bc1[i], ir1 = S.br1[i];
+      const int sx = ic0 + ic1, sy = ir0 + ir1;
+      unsigned long long best = ~0ull;
+      for (int j = tid; j < n; j += BS) {
+        if (j == i) continue;
+        const int dx = sx - (S.bc0[j] + S.bc1[j]);
+        const int dy = sy - (S.br0[j] + S.br1[j]);
+        const unsigned long long key = ((unsigned long long)(unsigned)(dx * dx + dy * dy) << 32) | (unsigned)j;
+        best = key < best ? key : best;
+      }
+      best = block_min_u64(best, red, par);
+      const int j = (int)(best & 0xffffffffu);
+      int m0 = min(ic0, S.bc0[j]), n0 = min(ir0, S.br0[j]);
+      int m1 = max(ic1, S.bc1[j]), n1 = max(ir1, S.br1[j]);
+      int px0, py0, bw, bh;
+      extent(P, m0, n0, m1, n1, px0, py0, bw, bh);
+      const int s = smallest_size(P, bw, bh);
+      const int ws = P.sw[s], hs = P.sh[s];
+      long long sum = T[S.csz[i]] + T[S.csz[j]];
+      int before_i = (j < i) ? 1 : 0, n_abs = 0;
+      int pos = 0;
+      while (pos < n) {
+        const int q = pos + tid;
+        unsigned long long cand = ~0ull;
+        if (q < n && q != i && q != j) {
+          int qx, qy, qw, qh;
+          extent(P, min(m0, S.bc0[q]), min(n0, S.br0[q]), max(m1, S.bc1[q]), max(n1, S.br1[q]), qx, qy, qw, qh);
+          if (qw <= ws && qh <= hs) cand = (unsigned long long)q;
+        }
+        cand = block_min_u64(cand, red, par);
+        if (cand != ~0ull) {
+          const int qq = (int)cand;
+          m0 = min(m0, S.bc0[qq]);
+          n0 = min(n0, S.br0[qq]);
+          m1 = max(m1, S.bc1[qq]);
+          n1 = max(n1, S.br1[qq]);
+          sum += T[S.csz[qq]];
+          before_i += (qq < i) ? 1 : 0;
+          n_abs++;
+          if (tid == 0) S.memb[qq] = 1;
+          pos = qq + 1;
+        } else {
+          pos += BS;
+        }
+      }
+      if (tid == 0) {
+        S.memb[i] = 1;
+        S.memb[j] = 1;
+      }
+      __syncthreads();
+      if (T[s] < sum) {
+        if (wid == 0) {   // stable compaction + append (warp 0)
+          int wpos = 0;
+          for (int base = 0; base < n; base += 32) {
+            const int q = base + lane;
+            bool keep = false;
+            int v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+            unsigned char vs = 0;
+            if (q < n) {
+              keep = !S.memb[q];
+              v0 = S.bc0[q]; v1 = S.br0[q]; v2 = S.bc1[q]; v3 = S.br1[q]; vs = S.csz[q];
+            }
+            const uint32_t km = __ballot_sync(0xffffffffu, keep);
+            __syncwarp();
+            if (keep) {
+              const int d = wpos + __popc(km & lanemask_lt());
+              S.bc0[d] = v0; S.br0[d] = v1; S.bc1[d] = v2; S.br1[d] = v3; S.csz[d] = vs;
+            }
+            if (q < n) S.memb[q] = 0;
+            wpos += __popc(km);
+            __syncwarp();
+          }
+          if (lane == 0) {
+            S.bc0[wpos] = m0; S.br0[wpos] = n0; S.bc1[wpos] = m1; S.br1[wpos] = n1;
+            S.csz[wpos] = (unsigned char)s;
+          }
+        }
+        __syncthreads();
+        n = n - (2 + n_abs) + 1;   // members removed, merged cluster appended
+        again = true;
+        i -= before_i;
+      } else {
+        for (int q = tid; q < n; q += BS) S.memb[q] = 0;
+        __syncthreads();
+        i++;
+      }
+    }
+  }
+  return n;
+}
 
 // The whole per-frame plan (a1-a4) with the CTA; `cap` = run/component
 // capacity of the shared-memory layout.  Returns false (having queued the
@@ -250,12 +371,18 @@ __device__ __forceinline__ bool plan_frame(const PlanArgs& P, int f, int cap, co
   }
   if (tid < kMaxClasses) S.run[tid] = 0;
   __syncthreads();
-  if (wid != 0) return true;
-
-  // ---- a3: greedy agglomerative merge (PAPER.md:184), warp 0 ------------
   const long long* T = P.cost;
   int n = ncomp;
   bool again = n > 0;
+  if (ncomp > kCoopMergeMin) {
+    // many components: the CTA runs the greedy (same order rules) with block-wide
+    // arg-mins; warp 0 then only places the final clusters
+    n = coop_merge(P, S, ncomp);
+    again = false;
+  }
+  if (wid != 0) return true;
+
+  // ---- a3: greedy agglomerative merge (PAPER.md:184), warp 0 ------------
   while (again) {
     again = false;
     int i = 0;
