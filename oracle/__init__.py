@@ -63,6 +63,10 @@ def lib():
         L.mpo_taps.argtypes = [i32, i32, i32, p, p, p]
         L.mpo_gather_resize.restype = i32
         L.mpo_gather_resize.argtypes = [p, i32, i32, i32, i32, p, i32, i32, p, p, p, p, i32]
+        L.mpo_yuv_to_rgb.restype = i32
+        L.mpo_yuv_to_rgb.argtypes = [C.c_double, C.c_double, C.c_double, i32, p]
+        L.mpo_gather_resize_nv12.restype = i32
+        L.mpo_gather_resize_nv12.argtypes = [p, i32, i32, i32, i32, p, i32, i32, p, p, p, p, i32, i32]
         L.mpo_iou.restype = f32
         L.mpo_iou.argtypes = [BoxC, BoxC]
         L.mpo_remap_box.restype = i32
@@ -177,6 +181,47 @@ def gather_resize(frames, pitch, W, H, windows, sizes, out_dims, out_cap, fmt=F3
     optrs = (C.c_void_p * k)(*[o.ctypes.data for o in outs])
     st = lib().mpo_gather_resize(ptrs, pitch, W, H, F, _ptr(win), len(win), k, _ptr(sz),
                                  _ptr(od), optrs, _ptr(cap), fmt)
+    return st, outs
+
+
+# --------------------------------------------------------------------------- NEXT-3
+BT709_LIMITED, BT601_LIMITED, BT709_FULL, BT601_FULL = 0, 1, 2, 3
+
+
+def yuv_to_rgb(Y, U, V, matrix=BT709_LIMITED):
+    """R23 colour conversion of one (Y, U, V) triple -> clamped fp64 (R, G, B)."""
+    out = np.zeros(3, np.float64)
+    st = lib().mpo_yuv_to_rgb(float(Y), float(U), float(V), int(matrix), _ptr(out))
+    if st:
+        raise ValueError("bad matrix")
+    return out
+
+
+def gather_resize_nv12(frames, pitch, W, H, windows, sizes, out_dims, out_cap, fmt=F32_NCHW,
+                       matrix=BT709_LIMITED):
+    """frames: list/array of uint8 [H*3/2][pitch] NV12 host frames (Y rows then
+    interleaved UV rows).  Returns (status, [class tensors]) like gather_resize."""
+    fr = [np.ascontiguousarray(f, dtype=np.uint8) for f in frames]
+    for f in fr:
+        if f.shape != (H + H // 2, pitch):
+            raise ValueError("NV12 frame must be [H*3/2][pitch]")
+    F = len(fr)
+    ptrs = (C.c_void_p * max(F, 1))(*[f.ctypes.data for f in fr])
+    win = np.ascontiguousarray(np.asarray(windows, dtype=np.int32).reshape(-1, 7))
+    sz = _sizes_arr(sizes)
+    od = _sizes_arr(out_dims)
+    k = len(sz)
+    cap = np.ascontiguousarray(np.asarray(out_cap, dtype=np.int32))
+    outs = []
+    for i in range(k):
+        ow, oh = int(od[i, 0]), int(od[i, 1])
+        if fmt == U8_NHWC:
+            outs.append(np.zeros((cap[i], oh, ow, 3), np.uint8))
+        else:
+            outs.append(np.zeros((cap[i], 3, oh, ow), np.float64 if fmt == F64_NCHW else np.float32))
+    optrs = (C.c_void_p * k)(*[o.ctypes.data for o in outs])
+    st = lib().mpo_gather_resize_nv12(ptrs, pitch, W, H, F, _ptr(win), len(win), k, _ptr(sz),
+                                      _ptr(od), optrs, _ptr(cap), fmt, int(matrix))
     return st, outs
 
 

@@ -448,6 +448,116 @@ int32_t mpo_gather_resize(const uint8_t* const* frames, int32_t pitch, int32_t W
 }
 
 /* ------------------------------------------------------------------------ */
+/* NEXT-3: decode-native input.  The paper decodes
+ * with ffmpeg "at the object detector resolution" and feeds the proxy a
+ * low-resolution frame; it names no pixel format.  Reading R23
+ * (DESIGN.md §3): the decoder's output is NV12 — a Y plane [H][pitch] followed
+ * by an interleaved chroma plane [H/2][pitch] (U at even bytes, V at odd
+ * bytes), W and H even; chroma sample (i, j) covers luma (2i..2i+1, 2j..2j+1),
+ * i.e. the chroma value seen at luma position (r, c) is U[r>>1][2(c>>1)].
+ * Each of Y, U, V is resampled with the R15 taps of the luma grid exactly as
+ * one RGB channel is in mpo_gather_resize, then converted (ITU-R BT.601 /
+ * BT.709 Y'CbCr -> R'G'B' definitions, 8-bit):
+ *   Y' = (Y - yo) / ys,  Pb = (U - 128) / cs,  Pr = (V - 128) / cs
+ *   limited range: yo = 16, ys = 219, cs = 224;  full range: yo = 0, ys = cs = 255
+ *   R = 255 [Y' + 2(1-Kr) Pr]
+ *   G = 255 [Y' - 2Kb(1-Kb)/Kg Pb - 2Kr(1-Kr)/Kg Pr],  Kg = 1 - Kr - Kb
+ *   B = 255 [Y' + 2(1-Kb) Pb]
+ * then clamped to [0, 255]; f32/f64 out = clamped value, u8 out =
+ * floor(v + 0.5) (R16).  matrix 0 = BT.709 limited (Kr .2126, Kb .0722),
+ * 1 = BT.601 limited (Kr .299, Kb .114), 2 = BT.709 full, 3 = BT.601 full. */
+int32_t mpo_yuv_to_rgb(double Y, double U, double V, int32_t matrix, double* rgb) {
+  double Kr, Kb, yo, ys, cs;
+  if (matrix < 0 || matrix > 3) return MPO_ERR_INVALID;
+  Kr = (matrix & 1) ? 0.299 : 0.2126;
+  Kb = (matrix & 1) ? 0.114 : 0.0722;
+  if (matrix < 2) {
+    yo = 16.0;
+    ys = 219.0;
+    cs = 224.0;
+  } else {
+    yo = 0.0;
+    ys = 255.0;
+    cs = 255.0;
+  }
+  double Kg = 1.0 - Kr - Kb;
+  double y = (Y - yo) / ys, pb = (U - 128.0) / cs, pr = (V - 128.0) / cs;
+  double r = 255.0 * (y + 2.0 * (1.0 - Kr) * pr);
+  double g = 255.0 * (y - 2.0 * Kb * (1.0 - Kb) / Kg * pb - 2.0 * Kr * (1.0 - Kr) / Kg * pr);
+  double b = 255.0 * (y + 2.0 * (1.0 - Kb) * pb);
+  double v[3] = {r, g, b};
+  for (int c = 0; c < 3; c++) rgb[c] = v[c] < 0.0 ? 0.0 : (v[c] > 255.0 ? 255.0 : v[c]);
+  return MPO_OK;
+}
+
+int32_t mpo_gather_resize_nv12(const uint8_t* const* frames, int32_t pitch, int32_t W, int32_t H,
+                               int32_t F, const mpo_window* windows, int32_t n_win, int32_t k,
+                               const mpo_size* sizes, const mpo_size* out_dims, void* const* out,
+                               const int32_t* out_cap, int32_t fmt, int32_t matrix) {
+  int status = MPO_OK;
+  if ((W & 1) || (H & 1) || pitch < W || matrix < 0 || matrix > 3) return MPO_ERR_INVALID;
+  for (int32_t wi = 0; wi < n_win; wi++) {
+    mpo_window win = windows[wi];
+    if (win.frame < 0 || win.frame >= F || win.size_idx < 0 || win.size_idx >= k ||
+        win.w != sizes[win.size_idx].w || win.h != sizes[win.size_idx].h || win.x < 0 ||
+        win.y < 0 || win.x + win.w > W || win.y + win.h > H || win.slot < 0) {
+      status = MPO_ERR_INVALID;
+      continue;
+    }
+    int32_t kk = win.size_idx;
+    if (win.slot >= out_cap[kk]) {
+      status = MPO_ERR_CAPACITY;
+      continue;
+    }
+    int32_t ow = out_dims[kk].w, oh = out_dims[kk].h;
+    const uint8_t* Yp = frames[win.frame];
+    const uint8_t* UVp = Yp + (int64_t)H * pitch;
+    for (int32_t oy = 0; oy < oh; oy++) {
+      int32_t y0, y1;
+      double ly;
+      mpo_taps(win.h, oh, oy, &y0, &y1, &ly);
+      int64_t r0 = win.y + y0, r1 = win.y + y1;
+      for (int32_t ox = 0; ox < ow; ox++) {
+        int32_t x0, x1;
+        double lx;
+        mpo_taps(win.w, ow, ox, &x0, &x1, &lx);
+        int64_t c0 = win.x + x0, c1 = win.x + x1;
+        double yuv[3], rgb[3];
+        for (int32_t ch = 0; ch < 3; ch++) {
+          double p00, p01, p10, p11;
+          if (ch == 0) {
+            p00 = Yp[r0 * pitch + c0];
+            p01 = Yp[r0 * pitch + c1];
+            p10 = Yp[r1 * pitch + c0];
+            p11 = Yp[r1 * pitch + c1];
+          } else {   /* U (ch 1) at byte 2(c>>1), V (ch 2) at 2(c>>1)+1 of chroma row r>>1 */
+            int32_t o = ch - 1;
+            p00 = UVp[(r0 >> 1) * pitch + 2 * (c0 >> 1) + o];
+            p01 = UVp[(r0 >> 1) * pitch + 2 * (c1 >> 1) + o];
+            p10 = UVp[(r1 >> 1) * pitch + 2 * (c0 >> 1) + o];
+            p11 = UVp[(r1 >> 1) * pitch + 2 * (c1 >> 1) + o];
+          }
+          yuv[ch] = (1.0 - ly) * ((1.0 - lx) * p00 + lx * p01) + ly * ((1.0 - lx) * p10 + lx * p11);
+        }
+        mpo_yuv_to_rgb(yuv[0], yuv[1], yuv[2], matrix, rgb);
+        int64_t plane = (int64_t)oh * ow;
+        for (int32_t c = 0; c < 3; c++) {
+          double v = rgb[c];
+          if (fmt == MPO_F32_NCHW) {
+            ((float*)out[kk])[((int64_t)win.slot * 3 + c) * plane + (int64_t)oy * ow + ox] = (float)v;
+          } else if (fmt == MPO_F64_NCHW) {
+            ((double*)out[kk])[((int64_t)win.slot * 3 + c) * plane + (int64_t)oy * ow + ox] = v;
+          } else {
+            ((uint8_t*)out[kk])[(((int64_t)win.slot * oh + oy) * ow + ox) * 3 + c] = (uint8_t)floor(v + 0.5);
+          }
+        }
+      }
+    }
+  }
+  return status;
+}
+
+/* ------------------------------------------------------------------------ */
 /* a6. Remap one detector box (reading R18; not in the paper).  Returns 0 if
  * the box is dropped.  Steps: keep iff score > score_thr (NaN dropped);
  * clip each coordinate to [0,ow] / [0,oh] with fmin/fmax (a NaN coordinate

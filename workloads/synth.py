@@ -89,6 +89,11 @@ class Config:
     def pitch(self) -> int:
         return (3 * self.W + 15) // 16 * 16
 
+    @property
+    def pitch_nv12(self) -> int:
+        """NV12 row pitch (bytes, both planes): W rounded up to 16."""
+        return (self.W + 15) // 16 * 16
+
 
 CONFIGS = {
     # BASELINE.json configs[0]: 960x540, 30 frames, one 256x256 window size, <=20 boxes/frame
@@ -128,6 +133,14 @@ def frame_pixels_np(seed: int, H: int, pitch: int) -> np.ndarray:
         z = (z ^ (z >> np.uint64(27))) * np.uint64(_MIX2)
         z = z ^ (z >> np.uint64(31))
     return z.view(np.uint8)[: H * pitch].reshape(H, pitch)
+
+
+def frame_nv12_np(seed: int, H: int, pitch: int) -> np.ndarray:
+    """NV12 frame uint8 [H*3/2][pitch] (rows 0..H-1 = Y plane, rows H.. =
+    interleaved U,V): the same splitmix64 byte stream as frame_pixels_np over
+    H*3/2 rows, i.e. Y, U and V uniform over 0..255 (values outside the
+    limited range exercise the clamp)."""
+    return frame_pixels_np(seed, H + H // 2, pitch)
 
 
 def _s64(x: int) -> int:
