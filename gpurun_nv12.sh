@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout -s KILL 900 python -m pytest tests/test_gpu_nv12.py -q > gpurun_out/pytest_nv12.log 2>&1

@@ -165,6 +165,45 @@ mp_status mp_gather_resize_strided(const uint8_t* d_frames, int64_t frame_stride
                                    mp_out_format fmt, int32_t* d_status, void* d_ws, size_t ws_bytes,
                                    void* stream);
 
+/* ---------------------------------------------------------------------------
+ * NEXT-3: decode-native input.  The paper decodes with
+ * ffmpeg "at the object detector resolution" and feeds the proxy
+ * a low-resolution frame; a GPU decoder (NVDEC) emits NV12.
+ * Reading R23 fixes the format and conversion.
+ */
+typedef enum {
+  MP_BT709_LIMITED = 0,   /* Kr .2126, Kb .0722; Y 16..235, C 16..240 (default for HD) */
+  MP_BT601_LIMITED = 1,   /* Kr .299,  Kb .114 */
+  MP_BT709_FULL = 2,      /* Y, C 0..255 */
+  MP_BT601_FULL = 3       /* JFIF */
+} mp_color_matrix;
+
+/*
+ * mp_gather_resize_nv12 — step a5 fed directly from NV12 decoder output: for
+ * every window, the R15 bilinear resample of its Y, U and V samples (chroma
+ * sample (i,j) covers luma (2i..2i+1, 2j..2j+1)) to its class's detector-input
+ * dims, converted to R'G'B' with `matrix` and clamped to [0,255] (R23), written
+ * in the same per-class layouts as mp_gather_resize (F32 NCHW 0..255 or U8
+ * NHWC).  One read of each window's luma and chroma footprint (two TMA tensor
+ * copies per tile); the conversion is fused into the resample's epilogue.
+ * Used both for the detector crops and for the full-frame proxy input (a
+ * full-frame window whose class has the proxy resolution as out_dims).
+ *
+ *  d_frames      device, 16-byte aligned; frame f at d_frames + f*frame_stride:
+ *                Y plane [H][pitch] then interleaved UV plane [H/2][pitch]
+ *                (U at even, V at odd bytes).
+ *  frame_stride  bytes, multiple of 16, >= (H + H/2) * pitch, < 2^40.
+ *  pitch         bytes per row of both planes, multiple of 16, >= W.
+ *  W, H          frame size in pixels, both even.
+ *  matrix        mp_color_matrix; anything else -> MP_ERR_INVALID.
+ *  Other arguments, workspace, status and launch count as mp_gather_resize.
+ */
+mp_status mp_gather_resize_nv12(const uint8_t* d_frames, int64_t frame_stride, int32_t pitch, int32_t W,
+                                int32_t H, int32_t F, const mp_window* d_windows, const int32_t* d_frame_off,
+                                int32_t k, const mp_size* sizes, const mp_size* out_dims, void* const* d_out,
+                                const int32_t* out_cap, mp_out_format fmt, mp_color_matrix matrix,
+                                int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
+
 /* Bytes of scratch mp_remap_nms needs for F frames and max_boxes raw boxes. */
 size_t mp_remap_nms_workspace_size(int32_t F, int32_t max_boxes);
 

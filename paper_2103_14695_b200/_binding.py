@@ -23,6 +23,7 @@ LIB_PATH = os.path.join(_HERE, "libmp_b200.so")
 
 MP_OK, MP_ERR_INVALID, MP_ERR_CUDA, MP_ERR_CAPACITY, MP_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 MP_OUT_F32_NCHW, MP_OUT_U8_NHWC = 0, 1
+MP_BT709_LIMITED, MP_BT601_LIMITED, MP_BT709_FULL, MP_BT601_FULL = 0, 1, 2, 3
 
 
 class MPError(RuntimeError):
@@ -62,6 +63,9 @@ def _load():
     L.mp_gather_resize_strided.restype = C.c_int
     L.mp_gather_resize_strided.argtypes = [vp, C.c_int64, i32, i32, i32, i32, vp, vp, i32, vp, vp, vp, vp, C.c_int,
                                            vp, vp, sz, vp]
+    L.mp_gather_resize_nv12.restype = C.c_int
+    L.mp_gather_resize_nv12.argtypes = [vp, C.c_int64, i32, i32, i32, i32, vp, vp, i32, vp, vp, vp, vp, C.c_int,
+                                        C.c_int, vp, vp, sz, vp]
     L.mp_proxy_sweep_workspace_size.restype = sz
     L.mp_proxy_sweep_workspace_size.argtypes = [C.POINTER(mp_plan_params), i32]
     L.mp_proxy_sweep.restype = C.c_int
@@ -226,6 +230,36 @@ def mp_gather_resize_strided(frames, W, H, windows, frame_off, sizes, out_dims, 
                                        int(fmt), _p(status), _p(ws), ws.numel(), _stream(stream))
     if st != MP_OK:
         raise MPError(st, "mp_gather_resize_strided")
+
+
+def mp_gather_resize_nv12(frames, W, H, windows, frame_off, sizes, out_dims, outs, fmt, status, ws,
+                          matrix=MP_BT709_LIMITED, stream=None) -> None:
+    """a5 from NV12 decoder output (NEXT-3, R23): frames uint8 CUDA tensor
+    [F, H*3/2, pitch] (Y rows then interleaved UV rows, pitch % 16 == 0)."""
+    _dev(windows, torch.int32, "windows")
+    _dev(frame_off, torch.int32, "frame_off")
+    _dev(status, torch.int32, "status")
+    _dev(ws, torch.uint8, "ws")
+    if not frames.is_cuda or frames.dtype != torch.uint8 or frames.dim() != 3:
+        raise ValueError("frames must be a uint8 CUDA tensor [F, H*3/2, pitch]")
+    if frames.stride(2) != 1 or frames.stride(1) != frames.shape[2]:
+        raise ValueError("frames rows must be contiguous with pitch = shape[2]")
+    F, rows, pitch = frames.shape
+    if rows != int(H) + int(H) // 2:
+        raise ValueError("NV12 frames need H*3/2 rows")
+    k = len(sizes)
+    if len(outs) != k or len(out_dims) != k:
+        raise ValueError("sizes, out_dims and outs must have one entry per size class")
+    odt = torch.float32 if fmt == MP_OUT_F32_NCHW else torch.uint8
+    for q, o in enumerate(outs):
+        _dev(o, odt, f"outs[{q}]")
+    ptrs = (C.c_void_p * k)(*[o.data_ptr() for o in outs])
+    cap = (C.c_int32 * k)(*[int(o.shape[0]) for o in outs])
+    st = _lib.mp_gather_resize_nv12(_p(frames), int(frames.stride(0)), int(pitch), int(W), int(H), int(F),
+                                    _p(windows), _p(frame_off), k, _sizes(sizes), _sizes(out_dims), ptrs, cap,
+                                    int(fmt), int(matrix), _p(status), _p(ws), ws.numel(), _stream(stream))
+    if st != MP_OK:
+        raise MPError(st, "mp_gather_resize_nv12")
 
 
 def mp_remap_nms_workspace_size(F: int, max_boxes: int) -> int:

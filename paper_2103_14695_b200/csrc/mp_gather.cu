@@ -42,25 +42,31 @@ constexpr int kStageDataBudget = 44 * 1024;
 constexpr int kDataOff = (kHdrBytes + kTapBytes + 127) / 128 * 128;   // TMA destination: 128-B aligned
 
 struct GatherArgs {
-  int k, W, H, pitch, F, fmt, stage_bytes, debug, tensor;
+  int k, W, H, pitch, F, fmt, stage_bytes, debug, tensor, src;
   int ncol[kMaxClasses];
   int box_w[kMaxClasses], box_h[kMaxClasses];
   int w[kMaxClasses], h[kMaxClasses], ow[kMaxClasses], oh[kMaxClasses];
   int TW[kMaxClasses], TR[kMaxClasses], nct[kMaxClasses], tpw[kMaxClasses];
   int cap[kMaxClasses], list_off[kMaxClasses], xtab_off[kMaxClasses], ytab_off[kMaxClasses];
+  int uv_off[kMaxClasses];   // NV12: byte offset of the staged chroma box (after the luma box)
+  float cvt[6];              // NV12 (R23): cy, -cy*yo, crv, cgu, cgv, cbu (fp32 of the fp64 coefficients)
   void* out[kMaxClasses];
 };
 
+enum { kSrcRGB24 = 0, kSrcNV12 = 1 };
 
-// One TMA tensor map per size class (box = the class's staged tile footprint).
+
+// One TMA tensor map per size class (box = the class's staged tile footprint);
+// NV12 adds one per class for the chroma plane at m[kMaxClasses + q].
 struct TmapArray {
-  CUtensorMap m[kMaxClasses];
+  CUtensorMap m[2 * kMaxClasses];
 };
 
 struct TileHdr {
   int valid, k, slot, oy0, ox0, rows, cols, stride;
   int x, b0, r_lo, xs, ys;   // window x, staged byte origin, first staged row, tap slice shifts
-  int pad[3];
+  int ya;                    // NV12: absolute first staged luma row (its chroma row is ya >> 1)
+  int pad[2];
 };
 static_assert(sizeof(TileHdr) <= kHdrBytes, "header");
 
@@ -154,7 +160,7 @@ __global__ void __launch_bounds__(kPrepThreads) gather_prep_kernel(GatherArgs A,
 // the extra (finite) staged byte has no effect.
 extern __shared__ __align__(128) unsigned char smem[];
 
-template <int FMT, int NCOL>
+template <int FMT, int NCOL, int SRC>
 __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr* hdr, unsigned int soff, int wid,
                                              int lane) {
   constexpr int NP = NCOL / 2;
@@ -162,7 +168,7 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
   const int2* yt = reinterpret_cast<const int2*>(&smem[soff + kHdrBytes + kXtapBytes]) + hdr->ys;
   const unsigned int doff = soff + kDataOff;
   const int q = hdr->k, rows = hdr->rows, cols = hdr->cols;
-  const int x0 = 3 * hdr->x - hdr->b0, r_lo = hdr->r_lo;
+  const int x0 = (SRC == kSrcNV12 ? hdr->x : 3 * hdr->x) - hdr->b0, r_lo = hdr->r_lo;
   xt += hdr->xs;
   const unsigned int stride = (unsigned int)hdr->stride;
   const int R = (rows + kCW - 1) / kCW;
@@ -170,27 +176,78 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
   if (rb0 >= rb1 || lane >= cols) return;
   const float2 M2 = make_float2(8388608.0f, 8388608.0f);
   unsigned int ba[NP], bb[NP];
+  unsigned int ca[NP], cb[NP], da[NP], db[NP];   // NV12: chroma byte of the left tap, +0/+2 to the right tap
   float2 lx[NP];
 #pragma unroll
   for (int p = 0; p < NP; p++) {
-    const int ca = lane + 64 * p, cb = ca + 32;
-    const int2 xa = xt[min(ca, cols - 1)];
-    const int2 xb = xt[min(cb, cols - 1)];
-    ba[p] = doff + x0 + 3 * xa.x;
-    bb[p] = doff + x0 + 3 * xb.x;
+    const int cA = lane + 64 * p, cB = cA + 32;
+    const int2 xa = xt[min(cA, cols - 1)];
+    const int2 xb = xt[min(cB, cols - 1)];
+    if (SRC == kSrcNV12) {
+      // luma column a = x + i0 at staged byte a - b0; its chroma pair (U,V) at
+      // 2(a>>1) - b0 = (a - b0) - (a & 1) of the chroma box; the right tap's
+      // pair is 2 bytes further iff a is odd (R23 siting)
+      ba[p] = doff + x0 + xa.x;
+      bb[p] = doff + x0 + xb.x;
+      const unsigned int pa = (unsigned int)(hdr->x + xa.x) & 1u, pb = (unsigned int)(hdr->x + xb.x) & 1u;
+      ca[p] = ba[p] + (unsigned int)A.uv_off[q] - pa;
+      cb[p] = bb[p] + (unsigned int)A.uv_off[q] - pb;
+      da[p] = 2u * pa;
+      db[p] = 2u * pb;
+    } else {
+      ba[p] = doff + x0 + 3 * xa.x;
+      bb[p] = doff + x0 + 3 * xb.x;
+    }
     lx[p] = make_float2(__int_as_float(xa.y), __int_as_float(xb.y));
   }
+  const int ya = hdr->ya;
   float2 P[NP][3], N[NP][3];   // ping-pong horizontal lerps (3 channels x column pair)
+#define MP_HL(H, CH, A0, B0, A1, B1)                                                           \
+  {                                                                                             \
+    const float2 m_ = make_float2(u8m(smem[A0]), u8m(smem[B0]));                                \
+    const float2 n_ = make_float2(u8m(smem[A1]), u8m(smem[B1]));                                \
+    H[p][CH] = __ffma2_rn(lx[p], fsub2(n_, m_), fsub2(m_, M2));                                  \
+  }
 #define MP_H(ROW, H)                                                                            \
   {                                                                                             \
     const unsigned int o_ = (unsigned int)(ROW) * stride;                                      \
-    _Pragma("unroll") for (int p = 0; p < NP; p++) {                                            \
-      const unsigned int pa_ = ba[p] + o_, pb_ = bb[p] + o_;                                    \
-      _Pragma("unroll") for (int ch = 0; ch < 3; ch++) {                                        \
-        const float2 m_ = make_float2(u8m(smem[pa_ + ch]), u8m(smem[pb_ + ch]));                 \
-        const float2 n_ = make_float2(u8m(smem[pa_ + 3 + ch]), u8m(smem[pb_ + 3 + ch]));         \
-        H[p][ch] = __ffma2_rn(lx[p], fsub2(n_, m_), fsub2(m_, M2));                              \
+    if (SRC == kSrcNV12) {                                                                      \
+      const unsigned int oc_ = (unsigned int)(((ya + (ROW)) >> 1) - (ya >> 1)) * stride;       \
+      _Pragma("unroll") for (int p = 0; p < NP; p++) {                                          \
+        const unsigned int pa_ = ba[p] + o_, pb_ = bb[p] + o_;                                  \
+        const unsigned int qa_ = ca[p] + oc_, qb_ = cb[p] + oc_;                                \
+        MP_HL(H, 0, pa_, pb_, pa_ + 1, pb_ + 1)                                                 \
+        MP_HL(H, 1, qa_, qb_, qa_ + da[p], qb_ + db[p])                                         \
+        MP_HL(H, 2, qa_ + 1, qb_ + 1, qa_ + 1 + da[p], qb_ + 1 + db[p])                         \
       }                                                                                         \
+    } else {                                                                                    \
+      _Pragma("unroll") for (int p = 0; p < NP; p++) {                                          \
+        const unsigned int pa_ = ba[p] + o_, pb_ = bb[p] + o_;                                  \
+        _Pragma("unroll") for (int ch = 0; ch < 3; ch++)                                        \
+            MP_HL(H, ch, pa_ + ch, pb_ + ch, pa_ + 3 + ch, pb_ + 3 + ch)                        \
+      }                                                                                         \
+    }                                                                                           \
+  }
+  // vertical lerp of column pair p -> v0, v1, v2 (RGB); NV12: the lerped
+  // Y, U, V are converted to R'G'B' and clamped to [0, 255] (R23)
+  const float2 CY = make_float2(A.cvt[0], A.cvt[0]), CYO = make_float2(A.cvt[1], A.cvt[1]);
+  const float2 CRV = make_float2(A.cvt[2], A.cvt[2]), CGU = make_float2(A.cvt[3], A.cvt[3]);
+  const float2 CGV = make_float2(A.cvt[4], A.cvt[4]), CBU = make_float2(A.cvt[5], A.cvt[5]);
+  const float2 C128 = make_float2(-128.0f, -128.0f);
+#define MP_V(T, B)                                                                              \
+  float2 v0 = __ffma2_rn(ly, fsub2(B[p][0], T[p][0]), T[p][0]);                                  \
+  float2 v1 = __ffma2_rn(ly, fsub2(B[p][1], T[p][1]), T[p][1]);                                  \
+  float2 v2 = __ffma2_rn(ly, fsub2(B[p][2], T[p][2]), T[p][2]);                                  \
+  if (SRC == kSrcNV12) {                                                                        \
+    const float2 yy_ = __ffma2_rn(CY, v0, CYO);                                                 \
+    const float2 uu_ = __fadd2_rn(v1, C128), vv_ = __fadd2_rn(v2, C128);                         \
+    v0 = __ffma2_rn(CRV, vv_, yy_);                                                             \
+    v1 = __ffma2_rn(CGU, uu_, __ffma2_rn(CGV, vv_, yy_));                                       \
+    v2 = __ffma2_rn(CBU, uu_, yy_);                                                             \
+    if (FMT == MP_OUT_F32_NCHW) {                                                               \
+      v0 = make_float2(fminf(fmaxf(v0.x, 0.0f), 255.0f), fminf(fmaxf(v0.y, 0.0f), 255.0f));     \
+      v1 = make_float2(fminf(fmaxf(v1.x, 0.0f), 255.0f), fminf(fmaxf(v1.y, 0.0f), 255.0f));     \
+      v2 = make_float2(fminf(fmaxf(v2.x, 0.0f), 255.0f), fminf(fmaxf(v2.y, 0.0f), 255.0f));     \
     }                                                                                           \
   }
   const int ow = A.ow[q], oh = A.oh[q];
@@ -213,9 +270,7 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
   while (orow < rb1 && y.x == r) {                                                              \
     const float2 ly = make_float2(__int_as_float(y.y), __int_as_float(y.y));                    \
     _Pragma("unroll") for (int p = 0; p < NP; p++) {                                            \
-      const float2 v0 = __ffma2_rn(ly, fsub2(B[p][0], T[p][0]), T[p][0]);                        \
-      const float2 v1 = __ffma2_rn(ly, fsub2(B[p][1], T[p][1]), T[p][1]);                        \
-      const float2 v2 = __ffma2_rn(ly, fsub2(B[p][2], T[p][2]), T[p][2]);                        \
+      MP_V(T, B)                                                                                \
       if (ok[2 * p]) {                                                                          \
         __stcs(o0 + 64 * p, v0.x);                                                              \
         __stcs(o1 + 64 * p, v1.x);                                                              \
@@ -253,9 +308,7 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
   while (orow < rb1 && y.x == r) {                                                              \
     const float2 ly = make_float2(__int_as_float(y.y), __int_as_float(y.y));                    \
     _Pragma("unroll") for (int p = 0; p < NP; p++) {                                            \
-      const float2 v0 = __ffma2_rn(ly, fsub2(B[p][0], T[p][0]), T[p][0]);                        \
-      const float2 v1 = __ffma2_rn(ly, fsub2(B[p][1], T[p][1]), T[p][1]);                        \
-      const float2 v2 = __ffma2_rn(ly, fsub2(B[p][2], T[p][2]), T[p][2]);                        \
+      MP_V(T, B)                                                                                \
       if (ok[2 * p]) {                                                                          \
         o[192 * p + 0] = u8_round(v0.x);                                                        \
         o[192 * p + 1] = u8_round(v1.x);                                                        \
@@ -282,10 +335,12 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
     }
 #undef MP_EMIT
   }
+#undef MP_V
 #undef MP_H
+#undef MP_HL
 }
 
-template <int FMT>
+template <int FMT, int SRC>
 __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(const __grid_constant__ GatherArgs A,
                                                                  const __grid_constant__ TmapArray tm,
                                                                  const uint8_t* const* __restrict__ frames,
@@ -385,7 +440,7 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
           set_status(d_status, MP_ERR_INVALID);
           mbar_arrive(&full[s]);
         } else {
-          const int b0 = (3 * (dcur.x + clo_cur)) & ~15;
+          const int b0 = ((SRC == kSrcNV12 ? 1 : 3) * (dcur.x + clo_cur)) & ~15;
           const int stride = A.box_w[q];
           const int xe = A.xtab_off[q] + cur.ox0, ye = A.ytab_off[q] + cur.oy0;   // first tap entries
           const int xs = xe & 1, ys = ye & 1;                                       // 16-B aligned slices
@@ -404,10 +459,21 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
           hdr->r_lo = rlo_cur;
           hdr->xs = xs;
           hdr->ys = ys;
+          hdr->ya = dcur.y + rlo_cur;
           if (A.debug == 2) {   // experiment: no pixel copies (compute-only bound)
             mbar_arrive_expect_tx(&full[s], xbytes + ybytes);
             bulk_g2s(xt, ws_tap + (xe - xs), xbytes, &full[s]);
             bulk_g2s(yt, ws_tap + (ye - ys), ybytes, &full[s]);
+          } else if (SRC == kSrcNV12) {
+            // two TMA boxes from the same column origin b0: luma rows ya.., then
+            // chroma rows (ya >> 1).. of the interleaved UV plane (R23)
+            const int ya = dcur.y + rlo_cur;
+            mbar_arrive_expect_tx(&full[s], (uint32_t)(stride * A.box_h[q]) + (uint32_t)(stride * ((A.box_h[q] >> 1) + 1)) +
+                                                xbytes + ybytes);
+            bulk_g2s(xt, ws_tap + (xe - xs), xbytes, &full[s]);
+            bulk_g2s(yt, ws_tap + (ye - ys), ybytes, &full[s]);
+            tma_load_3d(data, &tm.m[q], b0 >> 3, ya, dcur.frame, &full[s]);
+            tma_load_3d(data + A.uv_off[q], &tm.m[kMaxClasses + q], b0 >> 3, ya >> 1, dcur.frame, &full[s]);
           } else if (A.tensor) {
             // one TMA box: [box_h rows][box_w bytes] from (b0, y + r_lo) of frame d.frame;
             // rows past the frame bottom / bytes past the pitch are zero-filled.
@@ -448,10 +514,10 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
     const TileHdr* hdr = reinterpret_cast<const TileHdr*>(&smem[soff]);
     if (hdr->valid && A.debug != 1) {
       switch (A.ncol[hdr->k]) {
-        case 2: consume_tile<FMT, 2>(A, hdr, soff, wid, lane); break;
-        case 4: consume_tile<FMT, 4>(A, hdr, soff, wid, lane); break;
-        case 6: consume_tile<FMT, 6>(A, hdr, soff, wid, lane); break;
-        default: consume_tile<FMT, 8>(A, hdr, soff, wid, lane); break;
+        case 2: consume_tile<FMT, 2, SRC>(A, hdr, soff, wid, lane); break;
+        case 4: consume_tile<FMT, 4, SRC>(A, hdr, soff, wid, lane); break;
+        case 6: consume_tile<FMT, 6, SRC>(A, hdr, soff, wid, lane); break;
+        default: consume_tile<FMT, 8, SRC>(A, hdr, soff, wid, lane); break;
       }
     }
     __syncwarp();
@@ -470,9 +536,11 @@ static void host_tap(int in, int out, int d, int* i0, int* i1) {
 
 // Staged box of a class with tile dims (TW, TR): every tile reads source
 // columns c_lo .. i0(last)+1 (the +1 pixel is the always-present right tap)
-// starting at a 16-B aligned byte b0 >= 3*(x+c_lo)-15, and source rows
+// starting at a 16-B aligned byte b0 >= bpp*(x+c_lo)-15, and source rows
 // r_lo .. i0(last)+1.  Returns the box (bytes x rows) that covers any tile.
-static void class_box(int in_w, int in_h, int ow, int oh, int TW, int TR, int* box_w, int* box_h) {
+// NV12 (bpp 1): the chroma pair of the last luma column a sits at bytes up to
+// 2((a+1)>>1)+1 <= a+2, one byte past the luma footprint -> +1 byte.
+static void class_box(int in_w, int in_h, int ow, int oh, int TW, int TR, int src, int* box_w, int* box_h) {
   int nct = (ow + TW - 1) / TW, nrt = (oh + TR - 1) / TR;
   int max_rows = 0, max_cols = 0, a, b, c, d;
   for (int rt = 0; rt < nrt; rt++) {
@@ -490,15 +558,25 @@ static void class_box(int in_w, int in_h, int ow, int oh, int TW, int TR, int* b
     const int c_hi = (c + 1 < in_w - 1) ? c + 1 : in_w - 1;
     if (c_hi - a + 1 > max_cols) max_cols = c_hi - a + 1;
   }
-  *box_w = (3 * max_cols + 15 + 15) / 16 * 16;   // + up to 15 B of 16-B start alignment
+  const int bytes = src == kSrcNV12 ? max_cols + 1 : 3 * max_cols;
+  *box_w = (bytes + 15 + 15) / 16 * 16;   // + up to 15 B of 16-B start alignment
   *box_h = max_rows;
 }
 
-static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_size* sizes,
+// Staged bytes of a class box: RGB24 = the box; NV12 = the luma box (padded to
+// 128 B for the second TMA destination) + the chroma box (box_h/2 + 1 rows:
+// the chroma rows of box_h consecutive luma rows starting at any parity).
+static long long stage_data_bytes(int src, int bw, int bh) {
+  if (src != kSrcNV12) return (long long)bw * bh;
+  return ((long long)bw * bh + 127) / 128 * 128 + (long long)bw * (bh / 2 + 1);
+}
+
+static bool build_gather_args(int src, int pitch, int W, int H, int F, int k, const mp_size* sizes,
                               const mp_size* out_dims, void* const* d_out, const int32_t* out_cap,
                               mp_out_format fmt, GatherArgs* A) {
   if (W < 1 || H < 1 || W > 16384 || H > 16384 || F < 0 || k < 1 || k > kMaxClasses) return false;
-  if (pitch < 3 * W || (pitch & 15)) return false;
+  if (pitch < (src == kSrcNV12 ? W : 3 * W) || (pitch & 15)) return false;
+  if (src == kSrcNV12 && ((W & 1) || (H & 1))) return false;
   if (!sizes || !out_dims || !d_out || !out_cap) return false;
   if (fmt != MP_OUT_F32_NCHW && fmt != MP_OUT_U8_NHWC) return false;
   memset(A, 0, sizeof(*A));
@@ -508,6 +586,7 @@ static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_si
   A->pitch = pitch;
   A->F = F;
   A->fmt = fmt;
+  A->src = src;
   long long data_max = 0;
   int list = 0, taps = 0;
   const long long budget = kStageDataBudget;
@@ -533,8 +612,8 @@ static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_si
     int TW = 0, TR = 0, bw = 0, bh = 0;
     auto fit_rows = [&](int tw, int& rw, int& cbw, int& cbh) {
       for (rw = 8; rw >= 1; rw--) {
-        class_box(w, h, ow, oh, tw, kCW * rw, &cbw, &cbh);
-        if ((long long)cbw * cbh <= budget && cbw <= 2048 && cbh <= 256) return true;
+        class_box(w, h, ow, oh, tw, kCW * rw, src, &cbw, &cbh);
+        if (stage_data_bytes(src, cbw, cbh) <= budget && cbw <= 2048 && cbh <= 256) return true;
       }
       return false;
     };
@@ -567,7 +646,7 @@ static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_si
       if (ft && sscanf(ft, "%d,%d,%d", &fow, &ftw, &frw) == 3 && fow == ow) {
         TW = ftw;
         TR = kCW * frw;
-        class_box(w, h, ow, oh, TW, TR, &bw, &bh);
+        class_box(w, h, ow, oh, TW, TR, src, &bw, &bh);
       }
     }
     if (TW == 0) return false;   // too strong a downscale of too wide a window: unsupported
@@ -578,6 +657,7 @@ static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_si
     A->TR[q] = TR;
     A->box_w[q] = bw;
     A->box_h[q] = bh;
+    A->uv_off[q] = (int)(((long long)bw * bh + 127) / 128 * 128);
     A->nct[q] = (ow + TW - 1) / TW;
     A->tpw[q] = A->nct[q] * ((oh + TR - 1) / TR);
     A->cap[q] = out_cap[q];
@@ -588,7 +668,7 @@ static bool build_gather_args(int pitch, int W, int H, int F, int k, const mp_si
     taps += ow;
     A->ytab_off[q] = taps;
     taps += oh;
-    if ((long long)bw * bh > data_max) data_max = (long long)bw * bh;
+    if (stage_data_bytes(src, bw, bh) > data_max) data_max = stage_data_bytes(src, bw, bh);
   }
   A->stage_bytes = (int)((kDataOff + data_max + 64 + 127) / 128 * 128);
   return true;
@@ -663,7 +743,11 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
     MP_CUDA_TRY(cudaGetLastError());
     return MP_OK;
   };
-  return fmt == MP_OUT_F32_NCHW ? launch(gather_kernel<MP_OUT_F32_NCHW>) : launch(gather_kernel<MP_OUT_U8_NHWC>);
+  if (A.src == kSrcNV12)
+    return fmt == MP_OUT_F32_NCHW ? launch(gather_kernel<MP_OUT_F32_NCHW, kSrcNV12>)
+                                  : launch(gather_kernel<MP_OUT_U8_NHWC, kSrcNV12>);
+  return fmt == MP_OUT_F32_NCHW ? launch(gather_kernel<MP_OUT_F32_NCHW, kSrcRGB24>)
+                                : launch(gather_kernel<MP_OUT_U8_NHWC, kSrcRGB24>);
 }
 
 extern "C" mp_status mp_gather_resize(const uint8_t* const* d_frame_ptrs, int32_t pitch, int32_t W, int32_t H,
@@ -672,13 +756,40 @@ extern "C" mp_status mp_gather_resize(const uint8_t* const* d_frame_ptrs, int32_
                                       void* const* d_out, const int32_t* out_cap, mp_out_format fmt,
                                       int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
   GatherArgs A;
-  if (!build_gather_args(pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A)) return MP_ERR_INVALID;
+  if (!build_gather_args(kSrcRGB24, pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A))
+    return MP_ERR_INVALID;
   if (!d_frame_off || !d_status || (F > 0 && (!d_frame_ptrs || !d_windows))) return MP_ERR_INVALID;
   TmapArray tm;
   memset(&tm, 0, sizeof(tm));
   A.tensor = 0;
   return gather_launch(A, tm, d_frame_ptrs, d_windows, d_frame_off, k, out_dims, out_cap, fmt, d_status, d_ws,
                        ws_bytes, stream);
+}
+
+static EncodeTiledFn get_encode() {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult qr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+      qr != cudaDriverEntryPointSuccess || !fn) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  return (EncodeTiledFn)fn;
+}
+
+// A plane batch as a 3-D tensor of 8-byte elements [F][rows][pitch/8]; box =
+// one class's staged footprint.  Rows past the plane bottom and bytes past the
+// pitch are zero-filled by the copy engine.
+static bool encode_plane(EncodeTiledFn encode, CUtensorMap* m, const void* base, int pitch, int rows, int F,
+                         int64_t frame_stride, int box_w, int box_h) {
+  const cuuint64_t gdim[3] = {(cuuint64_t)(pitch / 8), (cuuint64_t)rows, (cuuint64_t)F};
+  const cuuint64_t gstride[2] = {(cuuint64_t)pitch, (cuuint64_t)frame_stride};
+  const cuuint32_t box[3] = {(cuuint32_t)(box_w / 8), (cuuint32_t)box_h, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  // measured on B200: 64-B L2 promotion beats none / 128 B / 256 B for these ~0.8 KB box rows
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(base), gdim, gstride, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 extern "C" mp_status mp_gather_resize_strided(const uint8_t* d_frames, int64_t frame_stride, int32_t pitch,
@@ -688,7 +799,8 @@ extern "C" mp_status mp_gather_resize_strided(const uint8_t* d_frames, int64_t f
                                               mp_out_format fmt, int32_t* d_status, void* d_ws, size_t ws_bytes,
                                               void* stream) {
   GatherArgs A;
-  if (!build_gather_args(pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A)) return MP_ERR_INVALID;
+  if (!build_gather_args(kSrcRGB24, pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A))
+    return MP_ERR_INVALID;
   if (!d_frame_off || !d_status || (F > 0 && (!d_frames || !d_windows))) return MP_ERR_INVALID;
   if (F > 0 && (((uintptr_t)d_frames) & 15)) return MP_ERR_INVALID;
   if (frame_stride < (int64_t)H * pitch || (frame_stride & 15) || frame_stride >= (int64_t(1) << 40))
@@ -697,25 +809,60 @@ extern "C" mp_status mp_gather_resize_strided(const uint8_t* d_frames, int64_t f
   memset(&tm, 0, sizeof(tm));
   A.tensor = 1;
   if (F > 0) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult qr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
-        qr != cudaDriverEntryPointSuccess || !fn) {
-      (void)cudaGetLastError();
-      return MP_ERR_CUDA;
-    }
-    EncodeTiledFn encode = (EncodeTiledFn)fn;
-    // measured on B200: 64-B L2 promotion beats none / 128 B / 256 B for these ~0.8 KB box rows
-    const CUtensorMapL2promotion l2promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    EncodeTiledFn encode = get_encode();
+    if (!encode) return MP_ERR_CUDA;
+    for (int q = 0; q < k; q++)
+      if (!encode_plane(encode, &tm.m[q], d_frames, pitch, H, F, frame_stride, A.box_w[q], A.box_h[q]))
+        return MP_ERR_UNSUPPORTED;
+  }
+  return gather_launch(A, tm, nullptr, d_windows, d_frame_off, k, out_dims, out_cap, fmt, d_status, d_ws,
+                       ws_bytes, stream);
+}
+
+// R23 conversion coefficients from the BT.601 / BT.709 definitions (computed in
+// fp64, rounded once to fp32): out = cy*Y - cy*yo + {crv*(V-128); cgu*(U-128)
+// + cgv*(V-128); cbu*(U-128)}.
+static bool nv12_coefficients(int matrix, float* c) {
+  if (matrix < MP_BT709_LIMITED || matrix > MP_BT601_FULL) return false;
+  const bool bt601 = matrix == MP_BT601_LIMITED || matrix == MP_BT601_FULL;
+  const bool full = matrix == MP_BT709_FULL || matrix == MP_BT601_FULL;
+  const double Kr = bt601 ? 0.299 : 0.2126, Kb = bt601 ? 0.114 : 0.0722, Kg = 1.0 - Kr - Kb;
+  const double yo = full ? 0.0 : 16.0, ys = full ? 255.0 : 219.0, cs = full ? 255.0 : 224.0;
+  const double cy = 255.0 / ys;
+  c[0] = (float)cy;
+  c[1] = (float)(-cy * yo);
+  c[2] = (float)(255.0 * 2.0 * (1.0 - Kr) / cs);
+  c[3] = (float)(-255.0 * 2.0 * Kb * (1.0 - Kb) / (Kg * cs));
+  c[4] = (float)(-255.0 * 2.0 * Kr * (1.0 - Kr) / (Kg * cs));
+  c[5] = (float)(255.0 * 2.0 * (1.0 - Kb) / cs);
+  return true;
+}
+
+extern "C" mp_status mp_gather_resize_nv12(const uint8_t* d_frames, int64_t frame_stride, int32_t pitch, int32_t W,
+                                           int32_t H, int32_t F, const mp_window* d_windows,
+                                           const int32_t* d_frame_off, int32_t k, const mp_size* sizes,
+                                           const mp_size* out_dims, void* const* d_out, const int32_t* out_cap,
+                                           mp_out_format fmt, mp_color_matrix matrix, int32_t* d_status,
+                                           void* d_ws, size_t ws_bytes, void* stream) {
+  GatherArgs A;
+  if (!build_gather_args(kSrcNV12, pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A))
+    return MP_ERR_INVALID;
+  if (!nv12_coefficients((int)matrix, A.cvt)) return MP_ERR_INVALID;
+  if (!d_frame_off || !d_status || (F > 0 && (!d_frames || !d_windows))) return MP_ERR_INVALID;
+  if (F > 0 && (((uintptr_t)d_frames) & 15)) return MP_ERR_INVALID;
+  if (frame_stride < (int64_t)(H + H / 2) * pitch || (frame_stride & 15) || frame_stride >= (int64_t(1) << 40))
+    return MP_ERR_INVALID;
+  TmapArray tm;
+  memset(&tm, 0, sizeof(tm));
+  A.tensor = 1;
+  if (F > 0) {
+    EncodeTiledFn encode = get_encode();
+    if (!encode) return MP_ERR_CUDA;
+    const uint8_t* uv = d_frames + (size_t)H * pitch;
     for (int q = 0; q < k; q++) {
-      // the frame batch as a 3-D tensor of 8-byte elements: [F][H][pitch/8]
-      const cuuint64_t gdim[3] = {(cuuint64_t)(pitch / 8), (cuuint64_t)H, (cuuint64_t)F};
-      const cuuint64_t gstride[2] = {(cuuint64_t)pitch, (cuuint64_t)frame_stride};
-      const cuuint32_t box[3] = {(cuuint32_t)(A.box_w[q] / 8), (cuuint32_t)A.box_h[q], 1};
-      const cuuint32_t estr[3] = {1, 1, 1};
-      if (encode(&tm.m[q], CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, (void*)d_frames, gdim, gstride, box, estr,
-                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2promo,
-                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      if (!encode_plane(encode, &tm.m[q], d_frames, pitch, H, F, frame_stride, A.box_w[q], A.box_h[q]) ||
+          !encode_plane(encode, &tm.m[kMaxClasses + q], uv, pitch, H / 2, F, frame_stride, A.box_w[q],
+                        A.box_h[q] / 2 + 1))
         return MP_ERR_UNSUPPORTED;
     }
   }

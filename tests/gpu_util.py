@@ -62,6 +62,30 @@ def gpu_gather(frames_np_or_t, pitch, W, H, windows, sizes, out_dims, caps, fmt=
     return int(st.item()), [o.cpu().numpy() for o in outs]
 
 
+def gpu_gather_nv12(frames_np_or_t, W, H, windows, sizes, out_dims, caps, fmt=mp.MP_OUT_F32_NCHW,
+                    matrix=mp.MP_BT709_LIMITED):
+    fr = frames_np_or_t if isinstance(frames_np_or_t, torch.Tensor) else \
+        torch.from_numpy(np.stack(frames_np_or_t)).to(DEV)
+    F = fr.shape[0]
+    win = np.asarray(windows, np.int32).reshape(-1, 7)
+    fo = np.searchsorted(win[:, 0], np.arange(F + 1), side="left").astype(np.int32) if len(win) else \
+        np.zeros(F + 1, np.int32)
+    fo[F] = len(win)
+    wt = torch.from_numpy(win if len(win) else np.zeros((1, 7), np.int32)).to(DEV)
+    fot = torch.from_numpy(fo).to(DEV)
+    outs = []
+    for q, (ow, oh) in enumerate(out_dims):
+        if fmt == mp.MP_OUT_F32_NCHW:
+            outs.append(torch.full((caps[q], 3, oh, ow), -1.0, dtype=torch.float32, device=DEV))
+        else:
+            outs.append(torch.zeros((caps[q], oh, ow, 3), dtype=torch.uint8, device=DEV))
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ws = torch.empty(B.mp_gather_workspace_size(out_dims, caps), dtype=torch.uint8, device=DEV)
+    B.mp_gather_resize_nv12(fr, W, H, wt, fot, sizes, out_dims, outs, fmt, st, ws, matrix)
+    torch.cuda.synchronize()
+    return int(st.item()), [o.cpu().numpy() for o in outs]
+
+
 def boxes_to_t(boxes):
     if len(boxes) == 0:
         return torch.zeros((1, 6), dtype=torch.float32, device=DEV)

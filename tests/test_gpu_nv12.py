@@ -1,0 +1,131 @@
+"""GPU parity of NEXT-3 (mp_gather_resize_nv12, reading R23) against the
+oracle's mpo_gather_resize_nv12 on the same seeded NV12 frames: f32 pixels
+within 1e-3 absolute, u8 within 1 LSB (the a5 tolerances), plus the full-frame
+proxy-input downscale, odd window offsets (chroma parity), all four matrices,
+frame edges and the error paths."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle as O  # noqa: E402
+from workloads import synth as S  # noqa: E402
+
+F32_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def G():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import gpu_util
+    return gpu_util
+
+
+def _frames(cfg, clip, F):
+    return [S.frame_nv12_np(S.frame_seed(clip, f), cfg.H, cfg.pitch_nv12) for f in range(F)]
+
+
+def _compare(G, frames, pitch, W, H, windows, sizes, out_dims, fmt, matrix=O.BT709_LIMITED):
+    win = np.asarray(windows, np.int32).reshape(-1, 7)
+    caps = [int((win[:, 5] == q).sum()) for q in range(len(sizes))]
+    st_r, ref = O.gather_resize_nv12(frames, pitch, W, H, win, sizes, out_dims, caps,
+                                     O.F32_NCHW if fmt == 0 else O.U8_NHWC, matrix)
+    st_g, got = G.gpu_gather_nv12(frames, W, H, win, sizes, out_dims, caps, fmt, matrix)
+    assert st_g == st_r == 0
+    for q in range(len(sizes)):
+        if caps[q] == 0:
+            continue
+        if fmt == 0:
+            err = np.abs(got[q].astype(np.float64) - ref[q]).max()
+            assert err <= F32_TOL, (q, err)
+        else:
+            d = np.abs(got[q].astype(np.int32) - ref[q].astype(np.int32))
+            assert d.max() <= 1, (q, d.max())
+    return ref, got
+
+
+@pytest.mark.parametrize("fmt", [0, 1])
+@pytest.mark.parametrize("name,frames", [("c1_540p", 30), ("c2_1080p_sparse", 24), ("c4_4k_drone", 2)])
+def test_nv12_parity_configs(G, name, frames, fmt):
+    cfg = S.CONFIGS[name]
+    scene = S.make_scene(cfg, 4, frames)
+    scores = S.score_grids(cfg, 4, scene)
+    plan = O.plan_windows(cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores)
+    _compare(G, _frames(cfg, 4, frames), cfg.pitch_nv12, cfg.W, cfg.H, plan["windows"], cfg.sizes,
+             cfg.out_dims, fmt)
+
+
+@pytest.mark.parametrize("matrix", [0, 1, 2, 3])
+@pytest.mark.parametrize("fmt", [0, 1])
+@pytest.mark.parametrize("scale", [1.0, 0.5, 0.7, 1.37, 0.26])
+def test_nv12_scales_offsets_matrices(G, scale, fmt, matrix):
+    """Every window offset parity (odd/even x and y), frame edges, up/down scales."""
+    W, H = 640, 360
+    pitch = 640
+    sizes = [(96, 64), (250, 130), (640, 360)]
+    out_dims = [(max(1, int(np.floor(scale * w + 0.5))), max(1, int(np.floor(scale * h + 0.5)))) for w, h in sizes]
+    frames = [S.frame_nv12_np(S.frame_seed(77, f), H, pitch) for f in range(2)]
+    rng = np.random.default_rng(int(scale * 1000) + matrix)
+    win = []
+    for f in range(2):
+        for q, (w, h) in enumerate(sizes):
+            xs = sorted({0, min(1, W - w), W - w, max(0, W - w - 1), int(rng.integers(0, W - w + 1))})
+            ys = sorted({0, min(1, H - h), H - h, max(0, H - h - 1), int(rng.integers(0, H - h + 1))})
+            for x in xs:
+                for y in ys:
+                    win.append([f, x, y, w, h, q, 0])
+    win = np.array(win, np.int32)
+    for q in range(3):
+        sel = np.nonzero(win[:, 5] == q)[0]
+        win[sel, 6] = np.arange(len(sel))
+    _compare(G, frames, pitch, W, H, win, sizes, out_dims, fmt, matrix)
+
+
+@pytest.mark.parametrize("name,proxy", [("c2_1080p_sparse", (384, 216)), ("c1_540p", (240, 135)),
+                                        ("c4_4k_drone", (480, 270))])
+def test_nv12_full_frame_proxy_input(G, name, proxy):
+    """The proxy's low-resolution input: one full-frame window
+    per frame in a class whose out_dims is the proxy resolution."""
+    cfg = S.CONFIGS[name]
+    F = 6 if cfg.W <= 1920 else 2
+    win = np.array([[f, 0, 0, cfg.W, cfg.H, 0, f] for f in range(F)], np.int32)
+    _compare(G, _frames(cfg, 9, F), cfg.pitch_nv12, cfg.W, cfg.H, win, [(cfg.W, cfg.H)], [proxy], 0)
+
+
+def test_nv12_grey_equals_rgb_path(G):
+    """U = V = 128 and R = G = B = Y: the NV12 kernel's output equals the RGB
+    kernel's output mapped by 255 (v - 16) / 219 (within fp32 rounding)."""
+    import paper_2103_14695_b200 as mp
+    W, H, pitch = 512, 288, 512
+    nv = S.frame_nv12_np(5, H, pitch).copy()
+    nv[H:] = 128
+    rgb = np.zeros((H, 3 * W), np.uint8)
+    rgb[:, :] = np.repeat(nv[:H, :W], 3, 1)
+    win = np.array([[0, 3, 7, 200, 150, 0, 0], [0, 311, 137, 200, 150, 0, 1]], np.int32)
+    st, a = G.gpu_gather([rgb], 3 * W, W, H, win, [(200, 150)], [(131, 97)], [2])
+    st2, b = G.gpu_gather_nv12([nv], W, H, win, [(200, 150)], [(131, 97)], [2])
+    assert st == st2 == 0
+    e = np.clip((a[0].astype(np.float64) - 16) * 255 / 219, 0, 255)
+    assert np.abs(b[0] - e).max() <= 1e-3
+    assert mp.MP_BT709_LIMITED == 0
+
+
+def test_nv12_invalid(G):
+    import paper_2103_14695_b200 as mp
+    W, H, pitch = 256, 128, 256
+    fr = [S.frame_nv12_np(5, H, pitch)]
+    win = np.array([[0, 0, 0, 64, 64, 0, 0], [0, 64, 0, 64, 64, 0, 1]], np.int32)
+    st, got = G.gpu_gather_nv12(fr, W, H, win, [(64, 64)], [(32, 32)], [1])
+    assert st == O.ERR_CAPACITY
+    st_r, ref = O.gather_resize_nv12(fr, pitch, W, H, win[:1], [(64, 64)], [(32, 32)], [1])
+    assert np.abs(got[0] - ref[0]).max() <= F32_TOL
+    bad = np.array([[0, 200, 0, 64, 64, 0, 0]], np.int32)
+    st, _ = G.gpu_gather_nv12(fr, W, H, bad, [(64, 64)], [(32, 32)], [1])
+    assert st == O.ERR_INVALID
+    with pytest.raises(mp.MPError):
+        G.gpu_gather_nv12(fr, W, H, win[:1], [(64, 64)], [(32, 32)], [1], matrix=4)
+    odd = [S.frame_nv12_np(5, 127, pitch)]   # H odd
+    with pytest.raises(mp.MPError):
+        G.gpu_gather_nv12(odd, W, 127, win[:1], [(64, 64)], [(32, 32)], [1])
