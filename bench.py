@@ -72,22 +72,22 @@ def union_area(rects):
     return int((np.diff(ys)[:, None] * np.diff(xs)[None, :] * cov).sum())
 
 
-def algorithmic_bytes(cfg, windows, frame_off, n_box, n_kept, F, fmt_bytes):
+def algorithmic_bytes(cfg, windows, frame_off, n_box, n_kept, F, fmt_bytes, bpp=3.0):
     """SURVEY.md §8(d) algorithmic bytes.  Returns dict with the gather kernel's
     bytes (union-of-footprints read, conservative; and per-window sum) and the
-    whole step's bytes."""
+    whole step's bytes.  bpp = source bytes per pixel (RGB24 3, NV12 1.5)."""
     R, C = cfg.grid
     od = cfg.out_dims
     sizes = cfg.sizes
     tap_area = {q: tapped(sizes[q][0], od[q][0]) * tapped(sizes[q][1], od[q][1]) for q in range(len(sizes))}
     full_tap = all(tap_area[q] == sizes[q][0] * sizes[q][1] for q in tap_area)
     out_b = sum(3 * od[q][0] * od[q][1] * fmt_bytes for q in windows[:, 5])
-    read_sum = sum(3 * tap_area[q] for q in windows[:, 5])
+    read_sum = int(sum(bpp * tap_area[q] for q in windows[:, 5]))
     if full_tap:
         read_union = 0
         for f in range(F):
             w = windows[frame_off[f]:frame_off[f + 1]]
-            read_union += 3 * union_area(w[:, 1:5].astype(np.int64))
+            read_union += int(bpp * union_area(w[:, 1:5].astype(np.int64)))
     else:
         read_union = read_sum
     n_win = len(windows)
@@ -95,6 +95,29 @@ def algorithmic_bytes(cfg, windows, frame_off, n_box, n_kept, F, fmt_bytes):
     step = (4 * R * C * F + 28 * n_win * 3 + read_union + out_b + 24 * n_box + 28 * n_kept + 8 * (F + 1))
     return dict(gather_union=gather, gather_sum=read_sum + out_b + 28 * n_win, step=step, out=out_b,
                 read_union=read_union, read_sum=read_sum)
+
+
+def proxy_input_bytes(cfg):
+    """Algorithmic bytes of NEXT-3's full-frame downscale of one NV12 frame at
+    DRAM granularity: the 32-byte sectors holding a luma sample the R15 taps
+    touch (rows i0, i0+1; columns i0, i0+1), the sectors holding the chroma
+    pairs those samples map to (R23), and the f32 output.  (At 1920->416 every
+    luma sector of a tapped row holds a tapped column, so this is the tapped
+    rows in full.)  Returns (sector-granular bytes, distinct-sample bytes)."""
+    pw, ph = cfg.proxy_dims
+
+    def taps_idx(n_in, n_out):
+        d = np.arange(n_out, dtype=np.int64)
+        n = (2 * d + 1) * n_in - n_out
+        i0 = np.minimum(np.where(n < 0, 0, n // (2 * n_out)), n_in - 1)
+        return np.union1d(i0, np.minimum(i0 + 1, n_in - 1))
+
+    cx, cy = taps_idx(cfg.W, pw), taps_idx(cfg.H, ph)
+    ux, uy = np.unique(cx >> 1), np.unique(cy >> 1)
+    out = 12 * pw * ph
+    sect = 32 * (len(np.unique(cx >> 5)) * len(cy) + len(np.unique((2 * ux) >> 5)) * len(uy))
+    samples = len(cx) * len(cy) + 2 * len(ux) * len(uy)
+    return sect + out, samples + out
 
 
 class ClockSampler:
@@ -152,15 +175,18 @@ class ClockSampler:
 ORACLE_MAX_FRAMES = 240
 
 
-def oracle_prepare(cfg, clip, n_frames):
+def oracle_prepare(cfg, clip, n_frames, src="rgb24"):
     """Seeded inputs for the first n_frames of a clip (generation is untimed)."""
     import oracle as O
     scene = S.make_scene(cfg, clip, n_frames)
     scores = S.score_grids(cfg, clip, scene)
-    frames = [S.frame_pixels_np(S.frame_seed(clip, f), cfg.H, cfg.pitch) for f in range(n_frames)]
+    if src == "nv12":
+        frames = [S.frame_nv12_np(S.frame_seed(clip, f), cfg.H, cfg.pitch_nv12) for f in range(n_frames)]
+    else:
+        frames = [S.frame_pixels_np(S.frame_seed(clip, f), cfg.H, cfg.pitch) for f in range(n_frames)]
     plan_all = O.plan_windows(cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores)
     boxes, wbo = S.standin_boxes(cfg, clip, scene, plan_all["windows"])
-    return dict(n=n_frames, scores=scores, frames=frames, plan=plan_all, boxes=boxes, wbo=wbo)
+    return dict(n=n_frames, scores=scores, frames=frames, plan=plan_all, boxes=boxes, wbo=wbo, src=src)
 
 
 def oracle_run(cfg, inp, n_frames, threads):
@@ -174,9 +200,17 @@ def oracle_run(cfg, inp, n_frames, threads):
 
     def work(idx):
         a, b = int(idx[0]), int(idx[-1]) + 1
+        if inp["src"] == "nv12":   # NEXT-3: proxy-input downscale, then the NV12 crops
+            pw = [[f - a, 0, 0, cfg.W, cfg.H, 0, f - a] for f in range(a, b)]
+            O.gather_resize_nv12(frames[a:b], cfg.pitch_nv12, cfg.W, cfg.H, pw, [(cfg.W, cfg.H)],
+                                 [cfg.proxy_dims], [b - a])
         p = O.plan_windows(cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores[a:b])
         caps = [int(c) for c in p["class_count"]]
-        O.gather_resize(frames[a:b], cfg.pitch, cfg.W, cfg.H, p["windows"], cfg.sizes, cfg.out_dims, caps)
+        if inp["src"] == "nv12":
+            O.gather_resize_nv12(frames[a:b], cfg.pitch_nv12, cfg.W, cfg.H, p["windows"], cfg.sizes, cfg.out_dims,
+                                 caps)
+        else:
+            O.gather_resize(frames[a:b], cfg.pitch, cfg.W, cfg.H, p["windows"], cfg.sizes, cfg.out_dims, caps)
         w0, w1 = plan_all["frame_off"][a], plan_all["frame_off"][b]
         sub_off = plan_all["frame_off"][a:b + 1] - w0
         bx = boxes[wbo[w0]:wbo[w1]]
@@ -189,10 +223,10 @@ def oracle_run(cfg, inp, n_frames, threads):
     return time.perf_counter() - t0
 
 
-def oracle_baseline(cfg, clip, threads, target_s):
+def oracle_baseline(cfg, clip, threads, target_s, src="rgb24"):
     """Bounded oracle sample taking about target_s seconds: returns (fps, n)."""
     n_max = min(cfg.frames, ORACLE_MAX_FRAMES)
-    inp = oracle_prepare(cfg, clip, n_max)
+    inp = oracle_prepare(cfg, clip, n_max, src)
     probe_n = min(n_max, max(threads, 8))
     per_frame = oracle_run(cfg, inp, probe_n, threads) / probe_n
     n = int(max(1, min(n_max, target_s / max(per_frame, 1e-9))))
@@ -208,7 +242,7 @@ def run_reference(args):
     import oracle as O
     O.build()
     # size each step's sample so the whole run stays within a few minutes
-    inp, n = oracle_baseline(cfg, 0, threads, 120.0 / max(1, args.steps + args.warmup))
+    inp, n = oracle_baseline(cfg, 0, threads, 120.0 / max(1, args.steps + args.warmup), args.src)
     for _ in range(args.warmup):
         oracle_run(cfg, inp, n, threads)
     tot = 0.0
@@ -219,10 +253,12 @@ def run_reference(args):
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "frames_per_step": n, "W": cfg.W, "H": cfg.H},
+            "config": {"workload": cfg.name, "frames_per_step": n, "W": cfg.W, "H": cfg.H, "src": args.src},
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "oracle",
                              "sample": f"first {n} frames of clip 0 of {cfg.name} per step "
-                                       f"(plan+gather+remap/NMS), {threads} threads on {host_cpu_desc()}"},
+                                       f"({'proxy-input downscale+' if args.src == 'nv12' else ''}"
+                                       f"plan+gather+remap/NMS, {args.src} frames), {threads} threads on "
+                                       f"{host_cpu_desc()}"},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -250,12 +286,18 @@ def run_b200(args):
     fmt_bytes = 4 if args.fmt == "f32" else 1
 
     # ---- untimed setup: synthetic inputs resident in HBM
+    nv12 = args.src == "nv12"
     scene = S.make_scene(cfg, clip, F)
     scores_np = S.score_grids(cfg, clip, scene)
     scores = torch.from_numpy(scores_np).to(dev)
-    frames = S.frame_pixels_torch([S.frame_seed(clip, f) for f in range(F)], cfg.H, cfg.pitch, device=dev)
+    seeds = [S.frame_seed(clip, f) for f in range(F)]
+    if nv12:   # NEXT-3: decoder-native NV12 frames (same bytes as S.frame_nv12_np)
+        frames = S.frame_pixels_torch(seeds, cfg.H + cfg.H // 2, cfg.pitch_nv12, device=dev)
+    else:
+        frames = S.frame_pixels_torch(seeds, cfg.H, cfg.pitch, device=dev)
+    pkw = dict(src=args.src, proxy_dims=cfg.proxy_dims) if nv12 else {}
     pipe = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
-                             cfg.iou_thr, fmt=fmt, device=dev)
+                             cfg.iou_thr, fmt=fmt, device=dev, **pkw)
     R, C = cfg.grid
     pipe.reserve(F, F * R * ((C + 1) // 2))
     pipe.plan(scores)
@@ -274,7 +316,7 @@ def run_b200(args):
     pipes = [pipe]
     for _ in range(1, args.depth):
         p2 = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
-                               cfg.iou_thr, fmt=fmt, device=dev)
+                               cfg.iou_thr, fmt=fmt, device=dev, **pkw)
         p2.reserve(F, n_win, caps=counts, max_boxes=max(len(boxes), 1))
         pipes.append(p2)
     runner = mp.PipelinedRunner(pipes, device=dev)
@@ -294,14 +336,18 @@ def run_b200(args):
     sampler.start()
     time.sleep(0.3)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    pevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(args.steps)] if nv12 else [None] * args.steps
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0.record(stream)
     runner.s_plan.wait_stream(stream)
+    if runner.s_proxy is not None:
+        runner.s_proxy.wait_stream(stream)
     for i in range(args.steps):
-        runner.step(scores, frames, boxes_t, wbo_t, gather_events=evs[i])
+        runner.step(scores, frames, boxes_t, wbo_t, gather_events=evs[i], proxy_events=pevs[i])
     runner.wait_all(stream)
     t1.record(stream)
     torch.cuda.synchronize()
@@ -310,10 +356,11 @@ def run_b200(args):
     clocks = sampler.stop()
     elapsed_ms = t0.elapsed_time(t1)
     gather_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    proxy_ms = float(np.mean([a.elapsed_time(b) for a, b in pevs])) if nv12 else None
     for p in pipes:
         p.check_status()
 
-    ab = algorithmic_bytes(cfg, windows, frame_off, len(boxes), n_kept, F, fmt_bytes)
+    ab = algorithmic_bytes(cfg, windows, frame_off, len(boxes), n_kept, F, fmt_bytes, 1.5 if nv12 else 3.0)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -327,7 +374,7 @@ def run_b200(args):
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            if pj.get("config") == cfg.name and pj.get("fmt") == args.fmt:
+            if pj.get("config") == cfg.name and pj.get("fmt") == args.fmt and pj.get("src", "rgb24") == args.src:
                 traffic = pj.get("dram_bytes_per_step")
         except (OSError, ValueError):
             pass
@@ -336,6 +383,14 @@ def run_b200(args):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(cfg, clip, scene, scores_np, boxes, wbo, fmt, dev, args)
+    proxy = None
+    if nv12:
+        pb, pbs = (x * F for x in proxy_input_bytes(cfg))
+        proxy = {"dims": list(cfg.proxy_dims), "kernel": "gather_kernel<.., NV12> row-sparse (tile::gather4)",
+                 "launch_ms": proxy_ms, "alg_bytes_per_launch": int(pb),
+                 "alg_bytes_per_launch_samples": int(pbs),
+                 "achieved_GBps": pb / (proxy_ms * 1e-3) / 1e9, "frac": pb / (proxy_ms * 1e-3) / 1e9 / peak,
+                 "frame_bytes_per_launch": int(F * (cfg.H + cfg.H // 2) * cfg.W)}
 
     # the only cross-GPU traffic: int64 counters (SUM) and elapsed time (MAX) over NCCL
     from paper_2103_14695_b200.sharding import Counters, reduce_counters
@@ -352,18 +407,19 @@ def run_b200(args):
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             threads = os.cpu_count() or 1
-            inp, n = oracle_baseline(cfg, clip, threads, 15.0)
+            inp, n = oracle_baseline(cfg, clip, threads, 15.0, args.src)
             dt = oracle_run(cfg, inp, n, threads)
             cpu = {"value": n / dt, "unit": "frames/s", "cores": threads, "kind": "oracle",
-                   "sample": f"first {n} of {F} frames of clip {clip} ({cfg.name}), plan+gather+remap/NMS, "
-                             f"{threads} threads, {host_cpu_desc()}"}
+                   "sample": f"first {n} of {F} frames of clip {clip} ({cfg.name}), "
+                             f"{'proxy-input downscale+' if nv12 else ''}plan+gather+remap/NMS, {args.src} "
+                             f"frames, {threads} threads, {host_cpu_desc()}"}
         line = {
             "metric": "frames/sec of proxy-guided window pipeline", "value": value, "unit": "frames/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": tmax_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg.name, "frames_per_step_per_gpu": F, "W": cfg.W, "H": cfg.H,
-                       "sizes": cfg.sizes, "out_dims": cfg.out_dims, "out_format": args.fmt,
+                       "sizes": cfg.sizes, "out_dims": cfg.out_dims, "out_format": args.fmt, "src": args.src,
                        "b_proxy": cfg.b_proxy, "windows_per_step": n_win, "class_count": counts,
                        "raw_boxes_per_step": int(len(boxes)), "kept_boxes_per_step": n_kept,
                        "l2": "inputs (%.1f GB frames) exceed L2; no flush" % (frames.numel() / 1e9),
@@ -380,8 +436,9 @@ def run_b200(args):
                          "gather_share_of_step": gather_ms / (tmax_ms / args.steps)},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * (mp.launches_per_call(0) + mp.launches_per_call(1) +
+            "gpu_launches": args.steps * (mp.launches_per_call(0) + mp.launches_per_call(1) * (2 if nv12 else 1) +
                                           mp.launches_per_call(2)),
+            "proxy_input": proxy,
             "counters": dataclasses.asdict(glob),
             "clocks": clocks,
         }
@@ -511,18 +568,21 @@ def run_e2e(cfg, clip, scene, scores_np, boxes, wbo, fmt, dev, args):
     import paper_2103_14695_b200 as mp
     F = cfg.frames
     pool = min(F, 128)
-    host_frames = torch.empty((pool, cfg.H, cfg.pitch), dtype=torch.uint8).pin_memory()
+    nv12 = args.src == "nv12"
+    rows, pitch = (cfg.H + cfg.H // 2, cfg.pitch_nv12) if nv12 else (cfg.H, cfg.pitch)
+    host_frames = torch.empty((pool, rows, pitch), dtype=torch.uint8).pin_memory()
     for i in range(pool):
-        host_frames[i].copy_(torch.from_numpy(S.frame_pixels_np(S.frame_seed(clip, i), cfg.H, cfg.pitch)))
+        host_frames[i].copy_(torch.from_numpy(S.frame_pixels_np(S.frame_seed(clip, i), rows, pitch)))
     host_scores = torch.from_numpy(scores_np).pin_memory()
     host_boxes = torch.from_numpy(boxes.view(np.float32).reshape(-1, 6).copy()).pin_memory()
     host_wbo = torch.from_numpy(wbo).pin_memory()
-    frames = torch.empty((F, cfg.H, cfg.pitch), dtype=torch.uint8, device=dev)
+    frames = torch.empty((F, rows, pitch), dtype=torch.uint8, device=dev)
     scores = torch.empty_like(host_scores, device=dev)
     boxes_t = torch.empty_like(host_boxes, device=dev)
     wbo_t = torch.empty_like(host_wbo, device=dev)
+    pkw = dict(src="nv12", proxy_dims=cfg.proxy_dims) if nv12 else {}
     pipe = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
-                             cfg.iou_thr, fmt=fmt, device=dev)
+                             cfg.iou_thr, fmt=fmt, device=dev, **pkw)
     R, C = cfg.grid
     pipe.reserve(F, F * R * ((C + 1) // 2))
     scores.copy_(host_scores)
@@ -533,7 +593,7 @@ def run_e2e(cfg, clip, scene, scores_np, boxes, wbo, fmt, dev, args):
     out_host = torch.empty((pipe.max_out, 6), dtype=torch.float32).pin_memory()
     off_host = torch.empty((F + 1,), dtype=torch.int32).pin_memory()
     stream = torch.cuda.current_stream(dev)
-    h2d = F * cfg.H * cfg.pitch + host_scores.numel() * 4 + host_boxes.numel() * 4 + host_wbo.numel() * 4
+    h2d = F * rows * pitch + host_scores.numel() * 4 + host_boxes.numel() * 4 + host_wbo.numel() * 4
     d2h = off_host.numel() * 4 + out_host.numel() * 4
 
     def step():
@@ -542,6 +602,8 @@ def run_e2e(cfg, clip, scene, scores_np, boxes, wbo, fmt, dev, args):
         scores.copy_(host_scores, non_blocking=True)
         boxes_t.copy_(host_boxes, non_blocking=True)
         wbo_t.copy_(host_wbo, non_blocking=True)
+        if nv12:
+            pipe.proxy_input(frames)
         pipe.plan(scores)
         pipe.gather(frames)
         pipe.merge(boxes_t, wbo_t)
@@ -575,6 +637,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=2, help="batches in flight (buffer sets) in the stream pipeline")
     ap.add_argument("--graphs", type=int, default=1, help="replay plan/merge as CUDA graphs")
+    ap.add_argument("--src", default="rgb24", choices=["rgb24", "nv12"],
+                    help="frame format: rgb24 rows (default) or NV12 decoder output with the proxy-input "
+                         "downscale in the step (NEXT-3)")
     ap.add_argument("--mode", default="path", choices=["path", "sweep", "wsel"],
                     help="path: the hot path a1-a7 (default); sweep: NEXT-1 proxy-module sweep; "
                          "wsel: NEXT-2 window-size selection step")

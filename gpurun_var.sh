@@ -1,6 +1,11 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout -s KILL 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1
-timeout -s KILL 600 python bench.py --steps 100 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/bench_c2.log 2>&1
-for c in c3_1080p_dense c4_4k_drone; do timeout -s KILL 600 python bench.py --config $c --no-e2e --no-cpu-baseline --steps 30 > gpurun_out/bench_$c.log 2>&1; done
-timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"plan_|gather_|nms_" -c 30 --csv --log-file gpurun_out/launches_c4.csv python bench.py --config c4_4k_drone --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --depth 1 > /dev/null 2>&1
+: > gpurun_out/var.log
+run() { env "$@" WHAT=proxy_nv12,proxy_rgb,crops_nv12,crops_rgb timeout -s KILL 300 python scripts/time_gather.py >> gpurun_out/var.log 2>&1; }
+run TAG=base
+run TAG=st3b64 MP_GATHER_STAGES=3 MP_GATHER_BUDGET_KB=64
+run TAG=st2b64 MP_GATHER_STAGES=2 MP_GATHER_BUDGET_KB=64
+run TAG=st2b96 MP_GATHER_STAGES=2 MP_GATHER_BUDGET_KB=96
+run TAG=dbg1 MP_GATHER_DEBUG=1
+run TAG=dbg2 MP_GATHER_DEBUG=2
+timeout -s KILL 900 python -m pytest tests/test_gpu_nv12.py tests/test_gpu_parity.py -q -x > gpurun_out/pytest_nv12.log 2>&1

@@ -32,23 +32,31 @@ namespace mpk {
 
 constexpr int kProducerWarps = 1;
 constexpr int kCW = 8;   // consumer warps per CTA; each owns a block of TR/kCW output rows
-constexpr int kStages = 2;
+constexpr int kStages = 2;      // default ring depth (A.stages; MP_GATHER_STAGES overrides, <= kMaxStages)
+constexpr int kMaxStages = 8;
 constexpr int kHdrBytes = 64;
 constexpr int kMaxTW = 256;
 constexpr int kMaxTR = 96;
 constexpr int kXtapBytes = (kMaxTW + 2) * 8, kYtapBytes = (kMaxTR + 2) * 8;
 constexpr int kTapBytes = kXtapBytes + kYtapBytes;
-constexpr int kStageDataBudget = 44 * 1024;
+constexpr int kStageDataBudget = 44 * 1024;        // dense classes
+constexpr int kSparseStageBudget = 96 * 1024;      // row-sparse classes (measured: 44 KB -> 1.44 ms, 96 KB -> 0.93 ms
+                                                   // for the c2 proxy-input downscale; bytes in flight per SM)
 constexpr int kDataOff = (kHdrBytes + kTapBytes + 127) / 128 * 128;   // TMA destination: 128-B aligned
 
 struct GatherArgs {
-  int k, W, H, pitch, F, fmt, stage_bytes, debug, tensor, src;
+  int k, W, H, pitch, F, fmt, stage_bytes, stages, debug, tensor, src;
+  int wait_mode;             // bit 0: producer sleeps on empty slots, bit 1: consumers sleep on full slots
+  int rpf;                   // row-sparse: rows per frame in the 2-D row view of the frame batch
   int ncol[kMaxClasses];
   int box_w[kMaxClasses], box_h[kMaxClasses];
   int w[kMaxClasses], h[kMaxClasses], ow[kMaxClasses], oh[kMaxClasses];
   int TW[kMaxClasses], TR[kMaxClasses], nct[kMaxClasses], tpw[kMaxClasses];
   int cap[kMaxClasses], list_off[kMaxClasses], xtab_off[kMaxClasses], ytab_off[kMaxClasses];
   int uv_off[kMaxClasses];   // NV12: byte offset of the staged chroma box (after the luma box)
+  int box_huv[kMaxClasses];  // NV12: staged chroma box rows
+  int sparse[kMaxClasses];   // row-sparse staging: only each output row's tap rows are staged
+  int pair_bytes[kMaxClasses];   // row-sparse: staged bytes per output row (RGB 2 rows, NV12 4 rows)
   float cvt[6];              // NV12 (R23): cy, -cy*yo, crv, cgu, cgv, cbu (fp32 of the fp64 coefficients)
   void* out[kMaxClasses];
 };
@@ -66,7 +74,8 @@ struct TileHdr {
   int valid, k, slot, oy0, ox0, rows, cols, stride;
   int x, b0, r_lo, xs, ys;   // window x, staged byte origin, first staged row, tap slice shifts
   int ya;                    // NV12: absolute first staged luma row (its chroma row is ya >> 1)
-  int pad[2];
+  int wy;                    // window y
+  int pad[1];
 };
 static_assert(sizeof(TileHdr) <= kHdrBytes, "header");
 
@@ -94,6 +103,18 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {   // packed a - b 
 
 // u8 -> (2^23 + u8) as an fp32 bit pattern; subtracting 2^23 afterwards is exact.
 __device__ __forceinline__ float u8m(uint32_t b) { return __int_as_float(0x4B000000u + b); }
+
+// (U, V) byte of a 16-bit chroma pair -> (2^23 + byte) as fp32 bits
+// (selector 0x7540: byte 0 = U, 0x7541: byte 1 = V).
+__device__ __forceinline__ float uvf(uint32_t pair, uint32_t sel) {
+  return __int_as_float(__byte_perm(pair, 0x4B000000u, sel));
+}
+
+// clamp to [0, 255] in one VIMNMX.RELU: non-negative fp32 bit patterns order
+// like int32 and negative ones (incl. -0.0) are negative ints -> +0.0.
+__device__ __forceinline__ float clamp255(float v) {
+  return __int_as_float(__vimin_s32_relu(__float_as_int(v), 0x437F0000));
+}
 
 __device__ __forceinline__ uint8_t u8_round(float v) {   // R16: floor(v + 0.5), clamped
   const int r = __float2int_rd(v + 0.5f);
@@ -200,7 +221,6 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
     }
     lx[p] = make_float2(__int_as_float(xa.y), __int_as_float(xb.y));
   }
-  const int ya = hdr->ya;
   float2 P[NP][3], N[NP][3];   // ping-pong horizontal lerps (3 channels x column pair)
 #define MP_HL(H, CH, A0, B0, A1, B1)                                                           \
   {                                                                                             \
@@ -208,17 +228,43 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
     const float2 n_ = make_float2(u8m(smem[A1]), u8m(smem[B1]));                                \
     H[p][CH] = __ffma2_rn(lx[p], fsub2(n_, m_), fsub2(m_, M2));                                  \
   }
-#define MP_H(ROW, H)                                                                            \
+  // NV12 chroma: one 16-bit load per tap fetches the (U, V) pair; bytes are
+  // placed into the 2^23 fp32 pattern with one byte-permute each
+#define MP_HC(H, QA, QB)                                                                        \
   {                                                                                             \
-    const unsigned int o_ = (unsigned int)(ROW) * stride;                                      \
+    const uint32_t la_ = *reinterpret_cast<const uint16_t*>(&smem[QA]);                         \
+    const uint32_t ra_ = *reinterpret_cast<const uint16_t*>(&smem[(QA) + da[p]]);                \
+    const uint32_t lb_ = *reinterpret_cast<const uint16_t*>(&smem[QB]);                         \
+    const uint32_t rb_ = *reinterpret_cast<const uint16_t*>(&smem[(QB) + db[p]]);                \
+    const float2 mu_ = make_float2(uvf(la_, 0x7540), uvf(lb_, 0x7540));                         \
+    const float2 nu_ = make_float2(uvf(ra_, 0x7540), uvf(rb_, 0x7540));                         \
+    const float2 mv_ = make_float2(uvf(la_, 0x7541), uvf(lb_, 0x7541));                         \
+    const float2 nv_ = make_float2(uvf(ra_, 0x7541), uvf(rb_, 0x7541));                         \
+    H[p][1] = __ffma2_rn(lx[p], fsub2(nu_, mu_), fsub2(mu_, M2));                                \
+    H[p][2] = __ffma2_rn(lx[p], fsub2(nv_, mv_), fsub2(mv_, M2));                                \
+  }
+  // NV12 luma only (the chroma lerps are copied from PREV: same chroma row)
+#define MP_HY(O_, H, PREV)                                                                      \
+  {                                                                                             \
+    const unsigned int o_ = (O_);                                                               \
+    _Pragma("unroll") for (int p = 0; p < NP; p++) {                                            \
+      const unsigned int pa_ = ba[p] + o_, pb_ = bb[p] + o_;                                    \
+      MP_HL(H, 0, pa_, pb_, pa_ + 1, pb_ + 1)                                                   \
+      H[p][1] = PREV[p][1];                                                                     \
+      H[p][2] = PREV[p][2];                                                                     \
+    }                                                                                           \
+  }
+  // horizontal lerps of one staged source row: luma/RGB row at byte offset
+  // O_, its chroma row (NV12) at OC_ (both relative to the staged boxes)
+#define MP_H(O_, OC_, H)                                                                        \
+  {                                                                                             \
+    const unsigned int o_ = (O_);                                                               \
     if (SRC == kSrcNV12) {                                                                      \
-      const unsigned int oc_ = (unsigned int)(((ya + (ROW)) >> 1) - (ya >> 1)) * stride;       \
+      const unsigned int oc_ = (OC_);                                                           \
       _Pragma("unroll") for (int p = 0; p < NP; p++) {                                          \
         const unsigned int pa_ = ba[p] + o_, pb_ = bb[p] + o_;                                  \
-        const unsigned int qa_ = ca[p] + oc_, qb_ = cb[p] + oc_;                                \
         MP_HL(H, 0, pa_, pb_, pa_ + 1, pb_ + 1)                                                 \
-        MP_HL(H, 1, qa_, qb_, qa_ + da[p], qb_ + db[p])                                         \
-        MP_HL(H, 2, qa_ + 1, qb_ + 1, qa_ + 1 + da[p], qb_ + 1 + db[p])                         \
+        MP_HC(H, ca[p] + oc_, cb[p] + oc_)                                                      \
       }                                                                                         \
     } else {                                                                                    \
       _Pragma("unroll") for (int p = 0; p < NP; p++) {                                          \
@@ -227,6 +273,19 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
             MP_HL(H, ch, pa_ + ch, pb_ + ch, pa_ + 3 + ch, pb_ + 3 + ch)                        \
       }                                                                                         \
     }                                                                                           \
+  }
+  // dense staging: source row r of the box (rows r_lo..); its chroma row is
+  // ((ya + r) >> 1) - (ya >> 1) of the chroma box (ya = first staged luma row)
+  const int ya = hdr->ya;
+#define MP_HD(ROW, H) \
+  MP_H((unsigned int)(ROW) * stride, (unsigned int)(((ya + (ROW)) >> 1) - (ya >> 1)) * stride, H)
+  // row ROW after row ROW-1 (held in PREV): NV12 rows with odd ya + ROW share
+  // their chroma row with the previous one -> only the luma is lerped
+#define MP_HD2(ROW, H, PREV)                                                                    \
+  if (SRC == kSrcNV12 && ((ya + (ROW)) & 1)) {                                                  \
+    MP_HY((unsigned int)(ROW) * stride, H, PREV)                                                \
+  } else {                                                                                      \
+    MP_HD(ROW, H)                                                                               \
   }
   // vertical lerp of column pair p -> v0, v1, v2 (RGB); NV12: the lerped
   // Y, U, V are converted to R'G'B' and clamped to [0, 255] (R23)
@@ -245,29 +304,27 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
     v1 = __ffma2_rn(CGU, uu_, __ffma2_rn(CGV, vv_, yy_));                                       \
     v2 = __ffma2_rn(CBU, uu_, yy_);                                                             \
     if (FMT == MP_OUT_F32_NCHW) {                                                               \
-      v0 = make_float2(fminf(fmaxf(v0.x, 0.0f), 255.0f), fminf(fmaxf(v0.y, 0.0f), 255.0f));     \
-      v1 = make_float2(fminf(fmaxf(v1.x, 0.0f), 255.0f), fminf(fmaxf(v1.y, 0.0f), 255.0f));     \
-      v2 = make_float2(fminf(fmaxf(v2.x, 0.0f), 255.0f), fminf(fmaxf(v2.y, 0.0f), 255.0f));     \
+      v0 = make_float2(clamp255(v0.x), clamp255(v0.y));                                         \
+      v1 = make_float2(clamp255(v1.x), clamp255(v1.y));                                         \
+      v2 = make_float2(clamp255(v2.x), clamp255(v2.y));                                         \
     }                                                                                           \
   }
   const int ow = A.ow[q], oh = A.oh[q];
-  int orow = rb0;
-  int2 y = yt[orow];
-  y.x -= r_lo;
-  int r = y.x;
-  const int rlast = yt[rb1 - 1].x - r_lo + 1;
-  MP_H(r, P)
+  const bool sparse = A.sparse[q] != 0;
+  const unsigned int pair = (unsigned int)A.pair_bytes[q];
+  const int wy = hdr->wy;
+  bool ok[NCOL];
+#pragma unroll
+  for (int j = 0; j < NCOL; j++) ok[j] = lane + 32 * j < cols;
+  // one output row from top/bottom horizontal lerps T, B with weight y.y
   if (FMT == MP_OUT_F32_NCHW) {
     const size_t plane = (size_t)oh * ow;
     float* o0 = reinterpret_cast<float*>(A.out[q]) + (size_t)hdr->slot * 3 * plane +
                 (size_t)(hdr->oy0 + rb0) * ow + hdr->ox0 + lane;
     float* o1 = o0 + plane;
     float* o2 = o1 + plane;
-    bool ok[NCOL];
-#pragma unroll
-    for (int j = 0; j < NCOL; j++) ok[j] = lane + 32 * j < cols;
-#define MP_EMIT(T, B)                                                                           \
-  while (orow < rb1 && y.x == r) {                                                              \
+#define MP_ROW(T, B)                                                                            \
+  {                                                                                             \
     const float2 ly = make_float2(__int_as_float(y.y), __int_as_float(y.y));                    \
     _Pragma("unroll") for (int p = 0; p < NP; p++) {                                            \
       MP_V(T, B)                                                                                \
@@ -285,27 +342,14 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
     o0 += ow;                                                                                   \
     o1 += ow;                                                                                   \
     o2 += ow;                                                                                   \
-    orow++;                                                                                     \
-    if (orow < rb1) { y = yt[orow]; y.x -= r_lo; }                                              \
   }
-    while (r < rlast) {
-      MP_H(r + 1, N)
-      MP_EMIT(P, N)
-      r++;
-      if (r >= rlast) break;
-      MP_H(r + 1, P)
-      MP_EMIT(N, P)
-      r++;
-    }
-#undef MP_EMIT
+#include "mp_gather_rows.inc"
+#undef MP_ROW
   } else {
     uint8_t* o = reinterpret_cast<uint8_t*>(A.out[q]) +
                  (((size_t)hdr->slot * oh + hdr->oy0 + rb0) * ow + hdr->ox0 + lane) * 3;
-    bool ok[NCOL];
-#pragma unroll
-    for (int j = 0; j < NCOL; j++) ok[j] = lane + 32 * j < cols;
-#define MP_EMIT(T, B)                                                                           \
-  while (orow < rb1 && y.x == r) {                                                              \
+#define MP_ROW(T, B)                                                                            \
+  {                                                                                             \
     const float2 ly = make_float2(__int_as_float(y.y), __int_as_float(y.y));                    \
     _Pragma("unroll") for (int p = 0; p < NP; p++) {                                            \
       MP_V(T, B)                                                                                \
@@ -321,22 +365,16 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
       }                                                                                         \
     }                                                                                           \
     o += (size_t)ow * 3;                                                                        \
-    orow++;                                                                                     \
-    if (orow < rb1) { y = yt[orow]; y.x -= r_lo; }                                              \
   }
-    while (r < rlast) {
-      MP_H(r + 1, N)
-      MP_EMIT(P, N)
-      r++;
-      if (r >= rlast) break;
-      MP_H(r + 1, P)
-      MP_EMIT(N, P)
-      r++;
-    }
-#undef MP_EMIT
+#include "mp_gather_rows.inc"
+#undef MP_ROW
   }
 #undef MP_V
+#undef MP_HD2
+#undef MP_HD
 #undef MP_H
+#undef MP_HY
+#undef MP_HC
 #undef MP_HL
 }
 
@@ -350,13 +388,14 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
                                                                  const int* __restrict__ frame_off,
                                                                  const int2* __restrict__ ws_tap,
                                                                  int* __restrict__ d_status) {
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * A.stage_bytes);
-  uint64_t* empty = full + kStages;
+  const int nst = A.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nst * A.stage_bytes);
+  uint64_t* empty = full + nst;
   __shared__ int cnt[kMaxClasses];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid < kMaxClasses) cnt[tid] = tid < A.k ? ws_cnt[tid] : 0;
   if (tid == 0) {
-    for (int s = 0; s < kStages; s++) {
+    for (int s = 0; s < nst; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kCW);
     }
@@ -422,12 +461,15 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
     for (int i = 0;; i++) {
       const int t = blockIdx.x + i * G;   // round-robin: concurrently processed tiles are
       if (t >= T) break;                   // neighbours in the frames and in the outputs
-      const int s = i % kStages;
+      const int s = i % nst;
       if (t + G < T) {
         decode(t + G, nxt);
         prefetch(nxt, dnxt, clo_nxt, rlo_nxt, rhi_nxt);
       }
-      if (i >= kStages) mbar_wait_sleep(&empty[s], ((i / kStages) - 1) & 1);
+      if (i >= nst) {
+        if (A.wait_mode & 1) mbar_wait_sleep(&empty[s], ((i / nst) - 1) & 1);
+        else mbar_wait(&empty[s], ((i / nst) - 1) & 1);
+      }
       unsigned char* stage = smem + (size_t)s * A.stage_bytes;
       TileHdr* hdr = reinterpret_cast<TileHdr*>(stage);
       unsigned char* xt = stage + kHdrBytes;
@@ -460,15 +502,23 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
           hdr->xs = xs;
           hdr->ys = ys;
           hdr->ya = dcur.y + rlo_cur;
+          hdr->wy = dcur.y;
           if (A.debug == 2) {   // experiment: no pixel copies (compute-only bound)
             mbar_arrive_expect_tx(&full[s], xbytes + ybytes);
+            bulk_g2s(xt, ws_tap + (xe - xs), xbytes, &full[s]);
+            bulk_g2s(yt, ws_tap + (ye - ys), ybytes, &full[s]);
+          } else if (A.sparse[q]) {
+            // row-sparse: the warp issues the 4-row TMA gathers below (RGB: two
+            // output rows per gather, odd counts padded; NV12: one per row)
+            const uint32_t nrow4 = SRC == kSrcNV12 ? (uint32_t)cur.rows : (uint32_t)(cur.rows + 1) / 2;
+            mbar_arrive_expect_tx(&full[s], nrow4 * (uint32_t)(4 * stride) + xbytes + ybytes);
             bulk_g2s(xt, ws_tap + (xe - xs), xbytes, &full[s]);
             bulk_g2s(yt, ws_tap + (ye - ys), ybytes, &full[s]);
           } else if (SRC == kSrcNV12) {
             // two TMA boxes from the same column origin b0: luma rows ya.., then
             // chroma rows (ya >> 1).. of the interleaved UV plane (R23)
             const int ya = dcur.y + rlo_cur;
-            mbar_arrive_expect_tx(&full[s], (uint32_t)(stride * A.box_h[q]) + (uint32_t)(stride * ((A.box_h[q] >> 1) + 1)) +
+            mbar_arrive_expect_tx(&full[s], (uint32_t)(stride * A.box_h[q]) + (uint32_t)(stride * A.box_huv[q]) +
                                                 xbytes + ybytes);
             bulk_g2s(xt, ws_tap + (xe - xs), xbytes, &full[s]);
             bulk_g2s(yt, ws_tap + (ye - ys), ybytes, &full[s]);
@@ -495,6 +545,35 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
         }
       }
       __syncwarp();
+      if (A.sparse[q] && dcur.valid && A.debug != 2) {
+        // row-sparse staging (strong vertical downscale): output row j of the
+        // tile needs source rows (i0_j, i0_j + 1) only (and, for NV12, chroma
+        // rows (y+i0_j)>>1 and the one after), fetched with sm_100 TMA row
+        // gathers (tile::gather4) over the 2-D row view of the frame batch
+        // (row = frame * rpf + row-in-frame; NV12 chroma rows follow the H
+        // luma rows).  Rows no tap touches are never read.  Lanes issue in
+        // parallel; lane 0 posted the byte count above.
+        const int b0 = ((SRC == kSrcNV12 ? 1 : 3) * (dcur.x + clo_cur)) & ~15;
+        const int fr = dcur.frame * A.rpf;
+        const int stride = A.box_w[q];
+        const int* ytap = &ws_tap[A.ytab_off[q] + cur.oy0].x;
+        if (SRC == kSrcNV12) {
+          for (int j = lane; j < cur.rows; j += 32) {
+            const int ry = dcur.y + __ldg(ytap + 2 * j);
+            // rows: luma i0, i0+1, then the chroma rows of those two luma
+            // rows (equal when y+i0 is even: the repeat is an L2 hit)
+            const int lr = fr + ry, cr = fr + A.H;
+            tma_gather4(data + (size_t)j * (4 * stride), &tm.m[q], b0 >> 3, lr, lr + 1, cr + (ry >> 1),
+                        cr + ((ry + 1) >> 1), &full[s]);
+          }
+        } else {
+          for (int jj = lane; 2 * jj < cur.rows; jj += 32) {
+            const int r0 = fr + dcur.y + __ldg(ytap + 4 * jj);
+            const int r1 = fr + dcur.y + __ldg(ytap + 2 * min(2 * jj + 1, cur.rows - 1));
+            tma_gather4(data + (size_t)jj * (4 * stride), &tm.m[q], b0 >> 3, r0, r0 + 1, r1, r1 + 1, &full[s]);
+          }
+        }
+      }
       cur = nxt;
       dcur = dnxt;
       clo_cur = clo_nxt;
@@ -508,8 +587,9 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
   for (int i = 0;; i++) {
     const int t = blockIdx.x + i * G;
     if (t >= T) break;
-    const int s = i % kStages;
-    mbar_wait_sleep(&full[s], (i / kStages) & 1);
+    const int s = i % nst;
+    if (A.wait_mode & 2) mbar_wait_sleep(&full[s], (i / nst) & 1);
+    else mbar_wait(&full[s], (i / nst) & 1);
     const unsigned int soff = (unsigned int)s * (unsigned int)A.stage_bytes;
     const TileHdr* hdr = reinterpret_cast<const TileHdr*>(&smem[soff]);
     if (hdr->valid && A.debug != 1) {
@@ -563,17 +643,22 @@ static void class_box(int in_w, int in_h, int ow, int oh, int TW, int TR, int sr
   *box_h = max_rows;
 }
 
-// Staged bytes of a class box: RGB24 = the box; NV12 = the luma box (padded to
-// 128 B for the second TMA destination) + the chroma box (box_h/2 + 1 rows:
-// the chroma rows of box_h consecutive luma rows starting at any parity).
-static long long stage_data_bytes(int src, int bw, int bh) {
+// Staged bytes of a class box.  Dense: RGB24 = the box; NV12 = the luma box
+// (padded to 128 B for the second TMA destination) + the chroma box (box_h/2 +
+// 1 rows: the chroma rows of box_h consecutive luma rows at any parity).
+// Row-sparse: TR row pairs of 2 box rows each (128-B aligned), twice for NV12.
+static long long pair_bytes(int src, int bw) { return (src == kSrcNV12 ? 4LL : 2LL) * bw; }
+static long long stage_data_bytes(int src, bool sparse, int bw, int bh, int TR) {
+  if (sparse) return (long long)TR * pair_bytes(src, bw);   // TR is a multiple of kCW (even)
   if (src != kSrcNV12) return (long long)bw * bh;
   return ((long long)bw * bh + 127) / 128 * 128 + (long long)bw * (bh / 2 + 1);
 }
 
-static bool build_gather_args(int src, int pitch, int W, int H, int F, int k, const mp_size* sizes,
-                              const mp_size* out_dims, void* const* d_out, const int32_t* out_cap,
-                              mp_out_format fmt, GatherArgs* A) {
+// allow_sparse: the entry point stages through a TMA tensor map (row-sparse
+// staging needs 2-row boxes); the pointer-array path always stages densely.
+static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int H, int F, int k,
+                              const mp_size* sizes, const mp_size* out_dims, void* const* d_out,
+                              const int32_t* out_cap, mp_out_format fmt, GatherArgs* A) {
   if (W < 1 || H < 1 || W > 16384 || H > 16384 || F < 0 || k < 1 || k > kMaxClasses) return false;
   if (pitch < (src == kSrcNV12 ? W : 3 * W) || (pitch & 15)) return false;
   if (src == kSrcNV12 && ((W & 1) || (H & 1))) return false;
@@ -589,7 +674,8 @@ static bool build_gather_args(int src, int pitch, int W, int H, int F, int k, co
   A->src = src;
   long long data_max = 0;
   int list = 0, taps = 0;
-  const long long budget = kStageDataBudget;
+  const char* bud = getenv("MP_GATHER_BUDGET_KB");   // experiment knob
+  const long long budget = (bud && atoi(bud) >= 8) ? 1024LL * atoi(bud) : kStageDataBudget;
   for (int q = 0; q < k; q++) {
     const int w = sizes[q].w, h = sizes[q].h, ow = out_dims[q].w, oh = out_dims[q].h;
     if (w < 1 || h < 1 || w > W || h > H || ow < 1 || oh < 1 || ow > 16384 || oh > 16384) return false;
@@ -609,18 +695,32 @@ static bool build_gather_args(int src, int pitch, int W, int H, int F, int k, co
     // else equal tiles rounded up to a multiple of 8 (full 32-B sectors).
     // Rows per warp: the tallest Rw whose box fits the stage budget and the
     // TMA limits.  Narrower fallbacks only when nothing fits.
+    // Row-sparse staging when the vertical downscale exceeds 2x (h > 2 oh):
+    // output rows then share no source rows, and staging only each row's two
+    // taps reads fewer bytes than the contiguous box (e.g. the proxy-input
+    // downscale, NEXT-3).  No halo rows, so short (Rw = 1) tiles are fine.
+    const bool sparse = allow_sparse && h > 2 * oh;
+    const int min_rw = sparse ? 1 : 3;
+    const long long cbudget = (sparse && !bud) ? (long long)kSparseStageBudget : budget;
     int TW = 0, TR = 0, bw = 0, bh = 0;
     auto fit_rows = [&](int tw, int& rw, int& cbw, int& cbh) {
       for (rw = 8; rw >= 1; rw--) {
         class_box(w, h, ow, oh, tw, kCW * rw, src, &cbw, &cbh);
-        if (stage_data_bytes(src, cbw, cbh) <= budget && cbw <= 2048 && cbh <= 256) return true;
+        if (sparse) {   // gather4 destinations: 4 rows x box_w bytes, 128-B aligned
+          cbh = 1;
+          cbw = (cbw + 31) / 32 * 32;
+        }
+        if (stage_data_bytes(src, sparse, cbw, cbh, kCW * rw) <= cbudget && cbw <= 2048 && cbh <= 256)
+          return true;
       }
       return false;
     };
-    for (int tw = kMaxTW; tw >= 32 && !TW; tw -= 32) {
+    // (a 32-multiple divisor narrower than 128 columns, e.g. 32 for ow = 416,
+    // loses to the equal split: per-tile overheads dominate narrow tiles)
+    for (int tw = kMaxTW; tw >= (ow < 128 ? 32 : 128) && !TW; tw -= 32) {
       if (ow % tw) continue;
       int rw, cbw, cbh;
-      if (fit_rows(tw, rw, cbw, cbh) && rw >= 3) {
+      if (fit_rows(tw, rw, cbw, cbh) && rw >= min_rw) {
         TW = tw;
         TR = kCW * rw;
         bw = cbw;
@@ -632,7 +732,7 @@ static bool build_gather_args(int src, int pitch, int W, int H, int F, int k, co
       tw = (tw + 7) / 8 * 8;
       if (tw > kMaxTW) continue;
       int rw, cbw, cbh;
-      if (fit_rows(tw, rw, cbw, cbh) && (rw >= 3 || tw <= 32)) {
+      if (fit_rows(tw, rw, cbw, cbh) && (rw >= min_rw || tw <= 32)) {
         TW = tw;
         TR = kCW * rw;
         bw = cbw;
@@ -647,6 +747,10 @@ static bool build_gather_args(int src, int pitch, int W, int H, int F, int k, co
         TW = ftw;
         TR = kCW * frw;
         class_box(w, h, ow, oh, TW, TR, src, &bw, &bh);
+        if (sparse) {
+          bh = 1;
+          bw = (bw + 31) / 32 * 32;
+        }
       }
     }
     if (TW == 0) return false;   // too strong a downscale of too wide a window: unsupported
@@ -657,7 +761,10 @@ static bool build_gather_args(int src, int pitch, int W, int H, int F, int k, co
     A->TR[q] = TR;
     A->box_w[q] = bw;
     A->box_h[q] = bh;
-    A->uv_off[q] = (int)(((long long)bw * bh + 127) / 128 * 128);
+    A->sparse[q] = sparse ? 1 : 0;
+    A->pair_bytes[q] = (int)pair_bytes(src, bw);
+    A->box_huv[q] = bh / 2 + 1;
+    A->uv_off[q] = sparse ? 2 * bw : (int)(((long long)bw * bh + 127) / 128 * 128);
     A->nct[q] = (ow + TW - 1) / TW;
     A->tpw[q] = A->nct[q] * ((oh + TR - 1) / TR);
     A->cap[q] = out_cap[q];
@@ -668,7 +775,7 @@ static bool build_gather_args(int src, int pitch, int W, int H, int F, int k, co
     taps += ow;
     A->ytab_off[q] = taps;
     taps += oh;
-    if (stage_data_bytes(src, bw, bh) > data_max) data_max = stage_data_bytes(src, bw, bh);
+    if (stage_data_bytes(src, sparse, bw, bh, TR) > data_max) data_max = stage_data_bytes(src, sparse, bw, bh, TR);
   }
   A->stage_bytes = (int)((kDataOff + data_max + 64 + 127) / 128 * 128);
   return true;
@@ -724,7 +831,12 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
   gather_prep_kernel<<<256, kPrepThreads, 0, s>>>(A, d_windows, d_frame_off, ws_cnt, ws_list, ws_tap, n_taps, d_status);
   MP_CUDA_TRY(cudaGetLastError());
   if (A.F == 0) return MP_OK;
-  const size_t smem = (size_t)kStages * A.stage_bytes + 2 * kStages * sizeof(uint64_t);
+  const char* wm = getenv("MP_GATHER_WAIT");   // experiment knob
+  A.wait_mode = wm ? atoi(wm) : 3;
+  const char* stg = getenv("MP_GATHER_STAGES");   // experiment knob
+  A.stages = stg ? atoi(stg) : kStages;
+  if (A.stages < 2 || A.stages > kMaxStages) A.stages = kStages;
+  const size_t smem = (size_t)A.stages * A.stage_bytes + 2 * A.stages * sizeof(uint64_t);
   if (smem > 227 * 1024) return MP_ERR_UNSUPPORTED;
   int dev = 0, sms = 0, per_sm = 0;
   MP_CUDA_TRY(cudaGetDevice(&dev));
@@ -756,7 +868,7 @@ extern "C" mp_status mp_gather_resize(const uint8_t* const* d_frame_ptrs, int32_
                                       void* const* d_out, const int32_t* out_cap, mp_out_format fmt,
                                       int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
   GatherArgs A;
-  if (!build_gather_args(kSrcRGB24, pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A))
+  if (!build_gather_args(kSrcRGB24, false, pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A))
     return MP_ERR_INVALID;
   if (!d_frame_off || !d_status || (F > 0 && (!d_frame_ptrs || !d_windows))) return MP_ERR_INVALID;
   TmapArray tm;
@@ -792,6 +904,26 @@ static bool encode_plane(EncodeTiledFn encode, CUtensorMap* m, const void* base,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The frame batch as a 2-D tensor of rows [F * rpf][pitch/8] (rpf = rows per
+// frame = frame_stride / pitch) with a one-row box of box_w bytes: the view
+// the tile::gather4 row gathers of row-sparse classes index.
+static bool encode_rows(EncodeTiledFn encode, CUtensorMap* m, const void* base, int pitch, int64_t total_rows,
+                        int box_w) {
+  const cuuint64_t gdim[2] = {(cuuint64_t)(pitch / 8), (cuuint64_t)total_rows};
+  const cuuint64_t gstride[1] = {(cuuint64_t)pitch};
+  const cuuint32_t box[2] = {(cuuint32_t)(box_w / 8), 1};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Row-sparse staging needs the 2-D row view: frame_stride a multiple of pitch.
+static bool row_view_ok(int64_t frame_stride, int pitch, int F) {
+  return pitch > 0 && frame_stride > 0 && frame_stride % pitch == 0 &&
+         (int64_t)F * (frame_stride / pitch) < (int64_t(1) << 31);
+}
+
 extern "C" mp_status mp_gather_resize_strided(const uint8_t* d_frames, int64_t frame_stride, int32_t pitch,
                                               int32_t W, int32_t H, int32_t F, const mp_window* d_windows,
                                               const int32_t* d_frame_off, int32_t k, const mp_size* sizes,
@@ -799,8 +931,10 @@ extern "C" mp_status mp_gather_resize_strided(const uint8_t* d_frames, int64_t f
                                               mp_out_format fmt, int32_t* d_status, void* d_ws, size_t ws_bytes,
                                               void* stream) {
   GatherArgs A;
-  if (!build_gather_args(kSrcRGB24, pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A))
+  const bool rows = row_view_ok(frame_stride, pitch, F);
+  if (!build_gather_args(kSrcRGB24, rows, pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A))
     return MP_ERR_INVALID;
+  A.rpf = rows ? (int)(frame_stride / pitch) : 0;
   if (!d_frame_off || !d_status || (F > 0 && (!d_frames || !d_windows))) return MP_ERR_INVALID;
   if (F > 0 && (((uintptr_t)d_frames) & 15)) return MP_ERR_INVALID;
   if (frame_stride < (int64_t)H * pitch || (frame_stride & 15) || frame_stride >= (int64_t(1) << 40))
@@ -811,9 +945,13 @@ extern "C" mp_status mp_gather_resize_strided(const uint8_t* d_frames, int64_t f
   if (F > 0) {
     EncodeTiledFn encode = get_encode();
     if (!encode) return MP_ERR_CUDA;
-    for (int q = 0; q < k; q++)
-      if (!encode_plane(encode, &tm.m[q], d_frames, pitch, H, F, frame_stride, A.box_w[q], A.box_h[q]))
-        return MP_ERR_UNSUPPORTED;
+    for (int q = 0; q < k; q++) {
+      const bool ok = A.sparse[q]
+                          ? encode_rows(encode, &tm.m[q], d_frames, pitch, (int64_t)F * A.rpf, A.box_w[q])
+                          : encode_plane(encode, &tm.m[q], d_frames, pitch, H, F, frame_stride, A.box_w[q],
+                                         A.box_h[q]);
+      if (!ok) return MP_ERR_UNSUPPORTED;
+    }
   }
   return gather_launch(A, tm, nullptr, d_windows, d_frame_off, k, out_dims, out_cap, fmt, d_status, d_ws,
                        ws_bytes, stream);
@@ -845,8 +983,10 @@ extern "C" mp_status mp_gather_resize_nv12(const uint8_t* d_frames, int64_t fram
                                            mp_out_format fmt, mp_color_matrix matrix, int32_t* d_status,
                                            void* d_ws, size_t ws_bytes, void* stream) {
   GatherArgs A;
-  if (!build_gather_args(kSrcNV12, pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A))
+  const bool rows = row_view_ok(frame_stride, pitch, F);
+  if (!build_gather_args(kSrcNV12, rows, pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A))
     return MP_ERR_INVALID;
+  A.rpf = rows ? (int)(frame_stride / pitch) : 0;
   if (!nv12_coefficients((int)matrix, A.cvt)) return MP_ERR_INVALID;
   if (!d_frame_off || !d_status || (F > 0 && (!d_frames || !d_windows))) return MP_ERR_INVALID;
   if (F > 0 && (((uintptr_t)d_frames) & 15)) return MP_ERR_INVALID;
@@ -860,10 +1000,13 @@ extern "C" mp_status mp_gather_resize_nv12(const uint8_t* d_frames, int64_t fram
     if (!encode) return MP_ERR_CUDA;
     const uint8_t* uv = d_frames + (size_t)H * pitch;
     for (int q = 0; q < k; q++) {
-      if (!encode_plane(encode, &tm.m[q], d_frames, pitch, H, F, frame_stride, A.box_w[q], A.box_h[q]) ||
-          !encode_plane(encode, &tm.m[kMaxClasses + q], uv, pitch, H / 2, F, frame_stride, A.box_w[q],
-                        A.box_h[q] / 2 + 1))
-        return MP_ERR_UNSUPPORTED;
+      const bool ok =
+          A.sparse[q] ? encode_rows(encode, &tm.m[q], d_frames, pitch, (int64_t)F * A.rpf, A.box_w[q])
+                      : (encode_plane(encode, &tm.m[q], d_frames, pitch, H, F, frame_stride, A.box_w[q],
+                                      A.box_h[q]) &&
+                         encode_plane(encode, &tm.m[kMaxClasses + q], uv, pitch, H / 2, F, frame_stride,
+                                      A.box_w[q], A.box_huv[q]));
+      if (!ok) return MP_ERR_UNSUPPORTED;
     }
   }
   return gather_launch(A, tm, nullptr, d_windows, d_frame_off, k, out_dims, out_cap, fmt, d_status, d_ws,

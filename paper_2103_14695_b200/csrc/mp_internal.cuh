@@ -180,6 +180,18 @@ __device__ __forceinline__ void tma_load_3d(void* dst_smem, const void* tmap, in
       : "memory");
 }
 
+// sm_100 TMA row gather: four rows r0..r3 (arbitrary indices) of a 2-D tensor
+// map whose box is {width, 1}, starting at column c0, land back to back in
+// shared memory (4 x width elements); completion as tx bytes on `bar`.
+__device__ __forceinline__ void tma_gather4(void* dst_smem, const void* tmap, int c0, int r0, int r1, int r2,
+                                            int r3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst_smem)),
+      "l"(tmap), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ----------------------------------------------------------------- misc
 __host__ __device__ __forceinline__ int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -3,9 +3,15 @@
 It owns the device buffers (torch CUDA tensors) and runs, on one stream and
 without host synchronisation, the three C-ABI calls of libmp_b200.so:
 
+    proxy_input(frames)     NEXT-3 full-frame downscale to the proxy's input
+                                   resolution (P:145, P:167), optional
     plan(scores)            a1-a4  mp_plan_windows
-    gather(frames)          a5     mp_gather_resize -> one batched tensor per size class
+    gather(frames)          a5     mp_gather_resize[_strided|_nv12] -> one batched
+                                   tensor per size class
     merge(boxes, offsets)   a6-a7  mp_remap_nms
+
+Frames are RGB24 rows (src="rgb24") or NV12 decoder output (src="nv12",
+[F, H*3/2, pitch] uint8, reading R23).
 
 Buffers are sized once (`reserve`) and reused, so a step is graph-capturable.
 All arithmetic runs in the CUDA kernels; torch only provides memory/streams.
@@ -23,10 +29,15 @@ class WindowPipeline:
     def __init__(self, W: int, H: int, sizes: Sequence[Tuple[int, int]], cost: Sequence[int],
                  out_dims: Sequence[Tuple[int, int]], b_proxy: float = 0.5, score_thr: float = 0.25,
                  iou_thr: float = 0.5, fmt: int = B.MP_OUT_F32_NCHW, cell: int = 32, device="cuda",
-                 want_mask: bool = False):
+                 want_mask: bool = False, src: str = "rgb24", matrix: int = B.MP_BT709_LIMITED,
+                 proxy_dims: Optional[Tuple[int, int]] = None):
+        if src not in ("rgb24", "nv12"):
+            raise ValueError("src must be 'rgb24' or 'nv12'")
         self.params = B.PlanParams(W, H, sizes, cost, b_proxy, cell, cell)
         self.W, self.H = int(W), int(H)
-        self.pitch = (3 * self.W + 15) // 16 * 16
+        self.src, self.matrix = src, int(matrix)
+        self.proxy_dims = (int(proxy_dims[0]), int(proxy_dims[1])) if proxy_dims else None
+        self.pitch = (3 * self.W + 15) // 16 * 16 if src == "rgb24" else (self.W + 15) // 16 * 16
         self.sizes = list(self.params.sizes)
         self.out_dims = [(int(a), int(b)) for (a, b) in out_dims]
         self.k = len(self.sizes)
@@ -54,6 +65,17 @@ class WindowPipeline:
                          if self.want_mask else None)
             self.plan_ws = torch.empty(max(B.mp_plan_workspace_size(self.params, self.F), 1), dtype=torch.uint8,
                                        device=dev)
+            if self.proxy_dims:
+                # one full-frame window per frame in a single class whose output is the proxy resolution
+                pw, ph = self.proxy_dims
+                f = torch.arange(self.F, dtype=torch.int32)
+                z = torch.zeros_like(f)
+                self.proxy_windows = torch.stack([f, z, z, z + self.W, z + self.H, z, f], 1).contiguous().to(dev) \
+                    if self.F else torch.zeros((1, 7), dtype=torch.int32, device=dev)
+                self.proxy_frame_off = torch.arange(self.F + 1, dtype=torch.int32).to(dev)
+                self.proxy_out = torch.empty((self.F, 3, ph, pw), dtype=torch.float32, device=dev)
+                self.proxy_ws = torch.empty(max(B.mp_gather_workspace_size([self.proxy_dims], [self.F]), 1),
+                                            dtype=torch.uint8, device=dev)
         if caps is not None and list(caps) != self.caps:
             self.caps = [int(c) for c in caps]
             self.outs = []
@@ -80,11 +102,31 @@ class WindowPipeline:
         B.mp_plan_windows(self.params, scores, F, self.mask, self.windows, self.frame_off, self.class_count,
                           self.status, self.plan_ws, stream)
 
+    def proxy_input(self, frames: torch.Tensor, stream=None):
+        """NEXT-3: every frame downscaled (R15 bilinear; NV12 converted, R23) to
+        the proxy's input resolution -> self.proxy_out f32 [F, 3, ph, pw]."""
+        if not self.proxy_dims:
+            raise ValueError("pipeline built without proxy_dims")
+        one = [(self.W, self.H)]
+        if self.src == "nv12":
+            B.mp_gather_resize_nv12(frames, self.W, self.H, self.proxy_windows, self.proxy_frame_off, one,
+                                    [self.proxy_dims], [self.proxy_out], B.MP_OUT_F32_NCHW, self.status,
+                                    self.proxy_ws, self.matrix, stream)
+        else:
+            B.mp_gather_resize_strided(frames, self.W, self.H, self.proxy_windows, self.proxy_frame_off, one,
+                                       [self.proxy_dims], [self.proxy_out], B.MP_OUT_F32_NCHW, self.status,
+                                       self.proxy_ws, stream)
+
     def gather(self, frames: torch.Tensor, stream=None):
-        """frames: either a uint8 [F, H, pitch] batch tensor (TMA tensor path,
-        mp_gather_resize_strided) or an int64 [F] tensor of frame addresses
-        (pointer-array path, mp_gather_resize)."""
-        if frames.dtype == torch.uint8:
+        """frames: a uint8 [F, H, pitch] RGB24 batch tensor (TMA tensor path,
+        mp_gather_resize_strided), an int64 [F] tensor of RGB24 frame addresses
+        (pointer-array path, mp_gather_resize), or, with src="nv12", a uint8
+        [F, H*3/2, pitch] NV12 batch (mp_gather_resize_nv12)."""
+        if self.src == "nv12":
+            B.mp_gather_resize_nv12(frames, self.W, self.H, self.windows, self.frame_off, self.sizes,
+                                    self.out_dims, self.outs, self.fmt, self.status, self.gather_ws, self.matrix,
+                                    stream)
+        elif frames.dtype == torch.uint8:
             B.mp_gather_resize_strided(frames, self.W, self.H, self.windows, self.frame_off, self.sizes,
                                        self.out_dims, self.outs, self.fmt, self.status, self.gather_ws, stream)
         else:
@@ -114,6 +156,10 @@ class PipelinedRunner:
     """Software pipeline over consecutive batches on three CUDA streams:
     plan(i+1) and remap/NMS(i-1) run while gather/resize(i) streams through HBM.
 
+    With proxy_dims set (NEXT-3), proxy_input(i) runs on a fourth stream and
+    plan(i) waits for it (the proxy consumes that downscale), so the downscale
+    of batch i+1 overlaps the gather of batch i.
+
     Each in-flight batch owns one WindowPipeline (double buffering: `depth`
     sets of plan/gather/NMS buffers), so no stage of batch i+1 overwrites a
     buffer a later stage of batch i still reads.  Ordering is enforced only
@@ -128,6 +174,7 @@ class PipelinedRunner:
         self.s_plan = torch.cuda.Stream(dev)
         self.s_gather = torch.cuda.Stream(dev)
         self.s_merge = torch.cuda.Stream(dev)
+        self.s_proxy = torch.cuda.Stream(dev) if self.pipes[0].proxy_dims else None
         self.done = [None] * self.depth
         self.i = 0
 
@@ -149,14 +196,26 @@ class PipelinedRunner:
                 self.g_merge.append(g2)
         torch.cuda.synchronize()
 
-    def step(self, scores, frames, boxes=None, win_box_off=None, gather_events=None):
+    def step(self, scores, frames, boxes=None, win_box_off=None, gather_events=None, proxy_events=None):
         """Enqueue one batch.  `boxes`/`win_box_off` are the detector's output
-        for this batch (None skips the merge).  gather_events: optional
-        (start, end) CUDA events recorded around the gather on its stream."""
+        for this batch (None skips the merge).  gather_events / proxy_events:
+        optional (start, end) CUDA events recorded around the gather / the
+        proxy-input downscale on their streams."""
         k = self.i % self.depth
         p = self.pipes[k]
         if self.done[k] is not None:
             self.s_plan.wait_event(self.done[k])
+        if self.s_proxy is not None:
+            if self.done[k] is not None:
+                self.s_proxy.wait_event(self.done[k])
+            if proxy_events is not None:
+                proxy_events[0].record(self.s_proxy)
+            p.proxy_input(frames, stream=self.s_proxy)
+            if proxy_events is not None:
+                proxy_events[1].record(self.s_proxy)
+            downscaled = torch.cuda.Event()
+            downscaled.record(self.s_proxy)
+            self.s_plan.wait_event(downscaled)
         if getattr(self, "g_plan", None):
             with torch.cuda.stream(self.s_plan):
                 self.g_plan[k].replay()

@@ -129,3 +129,42 @@ def test_nv12_invalid(G):
     odd = [S.frame_nv12_np(5, 127, pitch)]   # H odd
     with pytest.raises(mp.MPError):
         G.gpu_gather_nv12(odd, W, 127, win[:1], [(64, 64)], [(32, 32)], [1])
+
+
+def test_pipeline_nv12_runner_matches_oracle(G):
+    """WindowPipeline(src='nv12', proxy_dims) through the 4-stream runner:
+    proxy input, windows and crops equal the oracle's (c1, 12 frames)."""
+    import paper_2103_14695_b200 as mp
+    cfg = S.CONFIGS["c1_540p"]
+    F = 12
+    scene = S.make_scene(cfg, 2, F)
+    scores = S.score_grids(cfg, 2, scene)
+    frames_np = _frames(cfg, 2, F)
+    ref_plan = O.plan_windows(cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores)
+    caps = [int(c) for c in ref_plan["class_count"]]
+    dev = torch.device("cuda:0")
+    pipes = []
+    for _ in range(2):
+        p = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
+                              cfg.iou_thr, device=dev, src="nv12", proxy_dims=cfg.proxy_dims)
+        p.reserve(F, len(ref_plan["windows"]), caps=caps, max_boxes=1)
+        pipes.append(p)
+    runner = mp.PipelinedRunner(pipes, device=dev)
+    fr = torch.from_numpy(np.stack(frames_np)).to(dev)
+    sc = torch.from_numpy(scores).to(dev)
+    for _ in range(3):
+        runner.step(sc, fr)
+    runner.wait_all()
+    torch.cuda.synchronize()
+    for p in pipes:
+        p.check_status()
+        assert np.array_equal(p.windows[:len(ref_plan["windows"])].cpu().numpy(), ref_plan["windows"])
+        st, ref = O.gather_resize_nv12(frames_np, cfg.pitch_nv12, cfg.W, cfg.H, ref_plan["windows"], cfg.sizes,
+                                       cfg.out_dims, caps)
+        for q in range(len(caps)):
+            if caps[q]:
+                assert np.abs(p.outs[q].cpu().numpy() - ref[q]).max() <= F32_TOL
+        pw = [[f, 0, 0, cfg.W, cfg.H, 0, f] for f in range(F)]
+        st, pref = O.gather_resize_nv12(frames_np, cfg.pitch_nv12, cfg.W, cfg.H, pw, [(cfg.W, cfg.H)],
+                                        [cfg.proxy_dims], [F])
+        assert np.abs(p.proxy_out.cpu().numpy() - pref[0]).max() <= F32_TOL

@@ -90,6 +90,12 @@ class Config:
         return (3 * self.W + 15) // 16 * 16
 
     @property
+    def proxy_dims(self) -> Tuple[int, int]:
+        """Proxy-model input resolution for NEXT-3's full-frame downscale:
+        416x256, the larger of P:167's two examples (13x8 output grid)."""
+        return (416, 256)
+
+    @property
     def pitch_nv12(self) -> int:
         """NV12 row pitch (bytes, both planes): W rounded up to 16."""
         return (self.W + 15) // 16 * 16
