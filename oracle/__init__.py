@@ -75,6 +75,8 @@ def lib():
         L.mpo_proxy_sweep.argtypes = [i32, i32, i32, i32, i32, p, p, p, i32, p, i32, p, p, p]
         L.mpo_window_set_cost.restype = i32
         L.mpo_window_set_cost.argtypes = [i32, i32, i32, i32, f32, i32, p, p, p, i32, p, p, i32, p]
+        L.mpo_hungarian.restype = i32
+        L.mpo_hungarian.argtypes = [p, i32, i32, f32, p, p, p]
         L.mpo_remap_nms.restype = i32
         L.mpo_remap_nms.argtypes = [p, p, p, p, i32, i32, p, i32, i32, f32, f32, p, p, i32, p]
         _lib = L
@@ -321,3 +323,19 @@ def select_window_sizes(W, H, cell_w, cell_h, scores, k, cost_fn, b_proxy=0.5, s
         S.append(cand[best])
         hist.append(int(tot[best]))
     return S, hist
+
+
+# --------------------------------------------------------------------------- NEXT-4
+def hungarian(scores, floor=0.5):
+    """R24 matching of track prefixes (rows) to detections (columns): maximum
+    total score over pairs with score >= floor.  Returns (status, row_match,
+    col_match, total)."""
+    s = np.ascontiguousarray(np.asarray(scores, dtype=np.float32))
+    if s.ndim != 2:
+        s = s.reshape(0, 0) if s.size == 0 else s.reshape(s.shape[0], -1)
+    m, n = s.shape
+    rm = np.full(max(m, 1), -1, np.int32)
+    cm = np.full(max(n, 1), -1, np.int32)
+    tot = np.zeros(1, np.float64)
+    st = lib().mpo_hungarian(_ptr(s) if s.size else None, m, n, float(floor), _ptr(rm), _ptr(cm), _ptr(tot))
+    return st, rm[:m].copy(), cm[:n].copy(), float(tot[0])

@@ -760,3 +760,99 @@ int32_t mpo_window_set_cost(int32_t W, int32_t H, int32_t cw, int32_t ch, float 
   free(win); free(frame_off); free(sz); free(cs);
   return status;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-4a: Hungarian matching of detections to track prefixes — P:207 "We
+ * apply the Hungarian algorithm to match detections with tracks based on
+ * these scores ... If a detection d_j^(t) does not match with any track, we
+ * initialize a new track prefix".  The paper gives no floor; reading
+ * R24: maximise the total score over matchings
+ * that use only pairs with score >= floor (floor > 0; NaN never allowed).
+ * Written as the textbook square assignment: size S = max(m, n), cost
+ * a[i][j] = -w[i][j] with w = score if allowed else 0 (and 0 on padding), so
+ * a zero-weight pair in the optimum means "unmatched".  Solved with the
+ * classic O(S^3) shortest-augmenting-path Hungarian method with row and
+ * column potentials u, v (rows added one at a time; Dijkstra over columns
+ * with slack minv[j], predecessor way[j]; argmin ties -> smallest column).
+ * All arithmetic fp64.  rows = track prefixes (m), columns = detections (n).
+ * Outputs row_match[i] (column or -1), col_match[j] (row or -1), and *total
+ * = sum of matched scores in row order (fp64). */
+int32_t mpo_hungarian(const float* scores, int32_t m, int32_t n, float floor_, int32_t* row_match,
+                      int32_t* col_match, double* total) {
+  if (m < 0 || n < 0 || !(floor_ > 0.0f)) return MPO_ERR_INVALID;
+  int32_t S = m > n ? m : n;
+  for (int32_t i = 0; i < m; i++) row_match[i] = -1;
+  for (int32_t j = 0; j < n; j++) col_match[j] = -1;
+  *total = 0.0;
+  if (S == 0) return MPO_OK;
+  /* 1-indexed arrays as in the textbook formulation; index 0 is the virtual column */
+  double* a = (double*)malloc(sizeof(double) * (size_t)(S + 1) * (S + 1));
+  double* u = (double*)calloc(S + 1, sizeof(double));
+  double* v = (double*)calloc(S + 1, sizeof(double));
+  double* minv = (double*)malloc(sizeof(double) * (S + 1));
+  int32_t* p = (int32_t*)calloc(S + 1, sizeof(int32_t));
+  int32_t* way = (int32_t*)calloc(S + 1, sizeof(int32_t));
+  char* used = (char*)malloc(S + 1);
+  const double INF = 1e300;
+  for (int32_t i = 1; i <= S; i++)
+    for (int32_t j = 1; j <= S; j++) {
+      double w = 0.0;
+      if (i <= m && j <= n) {
+        float s = scores[(int64_t)(i - 1) * n + (j - 1)];
+        if (s >= floor_) w = (double)s; /* NaN compares false */
+      }
+      a[(int64_t)i * (S + 1) + j] = -w;
+    }
+  for (int32_t i = 1; i <= S; i++) {
+    p[0] = i;
+    int32_t j0 = 0;
+    for (int32_t j = 0; j <= S; j++) {
+      minv[j] = INF;
+      used[j] = 0;
+    }
+    do {
+      used[j0] = 1;
+      int32_t i0 = p[j0], j1 = 0;
+      double delta = INF;
+      for (int32_t j = 1; j <= S; j++) {
+        if (used[j]) continue;
+        double cur = a[(int64_t)i0 * (S + 1) + j] - u[i0] - v[j];
+        if (cur < minv[j]) {
+          minv[j] = cur;
+          way[j] = j0;
+        }
+        if (minv[j] < delta) {
+          delta = minv[j];
+          j1 = j;
+        }
+      }
+      for (int32_t j = 0; j <= S; j++) {
+        if (used[j]) {
+          u[p[j]] += delta;
+          v[j] -= delta;
+        } else {
+          minv[j] -= delta;
+        }
+      }
+      j0 = j1;
+    } while (p[j0] != 0);
+    do {
+      int32_t j1 = way[j0];
+      p[j0] = p[j1];
+      j0 = j1;
+    } while (j0);
+  }
+  /* p[j] = row assigned to column j; keep the pairs with positive weight */
+  int32_t* rm = (int32_t*)malloc(sizeof(int32_t) * (S + 1));
+  for (int32_t j = 1; j <= S; j++) rm[p[j]] = j;
+  for (int32_t i = 1; i <= m; i++) {
+    int32_t j = rm[i];
+    if (j <= n && -a[(int64_t)i * (S + 1) + j] > 0.0) {
+      row_match[i - 1] = j - 1;
+      col_match[j - 1] = i - 1;
+      *total += -a[(int64_t)i * (S + 1) + j];
+    }
+  }
+  free(rm); free(a); free(u); free(v); free(minv); free(p); free(way); free(used);
+  return MPO_OK;
+}
