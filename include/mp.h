@@ -303,12 +303,52 @@ mp_status mp_window_set_cost(const mp_plan_params* p, const float* d_scores, int
                              const int64_t* cand_cost, int32_t n_cand, int64_t* d_tot, void* d_ws,
                              size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * NEXT-4a: Hungarian matching of detections to track prefixes (PAPER.md:207
+ * "We apply the Hungarian algorithm to match detections with tracks based on
+ * these scores, and add each detection to the track that it matches with. If
+ * a detection d_j^(t) does not match with any track, we initialize a new
+ * track prefix").  The scores p_ij come from the tracker model
+ * (outside this library).  Batched over independent problems (clips).
+ *
+ * Reading R24: per problem, maximise the total score over
+ * matchings that use only pairs with score >= floor_ (NaN never matched), via
+ * the square assignment of size S = max(m, n) on cost -w (w = score if
+ * allowed else 0, zero padding) with the textbook shortest-augmenting-path
+ * Hungarian method in fp64 (rows in order, arg-min ties -> smallest column).
+ *
+ *  d_scores    device float; problem b's [m][n] row-major matrix starts at
+ *              d_scores + problems[b].score_off (rows = track prefixes,
+ *              columns = detections).
+ *  d_problems  device mp_assign_problem [B].
+ *  floor_      > 0, else MP_ERR_INVALID.
+ *  max_dim     host bound on max(m, n) over the batch, <= 1024 (sizes shared
+ *              memory); a problem with max(m, n) > max_dim gets *d_status =
+ *              MP_ERR_CAPACITY and all -1 outputs.
+ *  d_row_match device int32: row i of problem b -> matched column or -1, at
+ *              d_row_match[row_off + i]; d_col_match likewise per column.
+ *  d_total     device double [B]: sum of matched scores (fp64, row order).
+ *  Problems with m, n < 0 or negative offsets: *d_status = MP_ERR_INVALID.
+ *  Launches: memset + warp-per-problem kernel (S <= 64) + CTA-per-problem
+ *  kernel for the larger ones (queued on the device).  Graph-capturable.
+ */
+typedef struct {
+  int64_t score_off;
+  int32_t m, n, row_off, col_off;
+} mp_assign_problem;
+
+size_t mp_hungarian_workspace_size(int32_t B);
+
+mp_status mp_hungarian(const float* d_scores, const mp_assign_problem* d_problems, int32_t B, float floor_,
+                       int32_t max_dim, int32_t* d_row_match, int32_t* d_col_match, double* d_total,
+                       int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
+
 /* Human-readable name of a status code (static string, never NULL). */
 const char* mp_status_string(mp_status st);
 
 /* Number of device kernels the library launches per call (diagnostic, used
  * by bench.py to count launches): which = 0 plan, 1 gather, 2 remap_nms,
- * 3 proxy_sweep, 4 window_set_cost. */
+ * 3 proxy_sweep, 4 window_set_cost, 5 hungarian. */
 int32_t mp_launches_per_call(int32_t which);
 
 #ifdef __cplusplus

@@ -74,6 +74,10 @@ def _load():
     L.mp_window_set_cost_workspace_size.argtypes = [i32]
     L.mp_window_set_cost.restype = C.c_int
     L.mp_window_set_cost.argtypes = [C.POINTER(mp_plan_params), vp, i32, vp, vp, i32, vp, vp, sz, vp]
+    L.mp_hungarian_workspace_size.restype = sz
+    L.mp_hungarian_workspace_size.argtypes = [i32]
+    L.mp_hungarian.restype = C.c_int
+    L.mp_hungarian.argtypes = [vp, vp, i32, C.c_float, i32, vp, vp, vp, vp, vp, sz, vp]
     L.mp_remap_nms_workspace_size.restype = sz
     L.mp_remap_nms_workspace_size.argtypes = [i32, i32]
     L.mp_remap_nms.restype = C.c_int
@@ -325,3 +329,49 @@ def mp_window_set_cost(params: PlanParams, scores, F, cand, cand_cost, tot, ws, 
                                  _p(ws), ws.numel(), _stream(stream))
     if st != MP_OK:
         raise MPError(st, "mp_window_set_cost")
+
+
+# --------------------------------------------------------------------------- NEXT-4a
+import numpy as _np  # noqa: E402
+
+ASSIGN_PROBLEM_DTYPE = _np.dtype([("score_off", "<i8"), ("m", "<i4"), ("n", "<i4"), ("row_off", "<i4"),
+                                  ("col_off", "<i4")])   # = mp_assign_problem, 24 bytes
+
+
+def assign_problems(ms, ns):
+    """Host-side packing of a batch of [m_b][n_b] score matrices laid out back
+    to back: returns (mp_assign_problem records as a numpy structured array,
+    total score count, total rows, total columns)."""
+    ms = _np.asarray(ms, _np.int64)
+    ns = _np.asarray(ns, _np.int64)
+    rec = _np.zeros(len(ms), ASSIGN_PROBLEM_DTYPE)
+    so = _np.concatenate([[0], _np.cumsum(ms * ns)])
+    ro = _np.concatenate([[0], _np.cumsum(ms)])
+    co = _np.concatenate([[0], _np.cumsum(ns)])
+    rec["score_off"], rec["m"], rec["n"] = so[:-1], ms, ns
+    rec["row_off"], rec["col_off"] = ro[:-1], co[:-1]
+    return rec, int(so[-1]), int(ro[-1]), int(co[-1])
+
+
+def mp_hungarian_workspace_size(B: int) -> int:
+    return int(_lib.mp_hungarian_workspace_size(int(B)))
+
+
+def mp_hungarian(scores, problems, B, floor_, max_dim, row_match, col_match, total, status, ws,
+                 stream=None) -> None:
+    """NEXT-4a batched matching (R24).  scores float32 CUDA [total]; problems
+    uint8 CUDA [B*24] (ASSIGN_PROBLEM_DTYPE records); row_match / col_match
+    int32 CUDA; total float64 CUDA [B]."""
+    _dev(scores, torch.float32, "scores")
+    _dev(problems, torch.uint8, "problems")
+    _dev(row_match, torch.int32, "row_match")
+    _dev(col_match, torch.int32, "col_match")
+    _dev(total, torch.float64, "total")
+    _dev(status, torch.int32, "status")
+    _dev(ws, torch.uint8, "ws")
+    if problems.numel() < 24 * int(B):
+        raise ValueError("problems must hold B mp_assign_problem records")
+    st = _lib.mp_hungarian(_p(scores), _p(problems), int(B), float(floor_), int(max_dim), _p(row_match),
+                           _p(col_match), _p(total), _p(status), _p(ws), ws.numel(), _stream(stream))
+    if st != MP_OK:
+        raise MPError(st, "mp_hungarian")

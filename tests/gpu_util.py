@@ -111,3 +111,27 @@ def gpu_remap_nms(boxes, win_box_off, windows, frame_off, out_dims, W, H, score_
     n = min(int(ofo[F].item()), max_out)
     return dict(status=int(st.item()), boxes=out[:n].cpu().numpy(), src=src[:n].cpu().numpy(),
                 frame_off=ofo.cpu().numpy())
+
+
+def gpu_hungarian(mats, floor=0.5, max_dim=None):
+    """Run mp_hungarian on a list of float32 [m][n] matrices; returns
+    (status, [row_match], [col_match], totals)."""
+    ms = [int(a.shape[0]) for a in mats]
+    ns = [int(a.shape[1]) for a in mats]
+    rec, ns_tot, nr, nc = B.assign_problems(ms, ns)
+    flat = np.concatenate([np.ascontiguousarray(a, np.float32).ravel() for a in mats]) if ns_tot else \
+        np.zeros(1, np.float32)
+    sc = torch.from_numpy(flat if len(flat) else np.zeros(1, np.float32)).to(DEV)
+    pr = torch.from_numpy(rec.view(np.uint8).copy() if len(rec) else np.zeros(24, np.uint8)).to(DEV)
+    rm = torch.full((max(nr, 1),), -9, dtype=torch.int32, device=DEV)
+    cm = torch.full((max(nc, 1),), -9, dtype=torch.int32, device=DEV)
+    tot = torch.full((max(len(mats), 1),), -1.0, dtype=torch.float64, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ws = torch.empty(max(B.mp_hungarian_workspace_size(len(mats)), 1), dtype=torch.uint8, device=DEV)
+    md = max([max(m, n) for m, n in zip(ms, ns)] + [0]) if max_dim is None else max_dim
+    B.mp_hungarian(sc, pr, len(mats), floor, md, rm, cm, tot, st, ws)
+    torch.cuda.synchronize()
+    rmh, cmh = rm.cpu().numpy(), cm.cpu().numpy()
+    rows = [rmh[rec["row_off"][b]:rec["row_off"][b] + ms[b]] for b in range(len(mats))]
+    cols = [cmh[rec["col_off"][b]:rec["col_off"][b] + ns[b]] for b in range(len(mats))]
+    return int(st.item()), rows, cols, tot.cpu().numpy()[:len(mats)]

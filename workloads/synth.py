@@ -347,3 +347,33 @@ def standin_boxes(cfg: Config, clip: int, scene: Scene, windows: np.ndarray,
         off.append(off[-1] + len(arr))
     boxes = np.concatenate(out) if out else np.zeros(0, BOX_DTYPE)
     return boxes, np.asarray(off, np.int32)
+
+
+# --------------------------------------------------------------------------- NEXT-4a
+def assign_batch(seed: int, B: int, m_range=(3, 40), n_range=(3, 40), sigma_px: float = 24.0,
+                 miss: float = 0.1, spawn: float = 0.1):
+    """A batch of B synthetic tracker score matrices p_ij for the
+    Hungarian stage: per problem, m track prefixes at uniform positions in a
+    1920x1080 frame; each continues into a detection with probability 1-miss
+    (jittered by N(0, sigma_px/2)), plus Poisson(spawn*m) new detections; the
+    stand-in scorer gives p_ij = exp(-d_ij^2 / (2 sigma_px^2)) * U[0.85, 1]
+    (float32).  Sizes m ~ U[m_range], n follows from the model and is clipped
+    to n_range.  Returns (list of float32 [m][n] matrices)."""
+    rng = np.random.default_rng(splitmix64(seed ^ 0xA551))
+    out = []
+    for _ in range(B):
+        m = int(rng.integers(m_range[0], m_range[1] + 1))
+        tp = rng.uniform((0, 0), (1920, 1080), (m, 2))
+        keep = rng.random(m) >= miss
+        det = tp[keep] + rng.normal(0, sigma_px / 2, (int(keep.sum()), 2))
+        new = rng.uniform((0, 0), (1920, 1080), (int(rng.poisson(spawn * m)), 2))
+        det = np.concatenate([det, new])
+        rng.shuffle(det)
+        n = int(np.clip(len(det), n_range[0], n_range[1]))
+        if len(det) < n:
+            det = np.concatenate([det, rng.uniform((0, 0), (1920, 1080), (n - len(det), 2))])
+        det = det[:n]
+        d2 = ((tp[:, None, :] - det[None, :, :]) ** 2).sum(-1)
+        p = np.exp(-d2 / (2 * sigma_px ** 2)) * rng.uniform(0.85, 1.0, (m, n))
+        out.append(p.astype(np.float32))
+    return out
