@@ -559,6 +559,74 @@ def run_wsel(args):
     return 0
 
 
+def run_assign(args):
+    """NEXT-4a measurement: one tracker step for a batch of 8,192
+    clips — each a synthetic [m][n] score matrix, m ~ U[3,40] track prefixes
+    (traffic-camera scale), plus 64 dense 100-150-object problems (CTA tier) —
+    matched with mp_hungarian.  Metric: matching problems solved per second.
+    cpu_baseline: the oracle (plain C, fp64) over a bounded sample, threaded."""
+    import torch
+
+    import paper_2103_14695_b200 as mp
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    mats = S.assign_batch(11, 8192, (3, 40), (3, 40)) + S.assign_batch(12, 64, (100, 150), (100, 150))
+    Bn = len(mats)
+    rec, n_sc, nr, nc = mp.assign_problems([a.shape[0] for a in mats], [a.shape[1] for a in mats])
+    sc = torch.from_numpy(np.concatenate([a.ravel() for a in mats])).to(dev)
+    pr = torch.from_numpy(rec.view(np.uint8).copy()).to(dev)
+    rm = torch.empty(nr, dtype=torch.int32, device=dev)
+    cm = torch.empty(nc, dtype=torch.int32, device=dev)
+    tot = torch.empty(Bn, dtype=torch.float64, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = torch.empty(mp.mp_hungarian_workspace_size(Bn), dtype=torch.uint8, device=dev)
+    md = max(max(a.shape) for a in mats)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(3, args.warmup)):
+        mp.mp_hungarian(sc, pr, Bn, 0.5, md, rm, cm, tot, st, ws)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(dev.index or 0)
+    sampler.start()
+    time.sleep(0.3)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        mp.mp_hungarian(sc, pr, Bn, 0.5, md, rm, cm, tot, st, ws)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = t0.elapsed_time(t1)
+    assert int(st.item()) == 0
+    matched = int((rm >= 0).sum().item())
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle as O
+        from concurrent.futures import ThreadPoolExecutor
+        O.build()
+        threads = os.cpu_count() or 1
+        sample = mats[:2048] + mats[-16:]
+        t = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            list(ex.map(lambda a: O.hungarian(a, 0.5), sample))
+        dt = time.perf_counter() - t
+        cpu = {"value": len(sample) / dt, "unit": "problems/s", "cores": threads, "kind": "oracle",
+               "sample": f"{len(sample)} of the {Bn} problems (2048 traffic-size + 16 dense), "
+                         f"{threads} threads, {host_cpu_desc()}"}
+    print(json.dumps({
+        "metric": "tracker matching problems/sec (Hungarian, NEXT-4a)",
+        "value": Bn * args.steps / (ms * 1e-3), "unit": "problems/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "8192 clips x m,n~U[3,40] + 64 dense 100-150", "problems": Bn,
+                   "score_entries": n_sc, "floor": 0.5},
+        "roofline": {"bound": "latency", "note": "serial Dijkstra steps per problem; one warp (S<=64) or CTA "
+                                                  "per problem; reported as problems/s, not a bandwidth"},
+        "result": {"matched_pairs": matched, "rows": nr, "cols": nc},
+        "cpu_baseline": cpu, "clocks": clocks,
+        "gpu_launches": args.steps * mp.launches_per_call(5)}), flush=True)
+    return 0
+
+
 def run_e2e(cfg, clip, scene, scores_np, boxes, wbo, fmt, dev, args):
     """Same metric through WindowPipeline with HOST inputs: each step copies the
     clip's frames (from a pinned host pool), scores and detector boxes H2D and
@@ -640,9 +708,9 @@ def main():
     ap.add_argument("--src", default="rgb24", choices=["rgb24", "nv12"],
                     help="frame format: rgb24 rows (default) or NV12 decoder output with the proxy-input "
                          "downscale in the step (NEXT-3)")
-    ap.add_argument("--mode", default="path", choices=["path", "sweep", "wsel"],
+    ap.add_argument("--mode", default="path", choices=["path", "sweep", "wsel", "assign"],
                     help="path: the hot path a1-a7 (default); sweep: NEXT-1 proxy-module sweep; "
-                         "wsel: NEXT-2 window-size selection step")
+                         "wsel: NEXT-2 window-size selection step; assign: NEXT-4a batched Hungarian")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -651,6 +719,8 @@ def main():
         return run_sweep(args)
     if args.mode == "wsel":
         return run_wsel(args)
+    if args.mode == "assign":
+        return run_assign(args)
     return run_b200(args)
 
 

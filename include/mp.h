@@ -329,8 +329,10 @@ mp_status mp_window_set_cost(const mp_plan_params* p, const float* d_scores, int
  *              d_row_match[row_off + i]; d_col_match likewise per column.
  *  d_total     device double [B]: sum of matched scores (fp64, row order).
  *  Problems with m, n < 0 or negative offsets: *d_status = MP_ERR_INVALID.
- *  Launches: memset + warp-per-problem kernel (S <= 64) + CTA-per-problem
- *  kernel for the larger ones (queued on the device).  Graph-capturable.
+ *  Launches: memset + warp-per-problem kernel (S <= 64), then for the larger
+ *  ones (queued on the device) a warp-per-problem kernel with the scores in
+ *  shared memory (S <= 160, if max_dim > 64) and a CTA-per-problem kernel
+ *  (S <= 1024, if max_dim > 160).  Graph-capturable.
  */
 typedef struct {
   int64_t score_off;

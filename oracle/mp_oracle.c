@@ -773,7 +773,9 @@ int32_t mpo_window_set_cost(int32_t W, int32_t H, int32_t cw, int32_t ch, float 
  * a zero-weight pair in the optimum means "unmatched".  Solved with the
  * classic O(S^3) shortest-augmenting-path Hungarian method with row and
  * column potentials u, v (rows added one at a time; Dijkstra over columns
- * with slack minv[j], predecessor way[j]; argmin ties -> smallest column).
+ * with slack minv[j], predecessor way[j]; arg-min ties -> a free column
+ * first (it ends the search: every tie-break among minimum-slack columns
+ * gives a shortest augmenting path), then the smallest column index).
  * All arithmetic fp64.  rows = track prefixes (m), columns = detections (n).
  * Outputs row_match[i] (column or -1), col_match[j] (row or -1), and *total
  * = sum of matched scores in row order (fp64). */
@@ -821,7 +823,7 @@ int32_t mpo_hungarian(const float* scores, int32_t m, int32_t n, float floor_, i
           minv[j] = cur;
           way[j] = j0;
         }
-        if (minv[j] < delta) {
+        if (minv[j] < delta || (minv[j] == delta && p[j] == 0 && j1 != 0 && p[j1] != 0)) {
           delta = minv[j];
           j1 = j;
         }

@@ -17,7 +17,8 @@ extern "C" const char* mp_status_string(mp_status st) {
 //   gather: gather_prep + gather_kernel
 //   remap_nms: memset (not a kernel) + tiny + small + large + scan + scatter
 //   proxy_sweep: memset (not a kernel) + proxy_sweep_kernel
-//   hungarian: memset (not a kernel) + hung_warp_kernel + hung_block_kernel (when max_dim > 64)
+//   hungarian: memset (not a kernel) + hung_warp_kernel + hung_mid_kernel (max_dim > 64)
+//              + hung_block_kernel (max_dim > 160)
 extern "C" int32_t mp_launches_per_call(int32_t which) {
   switch (which) {
     case 0: return 4;
@@ -25,7 +26,7 @@ extern "C" int32_t mp_launches_per_call(int32_t which) {
     case 2: return 5;
     case 3: return 1;
     case 4: return 1;
-    case 5: return 2;
+    case 5: return 3;
   }
   return 0;
 }

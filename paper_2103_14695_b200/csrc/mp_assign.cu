@@ -8,7 +8,8 @@
 // with the shortest-augmenting-path Hungarian method: rows are added one at a
 // time; for each, a Dijkstra-like scan over the columns keeps the slack
 // minv[j] = min over visited rows of a[i][j] - u[i] - v[j] and its predecessor
-// way[j], moves to the arg-min column (ties -> smallest j), shifts the
+// way[j], moves to the arg-min column (ties -> a free column first, then the
+// smallest j: a free minimum ends the search at once), shifts the
 // potentials u, v by that minimum, and stops at a free column; the path is
 // then flipped.  All arithmetic is fp64 in the same order as the oracle, so
 // the matchings are identical (not merely equally good).
@@ -18,13 +19,17 @@
 // registers; u[], p[] (column -> row) and way[] live in shared memory.  Each
 // Dijkstra step = one coalesced read of row i0 of the scores (the columns of
 // a row are consecutive), a group arg-min of (delta, j), and the potential
-// update.  Tier 1: G = 32 (one warp per problem) for S <= 64; tier 2: G = 256
-// (one CTA per problem) for S <= 1024, queued on the device by tier 1.
+// update.  Tier 1: G = 32 (one warp per problem) for S <= 64; tier 2: one warp
+// per problem with 5 columns per lane and the scores staged in shared memory
+// for S <= 160 (warp-synchronous steps at shared-memory latency); tier 3:
+// G = 256 (one CTA per problem) for S <= 1024.  Tiers 2 and 3 are queued on
+// the device by tier 1.
 #include "mp_internal.cuh"
 
 namespace mpk {
 
 constexpr int kHungWarpMax = 64;     // tier 1: S <= 64 (2 columns per lane)
+constexpr int kHungMidMax = 160;     // tier 2: S <= 160 (5 columns per lane, scores in smem: <= 100 KB)
 constexpr int kHungBlockMax = 1024;  // tier 2: S <= 1024 (4 columns per thread)
 constexpr int kHungBlock = 256;
 
@@ -38,14 +43,16 @@ struct HungArgs {
   int* col_match;
   double* total;
   int* status;
-  int* q_cnt;    // tier-2 queue
-  int* q_list;
+  int* q_cnt;    // [0]: tier-2 queue length, [1]: tier-3 queue length
+  int* q_list;   // tier 2 at [0, B), tier 3 at [B, 2B)
 };
 
-// weight of pair (i, j), 1-indexed, of a problem; 0 outside [1,m] x [1,n] or below the floor
+// weight of pair (i, j), 1-indexed, of a problem; 0 outside [1,m] x [1,n] or below the floor.
+// SMEM: the matrix was staged in shared memory (plain loads) instead of global (__ldg).
+template <bool SMEM = false>
 __device__ __forceinline__ double hung_w(const float* sc, int m, int n, float floor_, int i, int j) {
   if (i > m || j > n) return 0.0;
-  const float s = __ldg(sc + (size_t)(i - 1) * n + (j - 1));
+  const float s = SMEM ? sc[(size_t)(i - 1) * n + (j - 1)] : __ldg(sc + (size_t)(i - 1) * n + (j - 1));
   return (s >= floor_) ? (double)s : 0.0;   // NaN compares false
 }
 
@@ -56,6 +63,7 @@ template <>
 struct Group<32> {   // one warp
   __device__ static void sync() { __syncwarp(); }
   // lexicographic arg-min of (d, j) over the group; every lane gets the result
+  // (callers pass j = busy * 2^30 + column, so free columns win ties)
   __device__ static void argmin(double& d, int& j, double*, int*) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -96,12 +104,12 @@ struct Group<kHungBlock> {   // one CTA
 
 // Solve one problem with a group of G threads (tid = rank in the group).
 // Shared: u[S+1] (double), p[S+1], way[S+1] (int), red_d/red_j scratch.
-template <int G, int KMAX>
+template <int G, int KMAX, bool SMEM = false>
 __device__ void hung_solve(const HungArgs& A, const mp_assign_problem& pb, int tid, double* u, int* p, int* way,
-                           double* red_d, int* red_j) {
+                           double* red_d, int* red_j, const float* sc_smem = nullptr) {
   using Grp = Group<G>;
   const int m = pb.m, n = pb.n, S = max(m, n);
-  const float* sc = A.scores + pb.score_off;
+  const float* sc = SMEM ? sc_smem : A.scores + pb.score_off;
   const double INF = 1e300;
   for (int j = tid; j <= S; j += G) {
     u[j] = 0.0;
@@ -130,24 +138,26 @@ __device__ void hung_solve(const HungArgs& A, const mp_assign_problem& pb, int t
       const int i0 = p[j0];
       const double ui0 = u[i0];
       double delta = INF;
-      int j1 = 0x7fffffff;
+      int key = 0x7fffffff;   // busy(j) << 30 | j of the best column: free columns first, then smallest j
 #pragma unroll
       for (int k = 0; k < KMAX; k++) {
         const int j = 1 + tid + G * k;
         if (j <= S && !used[k]) {
-          const double a = -hung_w(sc, m, n, A.floor_, i0, j);
+          const double a = -hung_w<SMEM>(sc, m, n, A.floor_, i0, j);
           const double cur = __dsub_rn(__dsub_rn(a, ui0), v[k]);
           if (cur < minv[k]) {
             minv[k] = cur;
             way[j] = j0;
           }
-          if (minv[k] < delta) {   // k ascending = j ascending: strict < keeps the smallest j
+          const int kj = (p[j] != 0 ? (1 << 30) : 0) | j;
+          if (minv[k] < delta || (minv[k] == delta && kj < key)) {
             delta = minv[k];
-            j1 = j;
+            key = kj;
           }
         }
       }
-      Grp::argmin(delta, j1, red_d, red_j);
+      Grp::argmin(delta, key, red_d, red_j);
+      const int j1 = key & ((1 << 30) - 1);
       Grp::sync();   // every read of u[i0] precedes the updates below
       // potentials: used columns (their rows) shift by +delta / -delta, the others' slack by -delta
 #pragma unroll
@@ -243,12 +253,39 @@ __global__ void __launch_bounds__(32 * kHungWarpsPerCta) hung_warp_kernel(const 
       hung_fail(A, pb, b, lane, 32, MP_OK);
       continue;
     }
-    if (S > kHungWarpMax) {   // tier 2
-      if (lane == 0) A.q_list[atomicAdd(A.q_cnt, 1)] = b;
+    if (S > kHungWarpMax) {   // tiers 2 / 3
+      if (lane == 0) {
+        if (S <= kHungMidMax) A.q_list[atomicAdd(&A.q_cnt[0], 1)] = b;
+        else A.q_list[A.B + atomicAdd(&A.q_cnt[1], 1)] = b;
+      }
       continue;
     }
     hung_solve<32, 2>(A, pb, lane, s_u[wid], s_p[wid], s_way[wid], nullptr, nullptr);
     hung_emit<32>(A, pb, b, lane, s_u[wid], s_p[wid]);
+  }
+}
+
+// Tier 2: one warp per problem (one warp per CTA), the problem's [m][n]
+// scores staged once in shared memory so every Dijkstra step reads its row at
+// shared-memory latency instead of L2's; warp-synchronous steps (no CTA
+// barriers).  S <= kHungMidMax (the m*n floats must fit the dynamic smem).
+__global__ void __launch_bounds__(32) hung_mid_kernel(const HungArgs A) {
+  extern __shared__ __align__(16) unsigned char hsm2[];
+  double* u = reinterpret_cast<double*>(hsm2);
+  int* p = reinterpret_cast<int*>(u + (kHungMidMax + 1));
+  int* way = p + (kHungMidMax + 1);
+  float* sc = reinterpret_cast<float*>(way + (kHungMidMax + 1));
+  const int lane = threadIdx.x;
+  const int nq = A.q_cnt[0];
+  for (int qi = blockIdx.x; qi < nq; qi += gridDim.x) {
+    const int b = A.q_list[qi];
+    const mp_assign_problem pb = A.probs[b];
+    const float* g = A.scores + pb.score_off;
+    const int mn = pb.m * pb.n;
+    for (int e = lane; e < mn; e += 32) sc[e] = __ldg(g + e);
+    __syncwarp();
+    hung_solve<32, kHungMidMax / 32, true>(A, pb, lane, u, p, way, nullptr, nullptr, sc);
+    hung_emit<32>(A, pb, b, lane, u, p);
   }
 }
 
@@ -259,9 +296,9 @@ __global__ void __launch_bounds__(kHungBlock) hung_block_kernel(const HungArgs A
   int* way = p + (A.max_dim + 1);
   __shared__ double red_d[kHungBlock / 32];
   __shared__ int red_j[kHungBlock / 32];
-  const int nq = *A.q_cnt;
+  const int nq = A.q_cnt[1];
   for (int qi = blockIdx.x; qi < nq; qi += gridDim.x) {
-    const int b = A.q_list[qi];
+    const int b = A.q_list[A.B + qi];
     const mp_assign_problem pb = A.probs[b];
     hung_solve<kHungBlock, kHungBlockMax / kHungBlock>(A, pb, threadIdx.x, u, p, way, red_d, red_j);
     hung_emit<kHungBlock>(A, pb, b, threadIdx.x, u, p);
@@ -274,7 +311,7 @@ using namespace mpk;
 
 extern "C" size_t mp_hungarian_workspace_size(int32_t B) {
   if (B < 0) return 0;
-  return 256 + (((size_t)B * sizeof(int) + 255) & ~size_t(255));
+  return 256 + (((size_t)2 * B * sizeof(int) + 255) & ~size_t(255));
 }
 
 extern "C" mp_status mp_hungarian(const float* d_scores, const mp_assign_problem* d_problems, int32_t B,
@@ -297,7 +334,7 @@ extern "C" mp_status mp_hungarian(const float* d_scores, const mp_assign_problem
   A.status = d_status;
   A.q_cnt = (int*)d_ws;
   A.q_list = (int*)((unsigned char*)d_ws + 256);
-  MP_CUDA_TRY(cudaMemsetAsync(A.q_cnt, 0, sizeof(int), s));
+  MP_CUDA_TRY(cudaMemsetAsync(A.q_cnt, 0, 2 * sizeof(int), s));
   int dev = 0, sms = 0;
   MP_CUDA_TRY(cudaGetDevice(&dev));
   MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -305,6 +342,13 @@ extern "C" mp_status mp_hungarian(const float* d_scores, const mp_assign_problem
   hung_warp_kernel<<<grid1, 32 * kHungWarpsPerCta, 0, s>>>(A);
   MP_CUDA_TRY(cudaGetLastError());
   if (max_dim > kHungWarpMax) {
+    const int md = min(max_dim, kHungMidMax);
+    const size_t smem2 = (size_t)(kHungMidMax + 1) * (sizeof(double) + 2 * sizeof(int)) + (size_t)md * md * sizeof(float);
+    MP_CUDA_TRY(cudaFuncSetAttribute(hung_mid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    hung_mid_kernel<<<sms * 2, 32, smem2, s>>>(A);
+    MP_CUDA_TRY(cudaGetLastError());
+  }
+  if (max_dim > kHungMidMax) {
     const size_t smem = (size_t)(max_dim + 1) * (sizeof(double) + 2 * sizeof(int));
     MP_CUDA_TRY(cudaFuncSetAttribute(hung_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     hung_block_kernel<<<sms * 4, kHungBlock, smem, s>>>(A);
