@@ -77,6 +77,17 @@ def lib():
         L.mpo_window_set_cost.argtypes = [i32, i32, i32, i32, f32, i32, p, p, p, i32, p, p, i32, p]
         L.mpo_hungarian.restype = i32
         L.mpo_hungarian.argtypes = [p, i32, i32, f32, p, p, p]
+        d = C.c_double
+        L.mpo_track_resample.restype = None
+        L.mpo_track_resample.argtypes = [p, i32, i32, p]
+        L.mpo_track_distance.restype = d
+        L.mpo_track_distance.argtypes = [p, p, i32]
+        L.mpo_dbscan.restype = i32
+        L.mpo_dbscan.argtypes = [p, i32, i32, d, i32, p, p, p]
+        L.mpo_cluster_centers.restype = None
+        L.mpo_cluster_centers.argtypes = [p, i32, i32, p, i32, p, p]
+        L.mpo_refine_track.restype = i32
+        L.mpo_refine_track.argtypes = [p, i32, p, p, p, p, i32, d, i32, p]
         L.mpo_remap_nms.restype = i32
         L.mpo_remap_nms.argtypes = [p, p, p, p, i32, i32, p, i32, i32, f32, f32, p, p, i32, p]
         _lib = L
@@ -339,3 +350,64 @@ def hungarian(scores, floor=0.5):
     tot = np.zeros(1, np.float64)
     st = lib().mpo_hungarian(_ptr(s) if s.size else None, m, n, float(floor), _ptr(rm), _ptr(cm), _ptr(tot))
     return st, rm[:m].copy(), cm[:n].copy(), float(tot[0])
+
+
+# --------------------------------------------------------------------------- NEXT-4b
+TRACK_N = 20   # P:244 "In our implementation, N = 20"
+
+
+def box_centers(boxes):
+    """R25: a track's path = its detections' box centres ((x1+x2)/2, (y1+y2)/2)
+    in fp64.  boxes: [n][4] (x1, y1, x2, y2)."""
+    b = np.asarray(boxes, np.float64).reshape(-1, 4)
+    return np.ascontiguousarray(np.stack([(b[:, 0] + b[:, 2]) / 2, (b[:, 1] + b[:, 3]) / 2], 1))
+
+
+def track_resample(points, N=TRACK_N):
+    p = np.ascontiguousarray(np.asarray(points, np.float64).reshape(-1, 2))
+    out = np.zeros((N, 2), np.float64)
+    lib().mpo_track_resample(_ptr(p), len(p), N, _ptr(out))
+    return out
+
+
+def track_distance(a, b):
+    a = np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1, 2))
+    b = np.ascontiguousarray(np.asarray(b, np.float64).reshape(-1, 2))
+    assert a.shape == b.shape
+    return float(lib().mpo_track_distance(_ptr(a), _ptr(b), len(a)))
+
+
+def dbscan(paths, eps, min_pts):
+    """R26 DBSCAN over resampled paths [T][N][2].  Returns (labels, is_core,
+    n_dbscan_clusters, n_clusters incl. noise singletons)."""
+    P = np.ascontiguousarray(np.asarray(paths, np.float64))
+    T, N = P.shape[0], P.shape[1]
+    lab = np.zeros(max(T, 1), np.int32)
+    core = np.zeros(max(T, 1), np.uint8)
+    nd = np.zeros(1, np.int32)
+    Cn = lib().mpo_dbscan(_ptr(P), T, N, float(eps), int(min_pts), _ptr(lab), _ptr(core), _ptr(nd))
+    return lab[:T].copy(), core[:T].astype(bool), int(nd[0]), int(Cn)
+
+
+def cluster_centers(paths, labels, C):
+    P = np.ascontiguousarray(np.asarray(paths, np.float64))
+    T, N = P.shape[0], P.shape[1]
+    lab = np.ascontiguousarray(np.asarray(labels, np.int32))
+    ctr = np.zeros((max(C, 1), N, 2), np.float64)
+    cnt = np.zeros(max(C, 1), np.int32)
+    lib().mpo_cluster_centers(_ptr(P), T, N, _ptr(lab), C, _ptr(ctr), _ptr(cnt))
+    return ctr[:C].copy(), cnt[:C].copy()
+
+
+def refine_track(path, first, last, centers, counts, cell=32.0, k=10):
+    """R27 refinement of one track: returns (clusters taken, (sx, sy, ex, ey))."""
+    path = np.ascontiguousarray(np.asarray(path, np.float64))
+    f = np.ascontiguousarray(np.asarray(first, np.float64))
+    l = np.ascontiguousarray(np.asarray(last, np.float64))
+    ctr = np.ascontiguousarray(np.asarray(centers, np.float64))
+    cnt = np.ascontiguousarray(np.asarray(counts, np.int32))
+    out = np.zeros(4, np.float64)
+    C = len(cnt)
+    n = lib().mpo_refine_track(_ptr(path), path.shape[0], _ptr(f), _ptr(l), _ptr(ctr) if C else None,
+                               _ptr(cnt) if C else None, C, float(cell), int(k), _ptr(out))
+    return int(n), out

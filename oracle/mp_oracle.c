@@ -858,3 +858,238 @@ int32_t mpo_hungarian(const float* scores, int32_t m, int32_t n, float floor_, i
   free(rm); free(a); free(u); free(v); free(minv); free(p); free(way); free(used);
   return MPO_OK;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-4b: track refinement (§3.4 "Refinement").
+ * Reading R25: a track's path is the sequence of its
+ * detections' box centres ((x1+x2)/2, (y1+y2)/2) in frame order (fp64);
+ * "N points evenly spaced along each track" = points at arc lengths
+ * L*i/(N-1), i = 0..N-1, along the polyline (L = total length), linearly
+ * interpolated inside the segment reached; point 0 and point N-1 are the
+ * first and last centres exactly; a track of one detection, or of length 0,
+ * resamples to N copies of its first centre.  N = 20 in the paper. */
+void mpo_track_resample(const double* pts, int32_t n, int32_t N, double* out) {
+  if (n <= 0) return;
+  double L = 0.0;
+  for (int32_t k = 0; k + 1 < n; k++) {
+    double dx = pts[2 * (k + 1)] - pts[2 * k], dy = pts[2 * (k + 1) + 1] - pts[2 * k + 1];
+    L = L + sqrt(dx * dx + dy * dy);
+  }
+  for (int32_t i = 0; i < N; i++) {
+    double x, y;
+    if (n == 1 || L == 0.0 || i == 0) {
+      x = pts[0];
+      y = pts[1];
+    } else if (i == N - 1) {
+      x = pts[2 * (n - 1)];
+      y = pts[2 * (n - 1) + 1];
+    } else {
+      double t = (L * (double)i) / (double)(N - 1);
+      /* walk the segments: s = arc length at the start of segment k */
+      double s = 0.0;
+      int32_t k = 0;
+      double seg = 0.0;
+      for (k = 0; k + 1 < n; k++) {
+        double dx = pts[2 * (k + 1)] - pts[2 * k], dy = pts[2 * (k + 1) + 1] - pts[2 * k + 1];
+        seg = sqrt(dx * dx + dy * dy);
+        if (s + seg >= t || k + 2 == n) break;
+        s = s + seg;
+      }
+      double lam = seg > 0.0 ? (t - s) / seg : 0.0;
+      if (lam > 1.0) lam = 1.0;
+      if (lam < 0.0) lam = 0.0;
+      x = pts[2 * k] + lam * (pts[2 * (k + 1)] - pts[2 * k]);
+      y = pts[2 * k + 1] + lam * (pts[2 * (k + 1) + 1] - pts[2 * k + 1]);
+    }
+    out[2 * i] = x;
+    out[2 * i + 1] = y;
+  }
+}
+
+/* P:244 d(s1, s2) = (1/N) sum_i eucl(P(s1)[i], P(s2)[i]); summed in i order. */
+double mpo_track_distance(const double* a, const double* b, int32_t N) {
+  double s = 0.0;
+  for (int32_t i = 0; i < N; i++) {
+    double dx = a[2 * i] - b[2 * i], dy = a[2 * i + 1] - b[2 * i + 1];
+    s = s + sqrt(dx * dx + dy * dy);
+  }
+  return s / (double)N;
+}
+
+/* P:243 "we begin by clustering the tracks in S* using DBSCAN".  Reading R26:
+ * textbook DBSCAN over the T resampled paths [T][N][2] with distance d:
+ * neighbourhood N(i) = {j : d(i,j) <= eps} (i included), core iff |N(i)| >=
+ * min_pts; points visited in index order, each unvisited core point starts a
+ * new cluster expanded breadth-first through core points (so clusters are
+ * numbered by their smallest core index and a border point takes the first
+ * cluster that reaches it); points never reached are noise and become
+ * singleton clusters numbered after the DBSCAN clusters in index
+ * order.  labels[i] = cluster id; is_core[i] = 0/1.  Returns the cluster
+ * count (DBSCAN clusters + singletons); *n_dbscan = DBSCAN clusters only. */
+int32_t mpo_dbscan(const double* paths, int32_t T, int32_t N, double eps, int32_t min_pts, int32_t* labels,
+                   uint8_t* is_core, int32_t* n_dbscan) {
+  uint8_t* adj = (uint8_t*)malloc((size_t)T * T + 1);
+  int32_t* queue = (int32_t*)malloc(sizeof(int32_t) * (T + 1));
+  for (int32_t i = 0; i < T; i++) {
+    int32_t cnt = 0;
+    for (int32_t j = 0; j < T; j++) {
+      double d = mpo_track_distance(paths + (size_t)i * N * 2, paths + (size_t)j * N * 2, N);
+      adj[(size_t)i * T + j] = d <= eps;
+      cnt += d <= eps;
+    }
+    is_core[i] = cnt >= min_pts;
+    labels[i] = -1;
+  }
+  int32_t C = 0;
+  for (int32_t i = 0; i < T; i++) {
+    if (labels[i] >= 0 || !is_core[i]) continue;
+    int32_t c = C++;
+    int32_t head = 0, tail = 0;
+    labels[i] = c;
+    queue[tail++] = i;
+    while (head < tail) {
+      int32_t q = queue[head++];
+      if (!is_core[q]) continue; /* border points do not expand */
+      for (int32_t j = 0; j < T; j++) {
+        if (adj[(size_t)q * T + j] && labels[j] < 0) {
+          labels[j] = c;
+          queue[tail++] = j;
+        }
+      }
+    }
+  }
+  *n_dbscan = C;
+  for (int32_t i = 0; i < T; i++)
+    if (labels[i] < 0) labels[i] = C++;
+  free(adj);
+  free(queue);
+  return C;
+}
+
+/* P:245 "the center of a cluster ... p_i is the average of points in
+ * {P(s)[i] | s in C}": members summed in index order (fp64), divided by the
+ * member count.  centers [C][N][2], counts [C]. */
+void mpo_cluster_centers(const double* paths, int32_t T, int32_t N, const int32_t* labels, int32_t C,
+                         double* centers, int32_t* counts) {
+  for (int32_t c = 0; c < C; c++) counts[c] = 0;
+  for (size_t e = 0; e < (size_t)C * N * 2; e++) centers[e] = 0.0;
+  for (int32_t i = 0; i < T; i++) {
+    int32_t c = labels[i];
+    counts[c]++;
+    for (int32_t e = 0; e < 2 * N; e++) centers[(size_t)c * N * 2 + e] += paths[(size_t)i * N * 2 + e];
+  }
+  for (int32_t c = 0; c < C; c++)
+    for (int32_t e = 0; e < 2 * N; e++) centers[(size_t)c * N * 2 + e] /= (double)counts[c];
+}
+
+/* Does the segment p->q intersect the closed box [x0,x1] x [y0,y1]?  (Slab
+ * test on the segment's parameter range [0,1], fp64.) */
+static int seg_box(double px, double py, double qx, double qy, double x0, double y0, double x1, double y1) {
+  double t0 = 0.0, t1 = 1.0;
+  double d[2] = {qx - px, qy - py}, p[2] = {px, py}, lo[2] = {x0, y0}, hi[2] = {x1, y1};
+  for (int a = 0; a < 2; a++) {
+    if (d[a] == 0.0) {
+      if (p[a] < lo[a] || p[a] > hi[a]) return 0;
+    } else {
+      double ta = (lo[a] - p[a]) / d[a], tb = (hi[a] - p[a]) / d[a];
+      if (ta > tb) { double t = ta; ta = tb; tb = t; }
+      if (ta > t0) t0 = ta;
+      if (tb < t1) t1 = tb;
+      if (t0 > t1) return 0;
+    }
+  }
+  return 1;
+}
+
+/* P:246-247 refinement of one track.  Reading R27: a cluster is a candidate
+ * iff its centre path (polyline of N points) intersects the 3x3-cell square
+ * around the cell (cell = `cell` px, cell index floor(p / cell)) of the
+ * track's first or of its last centre ("cluster centers that pass close to
+ * d_1 and d_n"); candidates are ranked by d(track, centre)
+ * (ties: smaller cluster id) and taken in order until their member counts
+ * sum to >= k ("keep the k = 10 closest cluster centers, where a cluster of n
+ * tracks counts n times"); the new start (end) point is, per coordinate, the
+ * member-count-weighted median of the taken centres' first (last) points:
+ * the value at position ceil(W/2) of the ascending list in which each value
+ * is repeated by its weight (the lower middle for even W).
+ * path = the track's resampled N points; first/last = its first and last
+ * centres.  Writes out[4] = (start x, start y, end x, end y) and returns the
+ * number of clusters taken (0 = no candidate: out = first, last unchanged). */
+static int cmp_dbl(const void* a, const void* b) {
+  double x = *(const double*)a, y = *(const double*)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+static double wmedian(const double* vals, const int32_t* w, int32_t n) {
+  /* expand, sort, pick position ceil(W/2) (1-indexed) */
+  int64_t W = 0;
+  for (int32_t i = 0; i < n; i++) W += w[i];
+  double* e = (double*)malloc(sizeof(double) * (size_t)(W > 0 ? W : 1));
+  int64_t t = 0;
+  for (int32_t i = 0; i < n; i++)
+    for (int32_t r = 0; r < w[i]; r++) e[t++] = vals[i];
+  qsort(e, (size_t)W, sizeof(double), cmp_dbl);
+  double v = e[(W + 1) / 2 - 1];
+  free(e);
+  return v;
+}
+
+int32_t mpo_refine_track(const double* path, int32_t N, const double* first, const double* last,
+                         const double* centers, const int32_t* counts, int32_t C, double cell, int32_t k,
+                         double* out) {
+  out[0] = first[0];
+  out[1] = first[1];
+  out[2] = last[0];
+  out[3] = last[1];
+  double* dist = (double*)malloc(sizeof(double) * (C > 0 ? C : 1));
+  int32_t* cand = (int32_t*)malloc(sizeof(int32_t) * (C > 0 ? C : 1));
+  int32_t nc = 0;
+  for (int32_t c = 0; c < C; c++) {
+    const double* ctr = centers + (size_t)c * N * 2;
+    int hit = 0;
+    for (int e = 0; e < 2 && !hit; e++) {
+      const double* pt = e ? last : first;
+      double cx = floor(pt[0] / cell), cy = floor(pt[1] / cell);
+      double x0 = (cx - 1.0) * cell, y0 = (cy - 1.0) * cell, x1 = (cx + 2.0) * cell, y1 = (cy + 2.0) * cell;
+      for (int32_t i = 0; i + 1 < N && !hit; i++)
+        hit = seg_box(ctr[2 * i], ctr[2 * i + 1], ctr[2 * i + 2], ctr[2 * i + 3], x0, y0, x1, y1);
+    }
+    if (hit) {
+      cand[nc] = c;
+      dist[nc] = mpo_track_distance(path, ctr, N);
+      nc++;
+    }
+  }
+  /* rank by (distance, id): insertion sort (candidate lists are short) */
+  for (int32_t a = 1; a < nc; a++) {
+    int32_t cc = cand[a];
+    double dd = dist[a];
+    int32_t b = a - 1;
+    while (b >= 0 && (dist[b] > dd || (dist[b] == dd && cand[b] > cc))) {
+      cand[b + 1] = cand[b];
+      dist[b + 1] = dist[b];
+      b--;
+    }
+    cand[b + 1] = cc;
+    dist[b + 1] = dd;
+  }
+  int32_t taken = 0, wsum = 0;
+  while (taken < nc && wsum < k) wsum += counts[cand[taken++]];
+  if (taken > 0) {
+    double* v = (double*)malloc(sizeof(double) * taken);
+    int32_t* w = (int32_t*)malloc(sizeof(int32_t) * taken);
+    for (int32_t q = 0; q < 4; q++) {
+      int32_t pt = q < 2 ? 0 : N - 1, ax = q & 1;
+      for (int32_t t = 0; t < taken; t++) {
+        v[t] = centers[(size_t)cand[t] * N * 2 + 2 * pt + ax];
+        w[t] = counts[cand[t]];
+      }
+      out[q] = wmedian(v, w, taken);
+    }
+    free(v);
+    free(w);
+  }
+  free(dist);
+  free(cand);
+  return taken;
+}

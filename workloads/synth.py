@@ -377,3 +377,68 @@ def assign_batch(seed: int, B: int, m_range=(3, 40), n_range=(3, 40), sigma_px: 
         p = np.exp(-d2 / (2 * sigma_px ** 2)) * rng.uniform(0.85, 1.0, (m, n))
         out.append(p.astype(np.float32))
     return out
+
+
+# --------------------------------------------------------------------------- NEXT-4b
+def lane_paths(seed: int, n_lanes: int = 12, W: int = 1920, H: int = 1080):
+    """Synthetic traffic-camera lanes for the refinement stage:
+    each lane is a 3-5 point polyline from one frame border to another through
+    the interior (a turning movement).  Returns a list of float64 [k][2]."""
+    rng = np.random.default_rng(splitmix64(seed ^ 0x7E4E))
+    def border_point():
+        side = int(rng.integers(0, 4))
+        t = rng.uniform(0.1, 0.9)
+        return [(t * W, 0.0), (W, t * H), (t * W, float(H)), (0.0, t * H)][side], side
+    lanes = []
+    for _ in range(n_lanes):
+        (a, sa) = border_point()
+        (b, sb) = border_point()
+        while sb == sa:
+            (b, sb) = border_point()
+        k = int(rng.integers(1, 4))
+        mids = [(rng.uniform(0.25, 0.75) * W, rng.uniform(0.25, 0.75) * H) for _ in range(k)]
+        lanes.append(np.asarray([a] + mids + [b], np.float64))
+    return lanes
+
+
+def _walk(lane, speed, rng, jitter):
+    """Positions every frame along a lane polyline at `speed` px/frame."""
+    seg = np.sqrt((np.diff(lane, axis=0) ** 2).sum(1))
+    L = seg.sum()
+    s = np.arange(0.0, L, speed)
+    cum = np.concatenate([[0], np.cumsum(seg)])
+    k = np.clip(np.searchsorted(cum, s, side="right") - 1, 0, len(seg) - 1)
+    lam = (s - cum[k]) / np.maximum(seg[k], 1e-12)
+    pts = lane[k] + lam[:, None] * (lane[k + 1] - lane[k])
+    return pts + rng.normal(0, jitter, pts.shape)
+
+
+def track_sets(seed: int, n_train: int = 2000, n_query: int = 4000, n_lanes: int = 12, gap: int = 16):
+    """Training tracks S* (full-rate walks along the lanes, box 24-60 px) and
+    query tracks (a random middle 30-80% of a walk, sampled every `gap`
+    frames — a reduced-rate track) as lists of float32 [n][4] boxes.
+    Returns (lanes, train boxes, query boxes, query lane ids)."""
+    rng = np.random.default_rng(splitmix64(seed ^ 0x7E4F))
+    lanes = lane_paths(seed, n_lanes)
+
+    def boxes_of(pts):
+        sz = rng.uniform(24, 60)
+        b = np.concatenate([pts - sz / 2, pts + sz / 2], 1)
+        return b.astype(np.float32)
+
+    train, query, qlane = [], [], []
+    for _ in range(n_train):
+        li = int(rng.integers(0, n_lanes))
+        train.append(boxes_of(_walk(lanes[li], rng.uniform(4, 12), rng, 3.0)))
+    for _ in range(n_query):
+        li = int(rng.integers(0, n_lanes))
+        pts = _walk(lanes[li], rng.uniform(4, 12), rng, 3.0)
+        n = len(pts)
+        a = int(rng.uniform(0.1, 0.35) * n)
+        b = max(a + 2, int(rng.uniform(0.65, 0.9) * n))
+        q = pts[a:b:gap]
+        if len(q) < 2:
+            q = pts[a:b][[0, -1]]
+        query.append(boxes_of(q))
+        qlane.append(li)
+    return lanes, train, query, np.asarray(qlane)
