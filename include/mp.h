@@ -345,12 +345,79 @@ mp_status mp_hungarian(const float* d_scores, const mp_assign_problem* d_problem
                        int32_t max_dim, int32_t* d_row_match, int32_t* d_col_match, double* d_total,
                        int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * NEXT-4b: track refinement (§3.4 "Refinement").  Offline:
+ * the training tracks S* are resampled, clustered with DBSCAN and their
+ * cluster centres indexed; online: each (reduced-rate) track is extended to
+ * the member-weighted median start and end of its k nearest cluster centres.
+ * Readings R25-R27.  All arithmetic fp64 in the oracle's order
+ * (results bit-identical to oracle/).  A track set is given as detection
+ * boxes float [n_det][4] (x1, y1, x2, y2), frame order within a track, with a
+ * CSR d_track_off int32 [T+1].
+ */
+
+/* mp_track_resample — R25: each track's box-centre path resampled to N points
+ * evenly spaced in arc length ("we compute N points evenly spaced along each
+ * track").  d_paths double [T][N][2]; d_ends double [T][4] (first and
+ * last centre: x0, y0, x1, y1), may be NULL.  Tracks with no detection get
+ * zeros.  2 <= N <= 64, else MP_ERR_INVALID.  One kernel. */
+mp_status mp_track_resample(const float* d_boxes, const int32_t* d_track_off, int32_t T, int32_t N,
+                            double* d_paths, double* d_ends, void* stream);
+
+/* mp_dbscan — R26: DBSCAN of T resampled paths under d(s1,s2) = mean
+ * point distance, neighbourhood d <= eps, core iff >= min_pts
+ * neighbours (self included); clusters numbered by smallest core index,
+ * border tracks join the lowest-numbered cluster with a core neighbour, noise
+ * tracks become singleton clusters numbered after them (index order).
+ *  d_labels  device int32 [T] cluster id per track.
+ *  d_is_core device uint8 [T] (may be NULL).
+ *  d_nclust  device int32 [2]: [0] = DBSCAN clusters, [1] = all clusters.
+ *  eps > 0, min_pts >= 1, T <= 65536, else MP_ERR_INVALID.
+ *  Launches: memset + adjacency (warp per track pair block, early exit once
+ *  the partial distance sum clearly exceeds eps*N) + core/union/label kernels
+ *  + two single-CTA scans (cluster and singleton numbering). */
+size_t mp_dbscan_workspace_size(int32_t T);
+mp_status mp_dbscan(const double* d_paths, int32_t T, int32_t N, double eps, int32_t min_pts, int32_t* d_labels,
+                    uint8_t* d_is_core, int32_t* d_nclust, void* d_ws, size_t ws_bytes, void* stream);
+
+/* mp_cluster_centers — P:245: the centre of cluster c is the pointwise mean of
+ * its members' paths (members summed in index order, fp64).  C = d_nclust[1]
+ * (device); clusters c >= C_max are not written (*d_status = MP_ERR_CAPACITY).
+ * d_centers double [C_max][N][2]; d_counts int32 [C_max]. */
+mp_status mp_cluster_centers(const double* d_paths, int32_t T, int32_t N, const int32_t* d_labels,
+                             const int32_t* d_nclust, int32_t C_max, double* d_centers, int32_t* d_counts,
+                             int32_t* d_status, void* stream);
+
+/* mp_refine_tracks — P:246-247 / R27: for each query track q (its resampled
+ * path d_paths[q] and end centres d_ends[q] from mp_track_resample): the
+ * candidate clusters are those whose centre polyline intersects the 3x3-cell
+ * square (cells of `cell` px) around the cell of the track's first or last
+ * centre — found through a grid index over the centres (cell -> clusters,
+ * built in the workspace on every call) and confirmed by an exact
+ * segment/square test; candidates are ranked by (d(track, centre), id) and
+ * taken until their member counts reach k; d_out[q] = (start x, start y,
+ * end x, end y) = per-coordinate member-weighted medians of the taken
+ * centres' first / last points (unchanged end centres if no candidate);
+ * d_taken[q] = clusters taken.
+ *  W, H: frame size (grid extent; centres outside are clamped into the grid).
+ *  cell > 0, 1 <= k, max_cand: per-query candidate capacity (<= 1024;
+ *  exceeding it sets *d_status = MP_ERR_CAPACITY and the query is left
+ *  unchanged).  C = d_nclust[1] <= C_max <= 65536.
+ *  Launches: memset + index count + scan + index fill + query (warp per query). */
+size_t mp_refine_workspace_size(int32_t W, int32_t H, double cell, int32_t C_max, int32_t N);
+mp_status mp_refine_tracks(const double* d_paths, const double* d_ends, int32_t Q, int32_t N,
+                           const double* d_centers, const int32_t* d_counts, const int32_t* d_nclust,
+                           int32_t C_max, int32_t W, int32_t H, double cell, int32_t k, int32_t max_cand,
+                           double* d_out, int32_t* d_taken, int32_t* d_status, void* d_ws, size_t ws_bytes,
+                           void* stream);
+
 /* Human-readable name of a status code (static string, never NULL). */
 const char* mp_status_string(mp_status st);
 
 /* Number of device kernels the library launches per call (diagnostic, used
  * by bench.py to count launches): which = 0 plan, 1 gather, 2 remap_nms,
- * 3 proxy_sweep, 4 window_set_cost, 5 hungarian. */
+ * 3 proxy_sweep, 4 window_set_cost, 5 hungarian, 6 track_resample,
+ * 7 dbscan, 8 cluster_centers, 9 refine_tracks. */
 int32_t mp_launches_per_call(int32_t which);
 
 #ifdef __cplusplus

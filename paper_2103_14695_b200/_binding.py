@@ -78,6 +78,20 @@ def _load():
     L.mp_hungarian_workspace_size.argtypes = [i32]
     L.mp_hungarian.restype = C.c_int
     L.mp_hungarian.argtypes = [vp, vp, i32, C.c_float, i32, vp, vp, vp, vp, vp, sz, vp]
+    dbl = C.c_double
+    L.mp_track_resample.restype = C.c_int
+    L.mp_track_resample.argtypes = [vp, vp, i32, i32, vp, vp, vp]
+    L.mp_dbscan_workspace_size.restype = sz
+    L.mp_dbscan_workspace_size.argtypes = [i32]
+    L.mp_dbscan.restype = C.c_int
+    L.mp_dbscan.argtypes = [vp, i32, i32, dbl, i32, vp, vp, vp, vp, sz, vp]
+    L.mp_cluster_centers.restype = C.c_int
+    L.mp_cluster_centers.argtypes = [vp, i32, i32, vp, vp, i32, vp, vp, vp, vp]
+    L.mp_refine_workspace_size.restype = sz
+    L.mp_refine_workspace_size.argtypes = [i32, i32, dbl, i32, i32]
+    L.mp_refine_tracks.restype = C.c_int
+    L.mp_refine_tracks.argtypes = [vp, vp, i32, i32, vp, vp, vp, i32, i32, i32, dbl, i32, i32, vp, vp, vp, vp, sz,
+                                   vp]
     L.mp_remap_nms_workspace_size.restype = sz
     L.mp_remap_nms_workspace_size.argtypes = [i32, i32]
     L.mp_remap_nms.restype = C.c_int
@@ -375,3 +389,65 @@ def mp_hungarian(scores, problems, B, floor_, max_dim, row_match, col_match, tot
                            _p(col_match), _p(total), _p(status), _p(ws), ws.numel(), _stream(stream))
     if st != MP_OK:
         raise MPError(st, "mp_hungarian")
+
+
+# --------------------------------------------------------------------------- NEXT-4b
+def mp_track_resample(boxes, track_off, T, N, paths, ends=None, stream=None) -> None:
+    """R25: boxes float32 CUDA [n_det, 4]; track_off int32 [T+1]; paths float64
+    [T, N, 2]; ends float64 [T, 4] or None."""
+    _dev(boxes, torch.float32, "boxes")
+    _dev(track_off, torch.int32, "track_off")
+    _dev(paths, torch.float64, "paths")
+    _dev(ends, torch.float64, "ends")
+    st = _lib.mp_track_resample(_p(boxes), _p(track_off), int(T), int(N), _p(paths), _p(ends), _stream(stream))
+    if st != MP_OK:
+        raise MPError(st, "mp_track_resample")
+
+
+def mp_dbscan_workspace_size(T: int) -> int:
+    return int(_lib.mp_dbscan_workspace_size(int(T)))
+
+
+def mp_dbscan(paths, T, N, eps, min_pts, labels, is_core, nclust, ws, stream=None) -> None:
+    """R26: labels int32 [T]; is_core uint8 [T] or None; nclust int32 [2]."""
+    _dev(paths, torch.float64, "paths")
+    _dev(labels, torch.int32, "labels")
+    _dev(is_core, torch.uint8, "is_core")
+    _dev(nclust, torch.int32, "nclust")
+    _dev(ws, torch.uint8, "ws")
+    st = _lib.mp_dbscan(_p(paths), int(T), int(N), float(eps), int(min_pts), _p(labels), _p(is_core), _p(nclust),
+                        _p(ws), ws.numel(), _stream(stream))
+    if st != MP_OK:
+        raise MPError(st, "mp_dbscan")
+
+
+def mp_cluster_centers(paths, T, N, labels, nclust, C_max, centers, counts, status, stream=None) -> None:
+    _dev(paths, torch.float64, "paths")
+    _dev(labels, torch.int32, "labels")
+    _dev(nclust, torch.int32, "nclust")
+    _dev(centers, torch.float64, "centers")
+    _dev(counts, torch.int32, "counts")
+    _dev(status, torch.int32, "status")
+    st = _lib.mp_cluster_centers(_p(paths), int(T), int(N), _p(labels), _p(nclust), int(C_max), _p(centers),
+                                 _p(counts), _p(status), _stream(stream))
+    if st != MP_OK:
+        raise MPError(st, "mp_cluster_centers")
+
+
+def mp_refine_workspace_size(W, H, cell, C_max, N) -> int:
+    return int(_lib.mp_refine_workspace_size(int(W), int(H), float(cell), int(C_max), int(N)))
+
+
+def mp_refine_tracks(paths, ends, Q, N, centers, counts, nclust, C_max, W, H, cell, k, max_cand, out, taken, status,
+                     ws, stream=None) -> None:
+    """R27: out float64 [Q, 4]; taken int32 [Q]."""
+    for t, dt, nm in ((paths, torch.float64, "paths"), (ends, torch.float64, "ends"), (centers, torch.float64,
+                      "centers"), (counts, torch.int32, "counts"), (nclust, torch.int32, "nclust"),
+                      (out, torch.float64, "out"), (taken, torch.int32, "taken"), (status, torch.int32, "status"),
+                      (ws, torch.uint8, "ws")):
+        _dev(t, dt, nm)
+    st = _lib.mp_refine_tracks(_p(paths), _p(ends), int(Q), int(N), _p(centers), _p(counts), _p(nclust),
+                               int(C_max), int(W), int(H), float(cell), int(k), int(max_cand), _p(out), _p(taken),
+                               _p(status), _p(ws), ws.numel(), _stream(stream))
+    if st != MP_OK:
+        raise MPError(st, "mp_refine_tracks")

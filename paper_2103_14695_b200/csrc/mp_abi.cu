@@ -19,6 +19,8 @@ extern "C" const char* mp_status_string(mp_status st) {
 //   proxy_sweep: memset (not a kernel) + proxy_sweep_kernel
 //   hungarian: memset (not a kernel) + hung_warp_kernel + hung_mid_kernel (max_dim > 64)
 //              + hung_block_kernel (max_dim > 160)
+//   track_resample: 1;  dbscan: memset + adj + core + union + root + scan + label + scan + noise (8);
+//   cluster_centers: 1;  refine_tracks: 3 memsets + index count + scan + fill + query (4)
 extern "C" int32_t mp_launches_per_call(int32_t which) {
   switch (which) {
     case 0: return 4;
@@ -27,6 +29,10 @@ extern "C" int32_t mp_launches_per_call(int32_t which) {
     case 3: return 1;
     case 4: return 1;
     case 5: return 3;
+    case 6: return 1;
+    case 7: return 8;
+    case 8: return 1;
+    case 9: return 4;
   }
   return 0;
 }

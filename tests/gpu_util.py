@@ -135,3 +135,46 @@ def gpu_hungarian(mats, floor=0.5, max_dim=None):
     rows = [rmh[rec["row_off"][b]:rec["row_off"][b] + ms[b]] for b in range(len(mats))]
     cols = [cmh[rec["col_off"][b]:rec["col_off"][b] + ns[b]] for b in range(len(mats))]
     return int(st.item()), rows, cols, tot.cpu().numpy()[:len(mats)]
+
+
+def gpu_refine_pipeline(train_boxes, query_boxes, eps, min_pts, N=20, W=1920, H=1080, cell=32.0, k=10,
+                        max_cand=1024, C_max=None):
+    """NEXT-4b end to end on the GPU: resample train + query tracks, DBSCAN the
+    training paths, cluster centres, refine the queries.  Returns a dict of
+    numpy arrays."""
+    def pack(tr):
+        off = np.concatenate([[0], np.cumsum([len(b) for b in tr])]).astype(np.int32)
+        bx = np.concatenate([np.asarray(b, np.float32).reshape(-1, 4) for b in tr]) if off[-1] else \
+            np.zeros((1, 4), np.float32)
+        return torch.from_numpy(bx).to(DEV), torch.from_numpy(off).to(DEV)
+
+    T, Q = len(train_boxes), len(query_boxes)
+    tb, to = pack(train_boxes)
+    qb, qo = pack(query_boxes)
+    tp = torch.empty((max(T, 1), N, 2), dtype=torch.float64, device=DEV)
+    te = torch.empty((max(T, 1), 4), dtype=torch.float64, device=DEV)
+    qp = torch.empty((max(Q, 1), N, 2), dtype=torch.float64, device=DEV)
+    qe = torch.empty((max(Q, 1), 4), dtype=torch.float64, device=DEV)
+    B.mp_track_resample(tb, to, T, N, tp, te)
+    B.mp_track_resample(qb, qo, Q, N, qp, qe)
+    lab = torch.full((max(T, 1),), -9, dtype=torch.int32, device=DEV)
+    core = torch.zeros((max(T, 1),), dtype=torch.uint8, device=DEV)
+    ncl = torch.zeros(2, dtype=torch.int32, device=DEV)
+    ws = torch.empty(max(B.mp_dbscan_workspace_size(T), 1), dtype=torch.uint8, device=DEV)
+    B.mp_dbscan(tp, T, N, eps, min_pts, lab, core, ncl, ws)
+    C_max = max(T, 1) if C_max is None else C_max
+    ctr = torch.zeros((max(C_max, 1), N, 2), dtype=torch.float64, device=DEV)
+    cnt = torch.zeros((max(C_max, 1),), dtype=torch.int32, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    B.mp_cluster_centers(tp, T, N, lab, ncl, C_max, ctr, cnt, st)
+    out = torch.full((max(Q, 1), 4), -1.0, dtype=torch.float64, device=DEV)
+    taken = torch.full((max(Q, 1),), -1, dtype=torch.int32, device=DEV)
+    rws = torch.empty(max(B.mp_refine_workspace_size(W, H, cell, C_max, N), 1), dtype=torch.uint8, device=DEV)
+    B.mp_refine_tracks(qp, qe, Q, N, ctr, cnt, ncl, C_max, W, H, cell, k, max_cand, out, taken, st, rws)
+    torch.cuda.synchronize()
+    C = int(ncl[1].item())
+    return dict(status=int(st.item()), train_paths=tp[:T].cpu().numpy(), train_ends=te[:T].cpu().numpy(),
+                query_paths=qp[:Q].cpu().numpy(), query_ends=qe[:Q].cpu().numpy(), labels=lab[:T].cpu().numpy(),
+                is_core=core[:T].cpu().numpy().astype(bool), nclust=ncl.cpu().numpy(),
+                centers=ctr[:min(C, C_max)].cpu().numpy(), counts=cnt[:min(C, C_max)].cpu().numpy(),
+                out=out[:Q].cpu().numpy(), taken=taken[:Q].cpu().numpy())
