@@ -627,6 +627,114 @@ def run_assign(args):
     return 0
 
 
+def run_refine(args):
+    """NEXT-4b measurement: offline index build over 4,000
+    full-rate training tracks of a 12-lane junction (resample + DBSCAN +
+    centres) and online refinement of 65,536 reduced-rate (gap 16) tracks
+    (resample + grid-indexed k-NN + weighted medians).  Metric: refined
+    tracks per second (the online step, timed as one step per iteration);
+    the index build is reported alongside."""
+    import torch
+
+    import paper_2103_14695_b200 as mp
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    N, W, H, cell, k = 20, 1920, 1080, 32.0, 10
+    lanes, train, query, _ = S.track_sets(21, 4000, 4096, 12, gap=16)
+    query = query * 16                                   # 65,536 query tracks (16 copies of 4,096)
+    eps, min_pts = 0.05 * math.hypot(W, H), 2
+
+    def pack(tr):
+        off = np.concatenate([[0], np.cumsum([len(b) for b in tr])]).astype(np.int32)
+        return (torch.from_numpy(np.concatenate(tr).astype(np.float32)).to(dev), torch.from_numpy(off).to(dev),
+                int(off[-1]))
+
+    T, Q = len(train), len(query)
+    tb, to, n_tdet = pack(train)
+    qb, qo, n_qdet = pack(query)
+    tp = torch.empty((T, N, 2), dtype=torch.float64, device=dev)
+    te = torch.empty((T, 4), dtype=torch.float64, device=dev)
+    qp = torch.empty((Q, N, 2), dtype=torch.float64, device=dev)
+    qe = torch.empty((Q, 4), dtype=torch.float64, device=dev)
+    lab = torch.empty(T, dtype=torch.int32, device=dev)
+    ncl = torch.zeros(2, dtype=torch.int32, device=dev)
+    dws = torch.empty(mp.mp_dbscan_workspace_size(T), dtype=torch.uint8, device=dev)
+    ctr = torch.empty((T, N, 2), dtype=torch.float64, device=dev)
+    cnt = torch.empty(T, dtype=torch.int32, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    out = torch.empty((Q, 4), dtype=torch.float64, device=dev)
+    taken = torch.empty(Q, dtype=torch.int32, device=dev)
+    rws = torch.empty(mp.mp_refine_workspace_size(W, H, cell, T, N), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def build():
+        mp.mp_track_resample(tb, to, T, N, tp, te)
+        mp.mp_dbscan(tp, T, N, eps, min_pts, lab, None, ncl, dws)
+        mp.mp_cluster_centers(tp, T, N, lab, ncl, T, ctr, cnt, st)
+
+    def online():
+        mp.mp_track_resample(qb, qo, Q, N, qp, qe)
+        mp.mp_refine_tracks(qp, qe, Q, N, ctr, cnt, ncl, T, W, H, cell, k, 256, out, taken, st, rws)
+
+    def timed(fn, n):
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(n):
+            fn()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        return t0.elapsed_time(t1) / n
+
+    for _ in range(max(3, args.warmup)):
+        build()
+        online()
+    torch.cuda.synchronize()
+    build_ms = timed(build, 3)
+    sampler = ClockSampler(dev.index or 0)
+    sampler.start()
+    time.sleep(0.3)
+    ms = timed(online, args.steps)
+    clocks = sampler.stop()
+    assert int(st.item()) == 0, int(st.item())
+    nd, C = (int(x) for x in ncl.cpu().tolist())
+    tk = taken.cpu().numpy()
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle as O
+        from concurrent.futures import ThreadPoolExecutor
+        O.build()
+        threads = os.cpu_count() or 1
+        ctr_h, cnt_h = ctr[:C].cpu().numpy(), cnt[:C].cpu().numpy()
+        sample = query[:2048]
+
+        def one(b):
+            c = O.box_centers(b)
+            return O.refine_track(O.track_resample(c, N), c[0], c[-1], ctr_h, cnt_h, cell, k)
+
+        t = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            list(ex.map(one, sample))
+        dt = time.perf_counter() - t
+        cpu = {"value": len(sample) / dt, "unit": "tracks/s", "cores": threads, "kind": "oracle",
+               "sample": f"{len(sample)} of the {Q} query tracks (resample + refine against the same "
+                         f"{C} centres), {threads} threads, {host_cpu_desc()}"}
+    print(json.dumps({
+        "metric": "refined tracks/sec (NEXT-4b online refinement)",
+        "value": Q / (ms * 1e-3), "unit": "tracks/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "12-lane junction, 4000 training tracks, 65536 gap-16 query tracks",
+                   "N": N, "eps_px": eps, "min_pts": min_pts, "cell_px": cell, "k": k,
+                   "train_detections": n_tdet, "query_detections": n_qdet},
+        "index_build_ms": build_ms,
+        "result": {"dbscan_clusters": nd, "clusters_incl_singletons": C,
+                   "queries_refined": int((tk > 0).sum()), "mean_taken": float(tk.mean())},
+        "roofline": {"bound": "latency", "note": "fp64 ALU + per-query serial selection; no bandwidth roofline"},
+        "cpu_baseline": cpu, "clocks": clocks,
+        "gpu_launches": args.steps * (mp.launches_per_call(6) + mp.launches_per_call(9))}), flush=True)
+    return 0
+
+
 def run_e2e(cfg, clip, scene, scores_np, boxes, wbo, fmt, dev, args):
     """Same metric through WindowPipeline with HOST inputs: each step copies the
     clip's frames (from a pinned host pool), scores and detector boxes H2D and
@@ -708,9 +816,10 @@ def main():
     ap.add_argument("--src", default="rgb24", choices=["rgb24", "nv12"],
                     help="frame format: rgb24 rows (default) or NV12 decoder output with the proxy-input "
                          "downscale in the step (NEXT-3)")
-    ap.add_argument("--mode", default="path", choices=["path", "sweep", "wsel", "assign"],
+    ap.add_argument("--mode", default="path", choices=["path", "sweep", "wsel", "assign", "refine"],
                     help="path: the hot path a1-a7 (default); sweep: NEXT-1 proxy-module sweep; "
-                         "wsel: NEXT-2 window-size selection step; assign: NEXT-4a batched Hungarian")
+                         "wsel: NEXT-2 window-size selection step; assign: NEXT-4a batched Hungarian; "
+                         "refine: NEXT-4b track refinement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -721,6 +830,8 @@ def main():
         return run_wsel(args)
     if args.mode == "assign":
         return run_assign(args)
+    if args.mode == "refine":
+        return run_refine(args)
     return run_b200(args)
 
 

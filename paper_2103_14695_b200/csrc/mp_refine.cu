@@ -241,34 +241,62 @@ __global__ void dbscan_noise_kernel(int T, const int* __restrict__ rank, const i
 }
 
 // ------------------------------------------------------------------ centres
-constexpr int kCtrChunk = 10;   // points per pass (20 doubles in registers)
+// One CTA per cluster: the members are found in index order chunk by chunk
+// (block scan of label == c over 1024 tracks), then threads t < 2N add their
+// coordinate of each member in that order (the oracle's summation order).
+constexpr int kCtrThreads = 256, kCtrChunk = 1024;
 
-__global__ void cluster_centers_kernel(const double* __restrict__ paths, int T, int N, const int* __restrict__ labels,
-                                       const int* __restrict__ nclust, int C_max, double* __restrict__ centers,
-                                       int* __restrict__ counts, int* __restrict__ status) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kCtrThreads) cluster_centers_kernel(const double* __restrict__ paths, int T, int N,
+                                                                     const int* __restrict__ labels,
+                                                                     const int* __restrict__ nclust, int C_max,
+                                                                     double* __restrict__ centers,
+                                                                     int* __restrict__ counts, int* __restrict__ status) {
+  __shared__ int mem[kCtrChunk];
+  __shared__ int tmp[33];
+  __shared__ int nmem;
+  const int c = blockIdx.x;
   const int C = nclust[1];
-  if (c == 0 && C > C_max) set_status(status, MP_ERR_CAPACITY);
-  if (c >= C || c >= C_max) return;
+  if (c == 0 && threadIdx.x == 0 && C > C_max) set_status(status, MP_ERR_CAPACITY);
+  if (c >= C) return;
+  const int tid = threadIdx.x;
+  double acc = 0.0;   // thread tid < 2N owns coordinate tid
   int cnt = 0;
-  for (int p0 = 0; p0 < N; p0 += kCtrChunk) {
-    double acc[2 * kCtrChunk];
+  for (int base = 0; base < T; base += kCtrChunk) {
+    // flags of this chunk -> member positions (index order)
+    constexpr int per = kCtrChunk / kCtrThreads;
+    int f[per], s = 0;
 #pragma unroll
-    for (int e = 0; e < 2 * kCtrChunk; e++) acc[e] = 0.0;
-    cnt = 0;
-    for (int i = 0; i < T; i++) {
-      if (__ldg(&labels[i]) != c) continue;
-      cnt++;
-      const double* pp = paths + (size_t)i * N * 2 + 2 * p0;
-#pragma unroll
-      for (int e = 0; e < 2 * kCtrChunk; e++)
-        if (2 * p0 + e < 2 * N) acc[e] = __dadd_rn(acc[e], pp[e]);
+    for (int r = 0; r < per; r++) {
+      const int i = base + tid * per + r;
+      f[r] = (i < T && labels[i] == c) ? 1 : 0;
+      s += f[r];
     }
+    const int lane = tid & 31, wid = tid >> 5;
+    const int inc = warp_incl_scan(s);
+    if (lane == 31) tmp[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      const int v = lane < kCtrThreads / 32 ? tmp[lane] : 0;
+      const int vi = warp_incl_scan(v);
+      if (lane < kCtrThreads / 32) tmp[lane] = vi - v;
+      if (lane == kCtrThreads / 32 - 1) nmem = vi;
+    }
+    __syncthreads();
+    int pos = tmp[wid] + inc - s;
 #pragma unroll
-    for (int e = 0; e < 2 * kCtrChunk; e++)
-      if (2 * p0 + e < 2 * N) centers[(size_t)c * N * 2 + 2 * p0 + e] = __ddiv_rn(acc[e], (double)cnt);
+    for (int r = 0; r < per; r++)
+      if (f[r]) mem[pos++] = base + tid * per + r;
+    __syncthreads();
+    const int nm = nmem;
+    if (tid < 2 * N)
+      for (int m = 0; m < nm; m++) acc = __dadd_rn(acc, paths[(size_t)mem[m] * N * 2 + tid]);
+    cnt += nm;
+    __syncthreads();
   }
-  counts[c] = cnt;
+  if (c < C_max) {
+    if (tid < 2 * N) centers[(size_t)c * N * 2 + tid] = __ddiv_rn(acc, (double)cnt);
+    if (tid == 0) counts[c] = cnt;
+  }
 }
 
 // ------------------------------------------------------------------ refine
@@ -360,42 +388,55 @@ __device__ bool seg_box(double px, double py, double qx, double qy, double x0, d
 }
 
 constexpr int kRefWarps = 4;
+
+// shared bytes per query warp (16-B multiple so every warp's doubles stay aligned)
+__host__ __device__ __forceinline__ size_t refine_warp_bytes(int cap, int C_max) {
+  return ((size_t)cap * (2 * 4 + 4 + 8 + 4) + 16 + (size_t)((C_max + 31) / 32) * 4 + 15) & ~size_t(15);
+}
 constexpr int kRefMaxCand = 1024;
 
 __global__ void __launch_bounds__(32 * kRefWarps) refine_query_kernel(const RefineArgs A) {
   extern __shared__ __align__(16) unsigned char rsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int cap = A.max_cand;
-  // per warp: raw ids [2*cap] int, unique ids [cap] int, dist [cap] double, order [cap] int
-  unsigned char* base = rsm + (size_t)wid * ((size_t)cap * (2 * 4 + 4 + 8 + 4));
+  // per warp: raw ids [2*cap] int, unique ids [cap] int, dist [cap] double, order [cap] int,
+  // seen-bitmap [ceil(C_max/32)] words (cleared again after each query)
+  const int bm_words = (A.C_max + 31) / 32;
+  unsigned char* base = rsm + (size_t)wid * refine_warp_bytes(cap, A.C_max);
   int* raw = reinterpret_cast<int*>(base);
   int* uniq = raw + 2 * cap;
   double* dist = reinterpret_cast<double*>(uniq + cap + (cap & 1));
   int* ord = reinterpret_cast<int*>(dist + cap);
+  unsigned int* seen = reinterpret_cast<unsigned int*>(ord + cap);
+  for (int w = lane; w < bm_words; w += 32) seen[w] = 0u;
+  __syncwarp();
   const int N = A.N;
   const int C = min(A.nclust[1], A.C_max);
   for (int q = blockIdx.x * kRefWarps + wid; q < A.Q; q += gridDim.x * kRefWarps) {
     const double* path = A.paths + (size_t)q * N * 2;
     const double fx = A.ends[4 * q], fy = A.ends[4 * q + 1], lx = A.ends[4 * q + 2], ly = A.ends[4 * q + 3];
-    // 1. raw candidate ids from the 4x4 cells around each end (closed 3x3-cell squares)
+    // 1. raw candidate ids from the 4x4 cells around each end (the closed
+    //    3x3-cell squares reach into the 4th row/column): lane = one cell
     int nraw = 0;
     bool over = false;
-    for (int e = 0; e < 2; e++) {
+    {
+      const int e = lane >> 4, cxo = (lane & 3) - 1, cyo = ((lane >> 2) & 3) - 1;
       const double px = e ? lx : fx, py = e ? ly : fy;
-      const int cx = cell_of(px, A.cell, A.gw), cy = cell_of(py, A.cell, A.gh);
-      for (int y = max(cy - 1, 0); y <= min(cy + 2, A.gh - 1); y++)
-        for (int x = max(cx - 1, 0); x <= min(cx + 2, A.gw - 1); x++) {
-          const int a = min(A.cell_off[y * A.gw + x], A.ids_cap), b = min(A.cell_off[y * A.gw + x + 1], A.ids_cap);
-          for (int t = a + lane; t < b; t += 32) {
-            const int slot = nraw + (t - a);
-            if (slot < 2 * cap) raw[slot] = A.cell_ids[t];
-          }
-          nraw += b - a;
-        }
+      const int x = cell_of(px, A.cell, A.gw) + cxo, y = cell_of(py, A.cell, A.gh) + cyo;
+      int a = 0, b = 0;
+      if (x >= 0 && x < A.gw && y >= 0 && y < A.gh) {
+        a = min(A.cell_off[y * A.gw + x], A.ids_cap);
+        b = min(A.cell_off[y * A.gw + x + 1], A.ids_cap);
+      }
+      const int len = b - a;
+      const int incl = warp_incl_scan(len);
+      nraw = __shfl_sync(0xffffffffu, incl, 31);
+      if (nraw <= 2 * cap)
+        for (int t = 0; t < len; t++) raw[incl - len + t] = A.cell_ids[a + t];
     }
     if (nraw > 2 * cap) over = true;
     __syncwarp();
-    // 2. unique ids, ascending
+    // 2. unique ids (first claim of each id in the seen-bitmap), then ascending
     int nu = 0;
     if (!over) {
       for (int base0 = 0; base0 < nraw; base0 += 32) {
@@ -404,12 +445,8 @@ __global__ void __launch_bounds__(32 * kRefWarps) refine_query_kernel(const Refi
         int v = 0;
         if (t < nraw) {
           v = raw[t];
-          first = true;
-          for (int u = 0; u < t; u++)
-            if (raw[u] == v) {
-              first = false;
-              break;
-            }
+          const unsigned int bit = 1u << (v & 31);
+          first = !(atomicOr(&seen[v >> 5], bit) & bit);
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, first);
         if (first) {
@@ -418,6 +455,8 @@ __global__ void __launch_bounds__(32 * kRefWarps) refine_query_kernel(const Refi
         }
         nu += __popc(bal);
       }
+      __syncwarp();
+      for (int t = lane; t < nraw; t += 32) seen[raw[t] >> 5] = 0u;   // clear for the next query
       if (nu > cap) over = true;
     }
     __syncwarp();
@@ -610,8 +649,8 @@ extern "C" mp_status mp_cluster_centers(const double* d_paths, int32_t T, int32_
   if (C_max == 0) return MP_OK;
   if (!d_centers || !d_counts || (T > 0 && (!d_paths || !d_labels))) return MP_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
-  cluster_centers_kernel<<<(C_max + 127) / 128, 128, 0, s>>>(d_paths, T, N, d_labels, d_nclust, C_max, d_centers,
-                                                            d_counts, d_status);
+  cluster_centers_kernel<<<C_max, kCtrThreads, 0, s>>>(d_paths, T, N, d_labels, d_nclust, C_max, d_centers, d_counts,
+                                                      d_status);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
@@ -701,7 +740,7 @@ extern "C" mp_status mp_refine_tracks(const double* d_paths, const double* d_end
     refine_index_fill_kernel<<<sms * 4, 256, 0, s>>>(A);
     MP_CUDA_TRY(cudaGetLastError());
   }
-  const size_t per_warp = (size_t)max_cand * (2 * 4 + 4 + 8 + 4) + 16;
+  const size_t per_warp = refine_warp_bytes(max_cand, C_max);
   const size_t smem = per_warp * kRefWarps;
   if (smem > 200 * 1024) return MP_ERR_UNSUPPORTED;
   MP_CUDA_TRY(cudaFuncSetAttribute(refine_query_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
