@@ -1,4 +1,7 @@
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out
-timeout -s KILL 900 python bench.py --mode refine --steps 20 --warmup 3 > gpurun_out/bench_refine.log 2>&1
-timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"track_|dbscan|cluster_|refine_|scan_kernel" -c 30 --csv --log-file gpurun_out/refine_ncu.csv python bench.py --mode refine --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+mkdir -p gpurun_out/final
+O=gpurun_out/final
+timeout -s KILL 900 compute-sanitizer --tool racecheck --print-limit 20 python -m pytest tests/test_gpu_assign.py -q -x -k "large or synth" > $O/san_racecheck_assign.log 2>&1; echo "rc=$?" >> $O/san_racecheck_assign.log
+timeout -s KILL 900 compute-sanitizer --tool synccheck --print-limit 20 python -m pytest tests/test_gpu_assign.py -q -x -k "large" > $O/san_synccheck_assign.log 2>&1; echo "rc=$?" >> $O/san_synccheck_assign.log
+timeout -s KILL 900 python -m pytest tests/test_gpu_assign.py -q > $O/pytest_assign.log 2>&1
+timeout -s KILL 600 python bench.py --mode assign --steps 50 --warmup 5 > $O/bench_assign.log 2>&1

@@ -177,6 +177,7 @@ __device__ void hung_solve(const HungArgs& A, const mp_assign_problem& pb, int t
       j0 = j1;
       if (p[j0] == 0) break;
     }
+    Grp::sync();   // every thread has read p[j0] for the exit test before it changes
     // flip the augmenting path (sequential, short)
     if (tid == 0) {
       do {

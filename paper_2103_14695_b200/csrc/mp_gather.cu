@@ -31,12 +31,15 @@
 namespace mpk {
 
 constexpr int kProducerWarps = 1;
-constexpr int kCW = 8;   // consumer warps per CTA; each owns a block of TR/kCW output rows
+#ifndef MP_KCW
+#define MP_KCW 8
+#endif
+constexpr int kCW = MP_KCW;   // consumer warps per CTA; each owns a block of TR/kCW output rows
 constexpr int kStages = 2;      // default ring depth (A.stages; MP_GATHER_STAGES overrides, <= kMaxStages)
 constexpr int kMaxStages = 8;
 constexpr int kHdrBytes = 64;
 constexpr int kMaxTW = 256;
-constexpr int kMaxTR = 96;
+constexpr int kMaxTR = 8 * kCW > 96 ? 8 * kCW : 96;   // Rw <= 8 rows per consumer warp
 constexpr int kXtapBytes = (kMaxTW + 2) * 8, kYtapBytes = (kMaxTR + 2) * 8;
 constexpr int kTapBytes = kXtapBytes + kYtapBytes;
 constexpr int kStageDataBudget = 44 * 1024;        // dense classes
