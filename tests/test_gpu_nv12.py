@@ -168,3 +168,50 @@ def test_pipeline_nv12_runner_matches_oracle(G):
         st, pref = O.gather_resize_nv12(frames_np, cfg.pitch_nv12, cfg.W, cfg.H, pw, [(cfg.W, cfg.H)],
                                         [cfg.proxy_dims], [F])
         assert np.abs(p.proxy_out.cpu().numpy() - pref[0]).max() <= F32_TOL
+
+
+def test_full_size_nv12_bench_config_parity(G):
+    """configs[1] at full size (1800 NV12 1080p frames) through the 4-stream
+    PipelinedRunner as `bench.py --src nv12` runs it: windows exact; crop and
+    proxy-input pixels on seeded samples, each recomputed by the oracle."""
+    import paper_2103_14695_b200 as mp
+    cfg = S.CONFIGS["c2_1080p_sparse"]
+    F = cfg.frames
+    scene = S.make_scene(cfg, 0, F)
+    scores = S.score_grids(cfg, 0, scene)
+    ref = O.plan_windows(cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores)
+    caps = [int(c) for c in ref["class_count"]]
+    n = len(ref["windows"])
+    pipes = []
+    for _ in range(2):
+        p = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
+                              cfg.iou_thr, device=G.DEV, src="nv12", proxy_dims=cfg.proxy_dims)
+        p.reserve(F, n + 64, caps=caps, max_boxes=1)
+        pipes.append(p)
+    runner = mp.PipelinedRunner(pipes, device=G.DEV)
+    frames = S.frame_pixels_torch([S.frame_seed(0, f) for f in range(F)], cfg.H + cfg.H // 2, cfg.pitch_nv12,
+                                  device=G.DEV)
+    sc = torch.from_numpy(scores).to(G.DEV)
+    runner.capture_graphs(sc)
+    for _ in range(3):
+        runner.step(sc, frames)
+    runner.wait_all()
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(77)
+    for p in pipes:
+        p.check_status()
+        assert np.array_equal(p.windows[:n].cpu().numpy(), ref["windows"])
+        for wi in rng.choice(n, size=25, replace=False):
+            w = ref["windows"][wi].copy()
+            f, q, slot = int(w[0]), int(w[5]), int(w[6])
+            fr = S.frame_nv12_np(S.frame_seed(0, f), cfg.H, cfg.pitch_nv12)
+            one = w.copy(); one[0] = 0; one[6] = 0
+            caps1 = [1 if qq == q else 0 for qq in range(len(cfg.sizes))]
+            st, o = O.gather_resize_nv12([fr], cfg.pitch_nv12, cfg.W, cfg.H, one[None], cfg.sizes, cfg.out_dims,
+                                         caps1)
+            assert np.abs(p.outs[q][slot].cpu().numpy() - o[q][0]).max() <= F32_TOL
+        for f in rng.choice(F, size=6, replace=False):
+            fr = S.frame_nv12_np(S.frame_seed(0, int(f)), cfg.H, cfg.pitch_nv12)
+            st, o = O.gather_resize_nv12([fr], cfg.pitch_nv12, cfg.W, cfg.H, [[0, 0, 0, cfg.W, cfg.H, 0, 0]],
+                                         [(cfg.W, cfg.H)], [cfg.proxy_dims], [1])
+            assert np.abs(p.proxy_out[int(f)].cpu().numpy() - o[0][0]).max() <= F32_TOL
