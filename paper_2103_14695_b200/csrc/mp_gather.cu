@@ -119,9 +119,12 @@ __device__ __forceinline__ float clamp255(float v) {
   return __int_as_float(__vimin_s32_relu(__float_as_int(v), 0x437F0000));
 }
 
-__device__ __forceinline__ uint8_t u8_round(float v) {   // R16: floor(v + 0.5), clamped
-  const int r = __float2int_rd(v + 0.5f);
-  return (uint8_t)min(max(r, 0), 255);
+// R16 for a pair of values already in [0, 255] (RGB lerps are convex
+// combinations of bytes; NV12 values are clamped first): floor(v + 0.5) as
+// the low byte of the fp32 bits of RD(fp32(v + 0.5) + 2^23) — packed, no
+// float->int conversion (v + 0.5 rounded in fp32, as the R16 decision is).
+__device__ __forceinline__ float2 u8_round2(float2 v) {
+  return __fadd2_rd(__fadd2_rn(v, make_float2(0.5f, 0.5f)), make_float2(8388608.0f, 8388608.0f));
 }
 
 __device__ __forceinline__ int tiles_total(const GatherArgs& A, const int* cnt) {
@@ -306,11 +309,9 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
     v0 = __ffma2_rn(CRV, vv_, yy_);                                                             \
     v1 = __ffma2_rn(CGU, uu_, __ffma2_rn(CGV, vv_, yy_));                                       \
     v2 = __ffma2_rn(CBU, uu_, yy_);                                                             \
-    if (FMT == MP_OUT_F32_NCHW) {                                                               \
-      v0 = make_float2(clamp255(v0.x), clamp255(v0.y));                                         \
-      v1 = make_float2(clamp255(v1.x), clamp255(v1.y));                                         \
-      v2 = make_float2(clamp255(v2.x), clamp255(v2.y));                                         \
-    }                                                                                           \
+    v0 = make_float2(clamp255(v0.x), clamp255(v0.y));                                           \
+    v1 = make_float2(clamp255(v1.x), clamp255(v1.y));                                           \
+    v2 = make_float2(clamp255(v2.x), clamp255(v2.y));                                           \
   }
   const int ow = A.ow[q], oh = A.oh[q];
   const bool sparse = A.sparse[q] != 0;
@@ -356,15 +357,16 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
     const float2 ly = make_float2(__int_as_float(y.y), __int_as_float(y.y));                    \
     _Pragma("unroll") for (int p = 0; p < NP; p++) {                                            \
       MP_V(T, B)                                                                                \
+      const float2 r0 = u8_round2(v0), r1 = u8_round2(v1), r2 = u8_round2(v2);                   \
       if (ok[2 * p]) {                                                                          \
-        o[192 * p + 0] = u8_round(v0.x);                                                        \
-        o[192 * p + 1] = u8_round(v1.x);                                                        \
-        o[192 * p + 2] = u8_round(v2.x);                                                        \
+        o[192 * p + 0] = (uint8_t)__float_as_uint(r0.x);                                        \
+        o[192 * p + 1] = (uint8_t)__float_as_uint(r1.x);                                        \
+        o[192 * p + 2] = (uint8_t)__float_as_uint(r2.x);                                        \
       }                                                                                         \
       if (ok[2 * p + 1]) {                                                                      \
-        o[192 * p + 96 + 0] = u8_round(v0.y);                                                   \
-        o[192 * p + 96 + 1] = u8_round(v1.y);                                                   \
-        o[192 * p + 96 + 2] = u8_round(v2.y);                                                   \
+        o[192 * p + 96 + 0] = (uint8_t)__float_as_uint(r0.y);                                   \
+        o[192 * p + 96 + 1] = (uint8_t)__float_as_uint(r1.y);                                   \
+        o[192 * p + 96 + 2] = (uint8_t)__float_as_uint(r2.y);                                   \
       }                                                                                         \
     }                                                                                           \
     o += (size_t)ow * 3;                                                                        \
