@@ -319,7 +319,7 @@ def run_b200(args):
                                cfg.iou_thr, fmt=fmt, device=dev, **pkw)
         p2.reserve(F, n_win, caps=counts, max_boxes=max(len(boxes), 1))
         pipes.append(p2)
-    runner = mp.PipelinedRunner(pipes, device=dev)
+    runner = mp.PipelinedRunner(pipes, device=dev, merge_on_gather_stream=bool(args.merge_on_gather))
     stream = torch.cuda.current_stream(dev)
     if args.graphs:
         runner.capture_graphs(scores, boxes_t, wbo_t)
@@ -813,6 +813,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=2, help="batches in flight (buffer sets) in the stream pipeline")
     ap.add_argument("--graphs", type=int, default=1, help="replay plan/merge as CUDA graphs")
+    ap.add_argument("--merge-on-gather", type=int, default=0,
+                    help="run remap/NMS on the gather stream right after the gather (no co-running)")
     ap.add_argument("--src", default="rgb24", choices=["rgb24", "nv12"],
                     help="frame format: rgb24 rows (default) or NV12 decoder output with the proxy-input "
                          "downscale in the step (NEXT-3)")

@@ -167,13 +167,16 @@ class PipelinedRunner:
         plan(i) -> gather(i) -> [detector] -> merge(i);  plan(i) waits merge(i-depth).
     """
 
-    def __init__(self, pipes, device="cuda"):
+    def __init__(self, pipes, device="cuda", merge_on_gather_stream: bool = False):
         self.pipes = list(pipes)
         self.depth = len(self.pipes)
         dev = torch.device(device)
         self.s_plan = torch.cuda.Stream(dev)
         self.s_gather = torch.cuda.Stream(dev)
-        self.s_merge = torch.cuda.Stream(dev)
+        # merge_on_gather_stream: remap/NMS(i) runs right after gather(i) on the
+        # gather stream instead of concurrently with gather(i+1) (the persistent
+        # gather leaves co-running latency-bound kernels little of each SM)
+        self.s_merge = self.s_gather if merge_on_gather_stream else torch.cuda.Stream(dev)
         self.s_proxy = torch.cuda.Stream(dev) if self.pipes[0].proxy_dims else None
         self.done = [None] * self.depth
         self.i = 0
