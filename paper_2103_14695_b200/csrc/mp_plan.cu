@@ -141,6 +141,8 @@ extern __shared__ __align__(16) unsigned char smem_raw[];
 // acceptance, remove + append); used when a frame has many components.
 __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n) {
   __shared__ unsigned long long red[64];
+  __shared__ int pub[6];
+  __shared__ long long pub_sum;
   int par = 0;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, BS = blockDim.x;
   const long long* T = P.cost;
@@ -169,36 +171,56 @@ __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n) {
       const int ws = P.sw[s], hs = P.sh[s];
       long long sum = T[S.csz[i]] + T[S.csz[j]];
       int before_i = (j < i) ? 1 : 0, n_abs = 0;
-      int pos = 0;
-      while (pos < n) {
-        const int q = pos + tid;
-        unsigned long long cand = ~0ull;
-        if (q < n && q != i && q != j) {
-          int qx, qy, qw, qh;
-          extent(P, min(m0, S.bc0[q]), min(n0, S.br0[q]), max(m1, S.bc1[q]), max(n1, S.br1[q]), qx, qy, qw, qh);
-          if (qw <= ws && qh <= hs) cand = (unsigned long long)q;
+      // absorption (k ascending, each fitting cluster at once, R7) by warp 0
+      // alone with ballots — no CTA barrier per absorbed cluster — then the
+      // grown box is published to the CTA through shared memory
+      if (wid == 0) {
+        int pos = 0;
+        while (pos < n) {
+          const int q = pos + lane;
+          bool fit = false;
+          if (q < n && q != i && q != j) {
+            int qx, qy, qw, qh;
+            extent(P, min(m0, S.bc0[q]), min(n0, S.br0[q]), max(m1, S.bc1[q]), max(n1, S.br1[q]), qx, qy, qw,
+                   qh);
+            fit = (qw <= ws) && (qh <= hs);
+          }
+          const uint32_t msk = __ballot_sync(0xffffffffu, fit);
+          if (msk) {
+            const int qq = pos + __ffs(msk) - 1;
+            m0 = min(m0, S.bc0[qq]);
+            n0 = min(n0, S.br0[qq]);
+            m1 = max(m1, S.bc1[qq]);
+            n1 = max(n1, S.br1[qq]);
+            sum += T[S.csz[qq]];
+            before_i += (qq < i) ? 1 : 0;
+            n_abs++;
+            if (lane == 0) S.memb[qq] = 1;
+            pos = qq + 1;
+          } else {
+            pos += 32;
+          }
         }
-        cand = block_min_u64(cand, red, par);
-        if (cand != ~0ull) {
-          const int qq = (int)cand;
-          m0 = min(m0, S.bc0[qq]);
-          n0 = min(n0, S.br0[qq]);
-          m1 = max(m1, S.bc1[qq]);
-          n1 = max(n1, S.br1[qq]);
-          sum += T[S.csz[qq]];
-          before_i += (qq < i) ? 1 : 0;
-          n_abs++;
-          if (tid == 0) S.memb[qq] = 1;
-          pos = qq + 1;
-        } else {
-          pos += BS;
+        if (lane == 0) {
+          S.memb[i] = 1;
+          S.memb[j] = 1;
+          pub[0] = m0;
+          pub[1] = n0;
+          pub[2] = m1;
+          pub[3] = n1;
+          pub[4] = before_i;
+          pub[5] = n_abs;
+          pub_sum = sum;
         }
-      }
-      if (tid == 0) {
-        S.memb[i] = 1;
-        S.memb[j] = 1;
       }
       __syncthreads();
+      m0 = pub[0];
+      n0 = pub[1];
+      m1 = pub[2];
+      n1 = pub[3];
+      before_i = pub[4];
+      n_abs = pub[5];
+      sum = pub_sum;
       if (T[s] < sum) {
         if (wid == 0) {   // stable compaction + append (warp 0)
           int wpos = 0;
