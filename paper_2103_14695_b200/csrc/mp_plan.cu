@@ -139,12 +139,18 @@ extern __shared__ __align__(16) unsigned char smem_raw[];
 // a3 with the whole CTA (exactly the P:184 greedy of the warp-0 path below:
 // same nearest-neighbour metric and ties, same ascending absorption, strict
 // acceptance, remove + append); used when a frame has many components.
+// Per step: block arg-min for the nearest neighbour; every warp tests its
+// 32-cluster chunks against the initial merged box (a cluster that does not
+// fit it can never fit the grown box, R7), warp 0 then walks only those
+// candidates in ascending order; an accepted merge is compacted by the whole
+// CTA (block scan of the keep flags, chunked read-then-write moves).
 __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n) {
   __shared__ unsigned long long red[64];
   __shared__ int pub[6];
   __shared__ long long pub_sum;
+  __shared__ uint32_t fitm[256];   // initial-fit ballots, one word per 32 clusters (n <= 8192)
   int par = 0;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, BS = blockDim.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, BS = blockDim.x, NW = BS >> 5;
   const long long* T = P.cost;
   bool again = true;
   while (again) {
@@ -171,34 +177,56 @@ __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n) {
       const int ws = P.sw[s], hs = P.sh[s];
       long long sum = T[S.csz[i]] + T[S.csz[j]];
       int before_i = (j < i) ? 1 : 0, n_abs = 0;
+      // initial-fit ballots (all warps)
+      const int nch = (n + 31) >> 5;
+      for (int c = wid; c < nch; c += NW) {
+        const int q = (c << 5) + lane;
+        bool fit = false;
+        if (q < n && q != i && q != j) {
+          int qx, qy, qw, qh;
+          extent(P, min(m0, S.bc0[q]), min(n0, S.br0[q]), max(m1, S.bc1[q]), max(n1, S.br1[q]), qx, qy, qw, qh);
+          fit = (qw <= ws) && (qh <= hs);
+        }
+        const uint32_t msk = __ballot_sync(0xffffffffu, fit);
+        if (lane == 0) fitm[c] = msk;
+      }
+      __syncthreads();
       // absorption (k ascending, each fitting cluster at once, R7) by warp 0
-      // alone with ballots — no CTA barrier per absorbed cluster — then the
-      // grown box is published to the CTA through shared memory
+      // over the initial candidates only; the grown box is then published
       if (wid == 0) {
-        int pos = 0;
-        while (pos < n) {
-          const int q = pos + lane;
-          bool fit = false;
-          if (q < n && q != i && q != j) {
-            int qx, qy, qw, qh;
-            extent(P, min(m0, S.bc0[q]), min(n0, S.br0[q]), max(m1, S.bc1[q]), max(n1, S.br1[q]), qx, qy, qw,
-                   qh);
-            fit = (qw <= ws) && (qh <= hs);
-          }
-          const uint32_t msk = __ballot_sync(0xffffffffu, fit);
-          if (msk) {
-            const int qq = pos + __ffs(msk) - 1;
-            m0 = min(m0, S.bc0[qq]);
-            n0 = min(n0, S.br0[qq]);
-            m1 = max(m1, S.bc1[qq]);
-            n1 = max(n1, S.br1[qq]);
-            sum += T[S.csz[qq]];
-            before_i += (qq < i) ? 1 : 0;
-            n_abs++;
-            if (lane == 0) S.memb[qq] = 1;
-            pos = qq + 1;
-          } else {
-            pos += 32;
+        for (int c0 = 0; c0 < nch; c0 += 32) {
+          const uint32_t word = (c0 + lane < nch) ? fitm[c0 + lane] : 0u;
+          uint32_t nz = __ballot_sync(0xffffffffu, word != 0u);
+          while (nz) {
+            const int c = c0 + __ffs(nz) - 1;
+            nz &= nz - 1;
+            // lanes re-test this word's remaining candidates against the current
+            // box at once; the first fitting one is absorbed and the ones before
+            // it dropped (they cannot fit the grown box either)
+            uint32_t rem = fitm[c];
+            while (rem) {
+              const int q = (c << 5) + lane;
+              bool fit = false;
+              if ((rem >> lane) & 1u) {
+                int qx, qy, qw, qh;
+                extent(P, min(m0, S.bc0[q]), min(n0, S.br0[q]), max(m1, S.bc1[q]), max(n1, S.br1[q]), qx, qy, qw,
+                       qh);
+                fit = (qw <= ws) && (qh <= hs);
+              }
+              const uint32_t fm = __ballot_sync(0xffffffffu, fit);
+              if (!fm) break;
+              const int bq = __ffs(fm) - 1;
+              const int qq = (c << 5) + bq;
+              m0 = min(m0, S.bc0[qq]);
+              n0 = min(n0, S.br0[qq]);
+              m1 = max(m1, S.bc1[qq]);
+              n1 = max(n1, S.br1[qq]);
+              sum += T[S.csz[qq]];
+              before_i += (qq < i) ? 1 : 0;
+              n_abs++;
+              if (lane == 0) S.memb[qq] = 1;
+              rem &= (bq == 31) ? 0u : ~((2u << bq) - 1u);
+            }
           }
         }
         if (lane == 0) {
@@ -222,34 +250,35 @@ __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n) {
       n_abs = pub[5];
       sum = pub_sum;
       if (T[s] < sum) {
-        if (wid == 0) {   // stable compaction + append (warp 0)
-          int wpos = 0;
-          for (int base = 0; base < n; base += 32) {
-            const int q = base + lane;
-            bool keep = false;
-            int v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-            unsigned char vs = 0;
-            if (q < n) {
-              keep = !S.memb[q];
-              v0 = S.bc0[q]; v1 = S.br0[q]; v2 = S.bc1[q]; v3 = S.br1[q]; vs = S.csz[q];
-            }
-            const uint32_t km = __ballot_sync(0xffffffffu, keep);
-            __syncwarp();
-            if (keep) {
-              const int d = wpos + __popc(km & lanemask_lt());
-              S.bc0[d] = v0; S.br0[d] = v1; S.bc1[d] = v2; S.br1[d] = v3; S.csz[d] = vs;
-            }
-            if (q < n) S.memb[q] = 0;
-            wpos += __popc(km);
-            __syncwarp();
+        // stable compaction by the CTA: destinations from a block scan of the
+        // keep flags (in S.cid, free during the merge); elements only move to
+        // lower indices, so reading a chunk before writing it is safe
+        for (int q = tid; q < n; q += BS) S.cid[q] = S.memb[q] ? 0 : 1;
+        __syncthreads();
+        const int kept = block_excl_scan_smem(S.cid, n, S.tmp);
+        for (int base = 0; base < n; base += BS) {
+          const int q = base + tid;
+          bool keep = false;
+          int v0 = 0, v1 = 0, v2 = 0, v3 = 0, d = 0;
+          unsigned char vs = 0;
+          if (q < n) {
+            keep = !S.memb[q];
+            d = S.cid[q];
+            v0 = S.bc0[q]; v1 = S.br0[q]; v2 = S.bc1[q]; v3 = S.br1[q]; vs = S.csz[q];
           }
-          if (lane == 0) {
-            S.bc0[wpos] = m0; S.br0[wpos] = n0; S.bc1[wpos] = m1; S.br1[wpos] = n1;
-            S.csz[wpos] = (unsigned char)s;
+          __syncthreads();
+          if (keep) {
+            S.bc0[d] = v0; S.br0[d] = v1; S.bc1[d] = v2; S.br1[d] = v3; S.csz[d] = vs;
           }
+          if (q < n) S.memb[q] = 0;
+          __syncthreads();
+        }
+        if (tid == 0) {
+          S.bc0[kept] = m0; S.br0[kept] = n0; S.bc1[kept] = m1; S.br1[kept] = n1;
+          S.csz[kept] = (unsigned char)s;
         }
         __syncthreads();
-        n = n - (2 + n_abs) + 1;   // members removed, merged cluster appended
+        n = kept + 1;   // members removed, merged cluster appended
         again = true;
         i -= before_i;
       } else {
