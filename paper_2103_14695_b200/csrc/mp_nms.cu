@@ -70,6 +70,8 @@ __host__ __device__ inline size_t nms_smem_bytes(int cap, int mask_cap, NmsSmem*
   const size_t maskb = sizeof(unsigned long long) * (size_t)mask_cap * ((mask_cap + 63) / 64);
   size_t u = keyb > maskb ? keyb : maskb;
   if ((size_t)cap > u) u = cap;
+  const size_t permb = (size_t)cap * (sizeof(float4) + 3 * sizeof(int));   // sorted-order permutation scratch
+  if (permb > u) u = permb;
   s.key = (unsigned long long*)take(u);
   s.supp = (unsigned char*)s.key;
   if (S) *S = s;
@@ -186,6 +188,31 @@ __device__ void nms_frame(const NmsArgs& A, int f, int b_lo, int b_hi, int w_lo,
   }
   for (int p = tid; p < n; p += blockDim.x) S.order[p] = (int)(S.key[p] & 0xffffffffu);
   __syncthreads();
+  // physically permute the candidates into the sorted order (through the now
+  // free key region) so the O(n^2) IoU loops read consecutive entries instead
+  // of order[]-scattered ones; order[] becomes the identity
+  {
+    float4* tb = reinterpret_cast<float4*>(S.key);
+    int* tc = reinterpret_cast<int*>(tb + n);
+    float* ts = reinterpret_cast<float*>(tc + n);
+    int* tr = reinterpret_cast<int*>(ts + n);
+    for (int p = tid; p < n; p += blockDim.x) {
+      const int q = S.order[p];
+      tb[p] = S.bx[q];
+      tc[p] = S.cls[q];
+      ts[p] = S.score[q];
+      tr[p] = S.src[q];
+    }
+    __syncthreads();
+    for (int p = tid; p < n; p += blockDim.x) {
+      S.bx[p] = tb[p];
+      S.cls[p] = tc[p];
+      S.score[p] = ts[p];
+      S.src[p] = tr[p];
+      S.order[p] = p;
+    }
+    __syncthreads();
+  }
 
   // ---- a7: greedy class-aware NMS
   int nk = 0;
@@ -193,7 +220,9 @@ __device__ void nms_frame(const NmsArgs& A, int f, int b_lo, int b_hi, int w_lo,
     const int words = (n + 63) >> 6;
     unsigned long long* mask = S.key;
     for (int idx = tid; idx < n * words; idx += blockDim.x) {
-      const int i = idx / words, wd = idx - i * words;
+      // consecutive threads = consecutive rows of one 64-column word: the
+      // (sorted, contiguous) column boxes are read as broadcasts
+      const int wd = idx / n, i = idx - wd * n;
       const int qi = S.order[i];
       const float4 bi = S.bx[qi];
       const int ci = S.cls[qi];
@@ -203,7 +232,7 @@ __device__ void nms_frame(const NmsArgs& A, int f, int b_lo, int b_hi, int w_lo,
         const int qj = S.order[j];
         if (S.cls[qj] == ci && iou_rn(bi, S.bx[qj]) > A.iou_thr) bits |= 1ull << (j - wd * 64);
       }
-      mask[idx] = bits;
+      mask[(size_t)i * words + wd] = bits;
     }
     __syncthreads();
     if (wid == 0) {

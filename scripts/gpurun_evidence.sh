@@ -17,3 +17,7 @@ for c in c1_540p c3_1080p_dense c4_4k_drone; do timeout -s KILL 600 python bench
 timeout -s KILL 600 python bench.py --impl reference --steps 5 --warmup 3 > $O/bench_ref.log 2>&1
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"plan_|gather_|nms_" -c 60 --csv --log-file $O/launches.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --depth 1 > $O/launches_bench.log 2>&1
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:"gather_kernel" -s 3 -c 1 -o $O/prof_gather -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --depth 1 > $O/prof_bench.log 2>&1
+timeout -s KILL 600 python bench.py --mode assign --steps 50 --warmup 5 > $O/bench_assign.log 2>&1
+timeout -s KILL 900 python bench.py --mode refine --steps 20 --warmup 3 > $O/bench_refine.log 2>&1
+timeout -s KILL 900 python bench.py --mode sweep > $O/bench_sweep.log 2>&1
+timeout -s KILL 900 python bench.py --mode wsel --steps 5 --warmup 3 > $O/bench_wsel.log 2>&1
