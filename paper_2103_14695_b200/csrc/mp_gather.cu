@@ -187,6 +187,18 @@ __global__ void __launch_bounds__(kPrepThreads) gather_prep_kernel(GatherArgs A,
 // the extra (finite) staged byte has no effect.
 extern __shared__ __align__(128) unsigned char smem[];
 
+// Experiment knobs (MP_GATHER_BUDGET_KB, _TILE, _WAIT, _STAGES, _DEBUG) are
+// read from the environment only in builds with -DMP_EXPERIMENT_KNOBS (the
+// dev sweeps of scripts/time_gather.py); the production library ignores them.
+static inline const char* knob(const char* name) {
+#ifdef MP_EXPERIMENT_KNOBS
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
 template <int FMT, int NCOL, int SRC>
 __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr* hdr, unsigned int soff, int wid,
                                              int lane) {
@@ -679,7 +691,7 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
   A->src = src;
   long long data_max = 0;
   int list = 0, taps = 0;
-  const char* bud = getenv("MP_GATHER_BUDGET_KB");   // experiment knob
+  const char* bud = knob("MP_GATHER_BUDGET_KB");   // experiment knob
   const long long budget = (bud && atoi(bud) >= 8) ? 1024LL * atoi(bud) : kStageDataBudget;
   for (int q = 0; q < k; q++) {
     const int w = sizes[q].w, h = sizes[q].h, ow = out_dims[q].w, oh = out_dims[q].h;
@@ -746,7 +758,7 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
     }
     {
       // experiment knob: MP_GATHER_TILE=ow,TW,Rw forces the tile of classes with that output width
-      const char* ft = getenv("MP_GATHER_TILE");
+      const char* ft = knob("MP_GATHER_TILE");
       int fow = 0, ftw = 0, frw = 0;
       if (ft && sscanf(ft, "%d,%d,%d", &fow, &ftw, &frw) == 3 && fow == ow) {
         TW = ftw;
@@ -836,9 +848,9 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
   gather_prep_kernel<<<256, kPrepThreads, 0, s>>>(A, d_windows, d_frame_off, ws_cnt, ws_list, ws_tap, n_taps, d_status);
   MP_CUDA_TRY(cudaGetLastError());
   if (A.F == 0) return MP_OK;
-  const char* wm = getenv("MP_GATHER_WAIT");   // experiment knob
+  const char* wm = knob("MP_GATHER_WAIT");   // experiment knob
   A.wait_mode = wm ? atoi(wm) : 3;
-  const char* stg = getenv("MP_GATHER_STAGES");   // experiment knob
+  const char* stg = knob("MP_GATHER_STAGES");   // experiment knob
   A.stages = stg ? atoi(stg) : kStages;
   if (A.stages < 2 || A.stages > kMaxStages) A.stages = kStages;
   const size_t smem = (size_t)A.stages * A.stage_bytes + 2 * A.stages * sizeof(uint64_t);
@@ -848,7 +860,7 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
   MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   // Diagnostic only (profiling the two halves of the pipeline): MP_GATHER_DEBUG=1
   // skips the consumer math, =2 skips the pixel copies.  Unset in production.
-  const char* dbg = getenv("MP_GATHER_DEBUG");
+  const char* dbg = knob("MP_GATHER_DEBUG");
   A.debug = dbg ? atoi(dbg) : 0;
   const int threads = (kCW + kProducerWarps) * 32;
   auto launch = [&](auto kern) -> mp_status {

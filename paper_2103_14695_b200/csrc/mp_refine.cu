@@ -19,8 +19,6 @@
 // in the oracle's order, so results are bit-identical to oracle/.
 #include <math.h>
 
-#include <algorithm>
-
 #include "mp_internal.cuh"
 
 namespace mpk {

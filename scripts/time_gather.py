@@ -1,7 +1,9 @@
 """Dev tool: time the gather kernels alone (CUDA events, after warm-up) for the
 c2 workload — the NV12 / RGB crop gather and the NEXT-3 proxy-input
 downscale.  Prints one JSON line per measurement.  Used to sweep the
-MP_GATHER_* experiment knobs; not part of the bench contract."""
+MP_GATHER_* experiment knobs, which the library reads only when built with
+-DMP_EXPERIMENT_KNOBS (e.g. nvcc ... -DMP_EXPERIMENT_KNOBS into a copy of
+libmp_b200.so); not part of the bench contract."""
 import json
 import os
 import sys
