@@ -54,9 +54,13 @@ class WindowPipeline:
     # ------------------------------------------------------------ buffers
     def reserve(self, F: int, max_windows: int, caps: Optional[Sequence[int]] = None, max_boxes: int = 0,
                 max_out: Optional[int] = None):
+        """Size the buffers for batches of F frames.  The window buffers only
+        grow (a smaller max_windows for the same F keeps them, and the planned
+        windows in them), so plan -> reserve(caps from the plan) -> gather
+        works without re-planning."""
         dev = self.device
         R, C = self.params.grid
-        if F != self.F or max_windows != self.max_windows:
+        if F != self.F or max_windows > self.max_windows:
             self.F, self.max_windows = int(F), int(max_windows)
             self.windows = torch.zeros((max(self.max_windows, 1), 7), dtype=torch.int32, device=dev)
             self.frame_off = torch.zeros(self.F + 1, dtype=torch.int32, device=dev)
