@@ -429,6 +429,8 @@ def run_b200(args):
             "roofline": {"bound": "hbm", "kernel": "gather_resize (prep + gather_kernel)",
                          "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "peak_nominal": 7700.0, "frac_nominal": achieved / 7700.0,
+                         "nominal_source": "B200 HBM3e 7.7 TB/s (HGX datasheet, B200_PROFILING.md)",
                          "alg_bytes_per_launch": ab["gather_union"],
                          "alg_bytes_per_launch_window_sum": ab["gather_sum"],
                          "launch_ms": gather_ms, "step_alg_bytes": ab["step"],
