@@ -418,7 +418,10 @@ def run_b200(args):
             threads = os.cpu_count() or 1
             inp, n = oracle_baseline(cfg, clip, threads, 15.0, args.src)
             dt = oracle_run(cfg, inp, n, threads)
+            n1 = max(1, n // max(threads, 1))          # the same oracle on one host thread
+            dt1 = oracle_run(cfg, inp, n1, 1)
             cpu = {"value": n / dt, "unit": "frames/s", "cores": threads, "kind": "oracle",
+                   "value_1thread": n1 / dt1, "sample_1thread": f"first {n1} frames, 1 thread",
                    "sample": f"first {n} of {F} frames of clip {clip} ({cfg.name}), "
                              f"{'proxy-input downscale+' if nv12 else ''}plan+gather+remap/NMS, {args.src} "
                              f"frames, {threads} threads, {host_cpu_desc()}"}
