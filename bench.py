@@ -355,10 +355,12 @@ def run_b200(args):
     runner.s_plan.wait_stream(stream)
     if runner.s_proxy is not None:
         runner.s_proxy.wait_stream(stream)
+    h0 = time.perf_counter()
     for i in range(args.steps):
         runner.step(scores, frame_ring[i % n_copies], boxes_t, wbo_t, gather_events=evs[i], proxy_events=pevs[i])
     runner.wait_all(stream)
     t1.record(stream)
+    host_enqueue_ms = (time.perf_counter() - h0) * 1e3   # no host sync in the loop: << device time
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -450,6 +452,7 @@ def run_b200(args):
                          "gather_share_of_step": gather_ms / (tmax_ms / args.steps)},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "host_enqueue_ms_per_step": host_enqueue_ms / args.steps,
             "gpu_launches": args.steps * (mp.launches_per_call(0) + mp.launches_per_call(1) * (2 if nv12 else 1) +
                                           mp.launches_per_call(2)),
             "proxy_input": proxy,
