@@ -87,26 +87,33 @@ def test_assign_clips_partition(libs_available):
         assert max(loads) - min(loads) <= cost.max() + 1e-9      # LPT bound
 
 
-def test_gloo_world2_counters_and_results_match_single_process(libs_available):
-    n_clips = 5
+@pytest.mark.parametrize("world,n_clips", [(2, 5), (4, 6)])
+def test_gloo_counters_and_results_match_single_process(libs_available, world, n_clips):
     port = _free_port()
     manager = mp_.get_context("spawn").Manager()
     out = manager.dict()
     ctx = mp_.get_context("spawn")
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_clips, out)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n_clips, out)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(240)
         assert p.exitcode == 0
-    (m0, g0, e0, d0), (m1, g1, e1, d1) = out[0], out[1]
-    assert sorted(m0 + m1) == list(range(n_clips)) and not set(m0) & set(m1)
-    assert g0 == g1 and e0 == e1 == 11.0
+    res = [out[r] for r in range(world)]
+    mine = [m for (m, _, _, _) in res]
+    assert sorted(c for m in mine for c in m) == list(range(n_clips))
+    assert sum(len(m) for m in mine) == n_clips                      # each clip on exactly one rank
+    g = [x[1] for x in res]
+    e = [x[2] for x in res]
+    assert all(gi == g[0] for gi in g) and all(ei == 10.0 + world - 1 for ei in e)   # SUM / MAX reductions
     # single-process reference
     from paper_2103_14695_b200.sharding import Counters
     ref = Counters()
+    digests = {}
+    for (_, _, _, d) in res:
+        digests.update(d)
     for clip in range(n_clips):
         c, d = _clip_counters(clip)
         ref.add(c)
-        assert (d0.get(clip) or d1.get(clip)) == d     # per-clip outputs independent of sharding
-    assert g0 == ref
+        assert digests[clip] == d     # per-clip outputs independent of the sharding
+    assert g[0] == ref
