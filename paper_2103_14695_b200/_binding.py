@@ -16,6 +16,7 @@ import ctypes as C
 import os
 from typing import Sequence
 
+import numpy as _np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -346,7 +347,6 @@ def mp_window_set_cost(params: PlanParams, scores, F, cand, cand_cost, tot, ws, 
 
 
 # --------------------------------------------------------------------------- NEXT-4a
-import numpy as _np  # noqa: E402
 
 ASSIGN_PROBLEM_DTYPE = _np.dtype([("score_off", "<i8"), ("m", "<i4"), ("n", "<i4"), ("row_off", "<i4"),
                                   ("col_off", "<i4")])   # = mp_assign_problem, 24 bytes
