@@ -126,8 +126,12 @@ size_t mp_gather_workspace_size(int32_t k, const mp_size* out_dims, const int32_
  * resampling convention R15/R16: half-pixel centres, taps clamped to the crop,
  * exact integer tap positions, fp32 arithmetic).
  *
- *  d_frame_ptrs  device array [F] of device pointers; frame f is uint8
- *                [H][pitch] with RGB24 pixels, 16-byte aligned.
+ *  d_frame_ptrs  device array [F] of device-accessible pointers; frame f is
+ *                uint8 [H][pitch] with RGB24 pixels, 16-byte aligned.  A frame
+ *                may live in HBM or in page-locked host memory (cudaHostAlloc /
+ *                cudaHostRegister, mapped under UVA): the kernel then reads
+ *                only the window footprints over PCIe (zero-copy; bit-identical
+ *                results, no staging copy of the whole frame).
  *  pitch         bytes per frame row, multiple of 16, >= 3*W.
  *  d_windows     device mp_window[n_win], n_win = d_frame_off[F] (read on
  *                device); each window must lie inside the frame, have
@@ -154,7 +158,8 @@ mp_status mp_gather_resize(const uint8_t* const* d_frame_ptrs, int32_t pitch, in
  * box of each tile is staged with ONE 3-D TMA tensor copy (per-class tensor
  * map encoded on the host each call) instead of one bulk copy per row.
  *
- *  d_frames      device, 16-byte aligned.
+ *  d_frames      device-accessible (HBM, or mapped page-locked host memory:
+ *                zero-copy, as in mp_gather_resize), 16-byte aligned.
  *  frame_stride  bytes, multiple of 16, >= H * pitch, < 2^40.
  *  Other arguments as mp_gather_resize.  The workspace is the same.
  */
@@ -189,7 +194,8 @@ typedef enum {
  * Used both for the detector crops and for the full-frame proxy input (a
  * full-frame window whose class has the proxy resolution as out_dims).
  *
- *  d_frames      device, 16-byte aligned; frame f at d_frames + f*frame_stride:
+ *  d_frames      device-accessible (HBM, or mapped page-locked host memory:
+ *                zero-copy), 16-byte aligned; frame f at d_frames + f*frame_stride:
  *                Y plane [H][pitch] then interleaved UV plane [H/2][pitch]
  *                (U at even, V at odd bytes).
  *  frame_stride  bytes, multiple of 16, >= (H + H/2) * pitch, < 2^40.

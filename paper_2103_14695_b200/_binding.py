@@ -136,6 +136,15 @@ def _dev(t, dtype, name):
         raise ValueError(f"{name} must be contiguous")
 
 
+def _frames_ok(frames, what):
+    """Frames may be a CUDA tensor or a page-locked host tensor (zero-copy:
+    the gather reads only the window footprints over PCIe)."""
+    if frames.dtype != torch.uint8 or frames.dim() != 3 or not (frames.is_cuda or frames.is_pinned()):
+        raise ValueError(f"frames must be a uint8 CUDA or pinned host tensor {what}")
+    if frames.stride(2) != 1 or frames.stride(1) != frames.shape[2]:
+        raise ValueError("frames rows must be contiguous with pitch = shape[2]")
+
+
 def _stream(stream):
     s = torch.cuda.current_stream() if stream is None else stream
     return C.c_void_p(s.cuda_stream)
@@ -200,8 +209,8 @@ def mp_gather_workspace_size(out_dims: Sequence, out_cap: Sequence[int]) -> int:
 
 def mp_gather_resize(frame_ptrs, pitch, W, H, F, windows, frame_off, sizes, out_dims, outs, fmt, status, ws,
                      stream=None) -> None:
-    """a5.  frame_ptrs int64 CUDA tensor [F] of device addresses of uint8
-    [H][pitch] frames; outs = list of k class tensors (f32 [cap,3,oh,ow] or
+    """a5.  frame_ptrs int64 CUDA tensor [F] of device-accessible addresses
+    (HBM or pinned host) of uint8 [H][pitch] frames; outs = list of k class tensors (f32 [cap,3,oh,ow] or
     u8 [cap,oh,ow,3]); capacity = outs[k].shape[0]."""
     _dev(frame_ptrs, torch.int64, "frame_ptrs")
     _dev(windows, torch.int32, "windows")
@@ -225,16 +234,14 @@ def mp_gather_resize(frame_ptrs, pitch, W, H, F, windows, frame_off, sizes, out_
 
 def mp_gather_resize_strided(frames, W, H, windows, frame_off, sizes, out_dims, outs, fmt, status, ws,
                              stream=None) -> None:
-    """a5 on a frame batch: frames uint8 CUDA tensor [F, H, pitch] (rows
-    contiguous, pitch % 16 == 0); frame stride taken from the tensor."""
+    """a5 on a frame batch: frames uint8 tensor [F, H, pitch] in HBM or pinned
+    host memory (rows contiguous, pitch % 16 == 0); frame stride taken from
+    the tensor."""
     _dev(windows, torch.int32, "windows")
     _dev(frame_off, torch.int32, "frame_off")
     _dev(status, torch.int32, "status")
     _dev(ws, torch.uint8, "ws")
-    if not frames.is_cuda or frames.dtype != torch.uint8 or frames.dim() != 3:
-        raise ValueError("frames must be a uint8 CUDA tensor [F, H, pitch]")
-    if frames.stride(2) != 1 or frames.stride(1) != frames.shape[2]:
-        raise ValueError("frames rows must be contiguous with pitch = shape[2]")
+    _frames_ok(frames, "[F, H, pitch]")
     F, Hh, pitch = frames.shape
     k = len(sizes)
     if len(outs) != k or len(out_dims) != k:
@@ -253,16 +260,14 @@ def mp_gather_resize_strided(frames, W, H, windows, frame_off, sizes, out_dims, 
 
 def mp_gather_resize_nv12(frames, W, H, windows, frame_off, sizes, out_dims, outs, fmt, status, ws,
                           matrix=MP_BT709_LIMITED, stream=None) -> None:
-    """a5 from NV12 decoder output (NEXT-3, R23): frames uint8 CUDA tensor
+    """a5 from NV12 decoder output (NEXT-3, R23): frames uint8 CUDA (or pinned
+    host, zero-copy) tensor
     [F, H*3/2, pitch] (Y rows then interleaved UV rows, pitch % 16 == 0)."""
     _dev(windows, torch.int32, "windows")
     _dev(frame_off, torch.int32, "frame_off")
     _dev(status, torch.int32, "status")
     _dev(ws, torch.uint8, "ws")
-    if not frames.is_cuda or frames.dtype != torch.uint8 or frames.dim() != 3:
-        raise ValueError("frames must be a uint8 CUDA tensor [F, H*3/2, pitch]")
-    if frames.stride(2) != 1 or frames.stride(1) != frames.shape[2]:
-        raise ValueError("frames rows must be contiguous with pitch = shape[2]")
+    _frames_ok(frames, "[F, H*3/2, pitch]")
     F, rows, pitch = frames.shape
     if rows != int(H) + int(H) // 2:
         raise ValueError("NV12 frames need H*3/2 rows")

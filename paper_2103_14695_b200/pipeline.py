@@ -125,7 +125,9 @@ class WindowPipeline:
         """frames: a uint8 [F, H, pitch] RGB24 batch tensor (TMA tensor path,
         mp_gather_resize_strided), an int64 [F] tensor of RGB24 frame addresses
         (pointer-array path, mp_gather_resize), or, with src="nv12", a uint8
-        [F, H*3/2, pitch] NV12 batch (mp_gather_resize_nv12)."""
+        [F, H*3/2, pitch] NV12 batch (mp_gather_resize_nv12).  Frames may sit
+        in HBM or in pinned host memory: from the host the kernels read only
+        the window footprints over PCIe (zero-copy, same bits)."""
         if self.src == "nv12":
             B.mp_gather_resize_nv12(frames, self.W, self.H, self.windows, self.frame_off, self.sizes,
                                     self.out_dims, self.outs, self.fmt, self.status, self.gather_ws, self.matrix,
@@ -149,11 +151,18 @@ class WindowPipeline:
 
     # ------------------------------------------------------------ helpers
     @staticmethod
-    def frame_ptrs(frames: torch.Tensor) -> torch.Tensor:
-        """Device address of each frame of a uint8 [F,H,pitch] tensor."""
+    def frame_ptrs(frames: torch.Tensor, device=None) -> torch.Tensor:
+        """Address of each frame of a uint8 [F,H,pitch] tensor, as an int64
+        tensor on `device` (default: the frames' device).  Frames in pinned
+        host memory give host addresses the gather reads zero-copy (only the
+        window footprints cross PCIe); their list goes to `device`."""
         F = frames.shape[0]
         step = frames.stride(0) * frames.element_size()
-        return (torch.arange(F, dtype=torch.int64, device=frames.device) * step + frames.data_ptr()).contiguous()
+        if not frames.is_cuda and not frames.is_pinned():
+            raise ValueError("frames must be in HBM or in pinned host memory")
+        dev = frames.device if device is None else torch.device(device)
+        ptrs = torch.arange(F, dtype=torch.int64, device=frames.device) * step + frames.data_ptr()
+        return ptrs.to(dev).contiguous()
 
 
 class PipelinedRunner:

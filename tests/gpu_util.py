@@ -32,11 +32,13 @@ def gpu_plan(W, H, cw, ch, b, sizes, cost, scores, max_windows=None, want_mask=T
 
 
 def gpu_gather(frames_np_or_t, pitch, W, H, windows, sizes, out_dims, caps, fmt=mp.MP_OUT_F32_NCHW,
-               strided=True):
+               strided=True, host=False):
+    """host=True: frames in pinned host memory (zero-copy reads over PCIe)."""
     if isinstance(frames_np_or_t, torch.Tensor):
         fr = frames_np_or_t
     else:
-        fr = torch.from_numpy(np.stack(frames_np_or_t)).to(DEV)
+        fr = torch.from_numpy(np.stack(frames_np_or_t))
+        fr = fr.pin_memory() if host else fr.to(DEV)
     F = fr.shape[0]
     win = np.asarray(windows, np.int32).reshape(-1, 7)
     # a CSR over frames consistent with the (frame-sorted) window list
@@ -56,16 +58,19 @@ def gpu_gather(frames_np_or_t, pitch, W, H, windows, sizes, out_dims, caps, fmt=
     if strided:
         B.mp_gather_resize_strided(fr, W, H, wt, fot, sizes, out_dims, outs, fmt, st, ws)
     else:
-        ptrs = mp.WindowPipeline.frame_ptrs(fr)
+        ptrs = mp.WindowPipeline.frame_ptrs(fr, device=DEV)
         B.mp_gather_resize(ptrs, pitch, W, H, F, wt, fot, sizes, out_dims, outs, fmt, st, ws)
     torch.cuda.synchronize()
     return int(st.item()), [o.cpu().numpy() for o in outs]
 
 
 def gpu_gather_nv12(frames_np_or_t, W, H, windows, sizes, out_dims, caps, fmt=mp.MP_OUT_F32_NCHW,
-                    matrix=mp.MP_BT709_LIMITED):
-    fr = frames_np_or_t if isinstance(frames_np_or_t, torch.Tensor) else \
-        torch.from_numpy(np.stack(frames_np_or_t)).to(DEV)
+                    matrix=mp.MP_BT709_LIMITED, host=False):
+    if isinstance(frames_np_or_t, torch.Tensor):
+        fr = frames_np_or_t
+    else:
+        fr = torch.from_numpy(np.stack(frames_np_or_t))
+        fr = fr.pin_memory() if host else fr.to(DEV)
     F = fr.shape[0]
     win = np.asarray(windows, np.int32).reshape(-1, 7)
     fo = np.searchsorted(win[:, 0], np.arange(F + 1), side="left").astype(np.int32) if len(win) else \
