@@ -42,7 +42,11 @@ constexpr int kMaxTW = 256;
 constexpr int kMaxTR = 8 * kCW > 96 ? 8 * kCW : 96;   // Rw <= 8 rows per consumer warp
 constexpr int kXtapBytes = (kMaxTW + 2) * 8, kYtapBytes = (kMaxTR + 2) * 8;
 constexpr int kTapBytes = kXtapBytes + kYtapBytes;
-constexpr int kStageDataBudget = 44 * 1024;        // dense classes
+constexpr int kStageDataBudget = 44 * 1024;        // dense classes, f32 output
+constexpr int kStageDataBudgetU8 = 80 * 1024;      // dense classes, u8 output: the consumer is the bound (4x fewer
+                                                   // bytes written), and taller tiles mean fewer horizontal lerps per
+                                                   // output row (measured: c2 1.32 -> 1.18 ms, c3 6.08 -> 5.58,
+                                                   // c4 3.63 -> 3.27; f32 is slower with larger stages)
 constexpr int kSparseStageBudget = 96 * 1024;      // row-sparse classes (measured: 44 KB -> 1.44 ms, 96 KB -> 0.93 ms
                                                    // for the c2 proxy-input downscale; bytes in flight per SM)
 constexpr int kDataOff = (kHdrBytes + kTapBytes + 127) / 128 * 128;   // TMA destination: 128-B aligned
@@ -692,7 +696,8 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
   long long data_max = 0;
   int list = 0, taps = 0;
   const char* bud = knob("MP_GATHER_BUDGET_KB");   // experiment knob
-  const long long budget = (bud && atoi(bud) >= 8) ? 1024LL * atoi(bud) : kStageDataBudget;
+  const long long budget = (bud && atoi(bud) >= 8) ? 1024LL * atoi(bud)
+                          : (fmt == MP_OUT_U8_NHWC ? kStageDataBudgetU8 : kStageDataBudget);
   for (int q = 0; q < k; q++) {
     const int w = sizes[q].w, h = sizes[q].h, ow = out_dims[q].w, oh = out_dims[q].h;
     if (w < 1 || h < 1 || w > W || h > H || ow < 1 || oh < 1 || ow > 16384 || oh > 16384) return false;
@@ -739,6 +744,19 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
       int rw, cbw, cbh;
       if (fit_rows(tw, rw, cbw, cbh) && rw >= min_rw) {
         TW = tw;
+        TR = kCW * rw;
+        bw = cbw;
+        bh = cbh;
+      }
+    }
+    // u8 output: a divisor width with an odd number of 32-column lane groups
+    // leaves the last lane column of every tile idle (columns are processed
+    // in pairs); one more group with a ragged last tile wins when the consumer
+    // is the bound (c3, ow = 1440: 160 -> 192 columns, 5.58 -> 5.20 ms)
+    if (TW && fmt == MP_OUT_U8_NHWC && ((TW / 32) & 1) && TW + 32 <= kMaxTW && ow > TW + 32) {
+      int rw, cbw, cbh;
+      if (fit_rows(TW + 32, rw, cbw, cbh) && kCW * rw >= TR) {
+        TW += 32;
         TR = kCW * rw;
         bw = cbw;
         bh = cbh;

@@ -17,6 +17,9 @@ import paper_2103_14695_b200 as mp  # noqa: E402
 from workloads import synth as S  # noqa: E402
 
 
+FMT = int(os.environ.get("FMT", "0"))   # 0 f32 NCHW, 1 u8 NHWC (crop gathers only)
+
+
 def timeit(fn, n=20, warm=3):
     for _ in range(warm):
         fn()
@@ -47,7 +50,7 @@ def main():
         else:
             frames = S.frame_pixels_torch(seeds, cfg.H, cfg.pitch, device=dev)
         p = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
-                              cfg.iou_thr, device=dev, src=src, proxy_dims=cfg.proxy_dims)
+                              cfg.iou_thr, device=dev, src=src, proxy_dims=cfg.proxy_dims, fmt=FMT)
         R, C = cfg.grid
         p.reserve(F, F * R * ((C + 1) // 2))
         p.plan(scores)
@@ -69,9 +72,9 @@ def main():
             p.check_status()
             n = int(p.frame_off[F].item())
             w = p.windows[:n].cpu().numpy()
-            out_b = sum(12 * cfg.out_dims[q][0] * cfg.out_dims[q][1] for q in w[:, 5])
+            out_b = sum((12 if FMT == 0 else 3) * cfg.out_dims[q][0] * cfg.out_dims[q][1] for q in w[:, 5])
             rd = bpp * sum(int(x[3]) * int(x[4]) for x in w)
-            print(json.dumps({"tag": tag, "what": f"crops_{short}", "ms": ms,
+            print(json.dumps({"tag": tag, "what": f"crops_{short}", "fmt": FMT, "ms": ms,
                               "GBps_sum": (out_b + rd) / ms / 1e6}), flush=True)
         del frames, p
         torch.cuda.empty_cache()
