@@ -14,6 +14,8 @@ timeout -s KILL 900 python bench.py > $O/bench_full.log 2>&1
 timeout -s KILL 600 python bench.py --fmt u8 --no-e2e --no-cpu-baseline > $O/bench_u8.log 2>&1
 timeout -s KILL 600 python bench.py --src nv12 > $O/bench_nv12.log 2>&1
 for c in c1_540p c3_1080p_dense c4_4k_drone; do timeout -s KILL 600 python bench.py --config $c --no-e2e --no-cpu-baseline --steps 50 > $O/bench_$c.log 2>&1; done
+for c in c3_1080p_dense c4_4k_drone; do timeout -s KILL 600 python bench.py --config $c --fmt u8 --no-e2e --no-cpu-baseline --steps 50 > $O/bench_u8_$c.log 2>&1; done
+timeout -s KILL 600 python scripts/zero_copy_probe.py > $O/zero_copy_probe.log 2>&1
 timeout -s KILL 600 python bench.py --impl reference --steps 5 --warmup 3 > $O/bench_ref.log 2>&1
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"plan_|gather_|nms_" -c 60 --csv --log-file $O/launches.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --depth 1 > $O/launches_bench.log 2>&1
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:"gather_kernel" -s 3 -c 1 -o $O/prof_gather -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --depth 1 > $O/prof_bench.log 2>&1
