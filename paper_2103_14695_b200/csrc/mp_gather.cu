@@ -18,7 +18,7 @@
 //                        and its source box (ONE 3-D TMA tensor copy over the
 //                        frame batch on the strided entry point, or one 1-D
 //                        bulk copy per source row on the pointer-array entry
-//                        point) land in a 2-stage shared-memory ring completing
+//                        point) land in a 2- or 3-stage shared-memory ring completing
 //                        on an mbarrier (complete_tx).  Warps 0-7 = consumers:
 //                        output columns lane + 32j (packed f32x2 math),
 //                        separable lerps reusing staged rows, streaming stores.
@@ -36,13 +36,17 @@ constexpr int kProducerWarps = 1;
 #endif
 constexpr int kCW = MP_KCW;   // consumer warps per CTA; each owns a block of TR/kCW output rows
 constexpr int kStages = 2;      // default ring depth (A.stages; MP_GATHER_STAGES overrides, <= kMaxStages)
+constexpr int kStagesF32 = 3;   // f32 output: 3 x 40 KB (measured c2 1.424 -> 1.389 ms, c3 6.86 -> 6.35, c4 4.22 -> 4.27
+                                // against 2 x 44 KB; 2 x 40 KB is slower, 1.53)
 constexpr int kMaxStages = 8;
 constexpr int kHdrBytes = 64;
 constexpr int kMaxTW = 256;
 constexpr int kMaxTR = 8 * kCW > 96 ? 8 * kCW : 96;   // Rw <= 8 rows per consumer warp
 constexpr int kXtapBytes = (kMaxTW + 2) * 8, kYtapBytes = (kMaxTR + 2) * 8;
 constexpr int kTapBytes = kXtapBytes + kYtapBytes;
-constexpr int kStageDataBudget = 44 * 1024;        // dense classes, f32 output
+constexpr int kStageDataBudget = 40 * 1024;        // dense classes, RGB f32 output (three stages, kStagesF32)
+constexpr int kStageDataBudgetNV12 = 44 * 1024;    // dense classes, NV12 f32 output (two stages: 3 x 40 KB measured
+                                                   // 1.311 -> 1.346 ms on c2)
 constexpr int kStageDataBudgetU8 = 80 * 1024;      // dense classes, u8 output: the consumer is the bound (4x fewer
                                                    // bytes written), and taller tiles mean fewer horizontal lerps per
                                                    // output row (measured: c2 1.32 -> 1.18 ms, c3 6.08 -> 5.58,
@@ -697,7 +701,8 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
   int list = 0, taps = 0;
   const char* bud = knob("MP_GATHER_BUDGET_KB");   // experiment knob
   const long long budget = (bud && atoi(bud) >= 8) ? 1024LL * atoi(bud)
-                          : (fmt == MP_OUT_U8_NHWC ? kStageDataBudgetU8 : kStageDataBudget);
+                          : (fmt == MP_OUT_U8_NHWC ? kStageDataBudgetU8
+                                                   : (src == kSrcNV12 ? kStageDataBudgetNV12 : kStageDataBudget));
   for (int q = 0; q < k; q++) {
     const int w = sizes[q].w, h = sizes[q].h, ow = out_dims[q].w, oh = out_dims[q].h;
     if (w < 1 || h < 1 || w > W || h > H || ow < 1 || oh < 1 || ow > 16384 || oh > 16384) return false;
@@ -869,8 +874,10 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
   const char* wm = knob("MP_GATHER_WAIT");   // experiment knob
   A.wait_mode = wm ? atoi(wm) : 3;
   const char* stg = knob("MP_GATHER_STAGES");   // experiment knob
-  A.stages = stg ? atoi(stg) : kStages;
+  A.stages = stg ? atoi(stg) : (fmt == MP_OUT_F32_NCHW && A.src == kSrcRGB24 ? kStagesF32 : kStages);
   if (A.stages < 2 || A.stages > kMaxStages) A.stages = kStages;
+  // fewer stages when the deepest ring does not fit (row-sparse classes stage 96 KB)
+  while (A.stages > 2 && (size_t)A.stages * A.stage_bytes + 2 * A.stages * sizeof(uint64_t) > 227 * 1024) A.stages--;
   const size_t smem = (size_t)A.stages * A.stage_bytes + 2 * A.stages * sizeof(uint64_t);
   if (smem > 227 * 1024) return MP_ERR_UNSUPPORTED;
   int dev = 0, sms = 0, per_sm = 0;
