@@ -872,7 +872,10 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
   MP_CUDA_TRY(cudaGetLastError());
   if (A.F == 0) return MP_OK;
   const char* wm = knob("MP_GATHER_WAIT");   // experiment knob
-  A.wait_mode = wm ? atoi(wm) : 3;
+  // default: plain try_wait loops (no suspend hint) — same-box A/B against
+  // sleeping waits: c2 f32 alone 1.387 -> 1.374 ms, pipelined step 1.547 ->
+  // 1.533 ms; u8 1.182 -> 1.175 ms; c4 unchanged
+  A.wait_mode = wm ? atoi(wm) : 0;
   const char* stg = knob("MP_GATHER_STAGES");   // experiment knob
   A.stages = stg ? atoi(stg) : (fmt == MP_OUT_F32_NCHW && A.src == kSrcRGB24 ? kStagesF32 : kStages);
   if (A.stages < 2 || A.stages > kMaxStages) A.stages = kStages;
