@@ -384,3 +384,65 @@ def test_pipelined_runner_with_graphs_parity(G):
             caps1 = [1 if qq == q else 0 for qq in range(len(cfg.sizes))]
             st, o = O.gather_resize([fr], cfg.pitch, cfg.W, cfg.H, one[None], cfg.sizes, cfg.out_dims, caps1)
             assert np.abs(p.outs[q][slot].cpu().numpy() - o[q][0]).max() <= F32_TOL
+
+
+@pytest.mark.parametrize("fmt", [0, 1], ids=["f32", "u8"])
+@pytest.mark.parametrize("name", ["c3_1080p_dense", "c4_4k_drone"])
+def test_full_size_pipelined_parity(G, name, fmt):
+    """configs[2] and configs[3] at full size in the launch configuration
+    bench.py times for them (PipelinedRunner: 3 streams, 2 buffer sets,
+    plan/merge as CUDA graphs, several steps): windows and kept boxes
+    bit-exact against the oracle, pixels on a seeded sample of windows
+    (f32 within 1e-3, u8 within 1 LSB)."""
+    import paper_2103_14695_b200 as mp
+    cfg = S.CONFIGS[name]
+    F = cfg.frames
+    clip = 5
+    scene = S.make_scene(cfg, clip, F)
+    scores = S.score_grids(cfg, clip, scene)
+    ref = O.plan_windows(cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores)
+    boxes, wbo = S.standin_boxes(cfg, clip, scene, ref["windows"])
+    r = O.remap_nms(boxes, wbo, ref["windows"], ref["frame_off"], cfg.out_dims, cfg.W, cfg.H, cfg.score_thr,
+                    cfg.iou_thr)
+    caps = [int(c) for c in ref["class_count"]]
+    n = len(ref["windows"])
+    pipes = []
+    for _ in range(2):
+        p = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
+                              cfg.iou_thr, fmt=fmt, device=G.DEV)
+        p.reserve(F, n, caps=caps, max_boxes=max(len(boxes), 1))
+        pipes.append(p)
+    runner = mp.PipelinedRunner(pipes, device=G.DEV)
+    sc = torch.from_numpy(scores).to(G.DEV)
+    bt = G.boxes_to_t(boxes)
+    wt = torch.from_numpy(wbo).to(G.DEV)
+    frames = S.frame_pixels_torch([S.frame_seed(clip, f) for f in range(F)], cfg.H, cfg.pitch, device=G.DEV)
+    runner.capture_graphs(sc, bt, wt)
+    for _ in range(4):
+        runner.step(sc, frames, bt, wt)
+    runner.wait_all()
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(17)
+    sample = rng.choice(n, size=min(12, n), replace=False)
+    for p in pipes:
+        p.check_status()
+        assert np.array_equal(p.frame_off.cpu().numpy(), ref["frame_off"])
+        assert np.array_equal(p.windows[:n].cpu().numpy(), ref["windows"])
+        nk = int(p.nms_frame_off[F].item())
+        assert np.array_equal(p.nms_frame_off.cpu().numpy(), r["frame_off"])
+        assert np.array_equal(p.nms_src[:nk].cpu().numpy(), r["src"])
+        assert np.array_equal(p.nms_out[:nk].cpu().numpy().view(np.uint32),
+                              r["boxes"].view(np.float32).reshape(-1, 6).view(np.uint32))
+        for wi in sample:
+            w = ref["windows"][wi].copy()
+            f, q, slot = int(w[0]), int(w[5]), int(w[6])
+            fr = S.frame_pixels_np(S.frame_seed(clip, f), cfg.H, cfg.pitch)
+            one = w.copy(); one[0] = 0; one[6] = 0
+            caps1 = [1 if qq == q else 0 for qq in range(len(cfg.sizes))]
+            st, o = O.gather_resize([fr], cfg.pitch, cfg.W, cfg.H, one[None], cfg.sizes, cfg.out_dims, caps1,
+                                    O.F32_NCHW if fmt == 0 else O.U8_NHWC)
+            got = p.outs[q][slot].cpu().numpy()
+            if fmt == 0:
+                assert np.abs(got.astype(np.float64) - o[q][0]).max() <= F32_TOL, (wi, q)
+            else:
+                assert np.abs(got.astype(np.int32) - o[q][0].astype(np.int32)).max() <= 1, (wi, q)
