@@ -31,6 +31,10 @@
 namespace mpk {
 
 constexpr int kProducerWarps = 1;
+#ifndef MP_TILE_CHUNK
+#define MP_TILE_CHUNK 2
+#endif
+constexpr int kTileChunk = MP_TILE_CHUNK;   // tiles per dynamic-scheduling ticket
 #ifndef MP_KCW
 #define MP_KCW 8
 #endif
@@ -407,7 +411,7 @@ template <int FMT, int SRC>
 __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(const __grid_constant__ GatherArgs A,
                                                                  const __grid_constant__ TmapArray tm,
                                                                  const uint8_t* const* __restrict__ frames,
-                                                                 const int* __restrict__ ws_cnt,
+                                                                 int* __restrict__ ws_cnt,
                                                                  const int* __restrict__ ws_list,
                                                                  const mp_window* __restrict__ windows,
                                                                  const int* __restrict__ frame_off,
@@ -479,16 +483,43 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
       rlo = __ldg(&ws_tap[A.ytab_off[ti.q] + ti.oy0].x);
       rhi = __ldg(&ws_tap[A.ytab_off[ti.q] + ti.oy0 + ti.rows - 1].x);
     };
-    if (blockIdx.x < T) {
-      decode(blockIdx.x, cur);
+    // Dynamic tile scheduling: CTA b takes tile b first, then the next free
+    // tile from a global counter (ticket G + n), claimed one tile ahead so the
+    // atomic's latency overlaps the current tile.  Tiles are still handed out
+    // in order (concurrently processed tiles stay neighbours in the frames and
+    // outputs), but a CTA whose SM also runs plan/NMS blocks of neighbouring
+    // batches simply takes fewer tiles instead of finishing last.
+    // Tickets hand out chunks of kTileChunk consecutive tiles; the next
+    // chunk's ticket is claimed when a chunk is opened, so the atomic has
+    // kTileChunk tiles of time to return (one tile was not enough for the
+    // small c2 tiles: 1.37 -> 1.47 ms).  Measured against the former static
+    // round-robin (same box, alone): chunks of 2: c2 1.383 -> 1.360 ms, c3
+    // 6.61 -> 6.49, c4 4.15 -> 4.00; chunks of 4 / 8 balance less well.
+    int* tile_ctr = ws_cnt + kMaxClasses;
+    int ticket = 0, cbase = 0, cleft = 0;   // ticket: lane 0's in-flight atomic
+    if (lane == 0) ticket = atomicAdd(tile_ctr, 1);
+    auto next_tile = [&]() -> int {
+      if (cleft == 0) {
+        cbase = G + __shfl_sync(0xffffffffu, ticket, 0) * kTileChunk;
+        cleft = kTileChunk;
+        if (lane == 0) ticket = atomicAdd(tile_ctr, 1);
+      }
+      cleft--;
+      return cbase++;
+    };
+    int t = blockIdx.x;
+    int tn = T;
+    if (t < T) {
+      decode(t, cur);
       prefetch(cur, dcur, clo_cur, rlo_cur, rhi_cur);
+      tn = next_tile();
     }
     for (int i = 0;; i++) {
-      const int t = blockIdx.x + i * G;   // round-robin: concurrently processed tiles are
-      if (t >= T) break;                   // neighbours in the frames and in the outputs
       const int s = i % nst;
-      if (t + G < T) {
-        decode(t + G, nxt);
+      // the next tile's descriptor loads are issued before the wait for a
+      // free stage, so their latency hides behind it
+      if (tn < T) {
+        decode(tn, nxt);
         prefetch(nxt, dnxt, clo_nxt, rlo_nxt, rhi_nxt);
       }
       if (i >= nst) {
@@ -497,6 +528,13 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
       }
       unsigned char* stage = smem + (size_t)s * A.stage_bytes;
       TileHdr* hdr = reinterpret_cast<TileHdr*>(stage);
+      if (t >= T) {   // no tile left: an end marker releases the consumers
+        if (lane == 0) {
+          hdr->valid = -1;
+          mbar_arrive(&full[s]);
+        }
+        break;
+      }
       unsigned char* xt = stage + kHdrBytes;
       unsigned char* yt = stage + kHdrBytes + kXtapBytes;
       unsigned char* data = stage + kDataOff;
@@ -604,19 +642,20 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
       clo_cur = clo_nxt;
       rlo_cur = rlo_nxt;
       rhi_cur = rhi_nxt;
+      t = tn;
+      tn = tn < T ? next_tile() : T;
     }
     return;
   }
 
   // ===================== consumer warps =====================
   for (int i = 0;; i++) {
-    const int t = blockIdx.x + i * G;
-    if (t >= T) break;
     const int s = i % nst;
     if (A.wait_mode & 2) mbar_wait_sleep(&full[s], (i / nst) & 1);
     else mbar_wait(&full[s], (i / nst) & 1);
     const unsigned int soff = (unsigned int)s * (unsigned int)A.stage_bytes;
     const TileHdr* hdr = reinterpret_cast<const TileHdr*>(&smem[soff]);
+    if (hdr->valid < 0) break;   // end marker
     if (hdr->valid && A.debug != 1) {
       switch (A.ncol[hdr->k]) {
         case 2: consume_tile<FMT, 2, SRC>(A, hdr, soff, wid, lane); break;
@@ -867,7 +906,7 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
   int* ws_cnt = (int*)(ws + L.cnt_off);
   int* ws_list = (int*)(ws + L.list_off);
   int2* ws_tap = (int2*)(ws + L.tap_off);
-  MP_CUDA_TRY(cudaMemsetAsync(ws_cnt, 0, kMaxClasses * sizeof(int), s));
+  MP_CUDA_TRY(cudaMemsetAsync(ws_cnt, 0, (kMaxClasses + 1) * sizeof(int), s));   // class counts + tile counter
   gather_prep_kernel<<<256, kPrepThreads, 0, s>>>(A, d_windows, d_frame_off, ws_cnt, ws_list, ws_tap, n_taps, d_status);
   MP_CUDA_TRY(cudaGetLastError());
   if (A.F == 0) return MP_OK;
