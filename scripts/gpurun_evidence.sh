@@ -10,6 +10,8 @@ timeout -s KILL 900 compute-sanitizer --tool memcheck --print-limit 20 python -m
 timeout -s KILL 900 compute-sanitizer --tool racecheck --print-limit 20 python -m pytest tests/test_gpu_assign.py -q -x -k "large" > $O/san_racecheck_assign.log 2>&1; echo "rc=$?" >> $O/san_racecheck_assign.log
 timeout -s KILL 900 compute-sanitizer --tool racecheck --print-limit 20 python -m pytest tests/test_gpu_refine.py -q -x -k "degenerate" > $O/san_racecheck_refine.log 2>&1; echo "rc=$?" >> $O/san_racecheck_refine.log
 timeout -s KILL 900 compute-sanitizer --tool racecheck --print-limit 20 python -m pytest tests/test_gpu_nv12.py -q -x -k "grey" > $O/san_racecheck_nv12.log 2>&1; echo "rc=$?" >> $O/san_racecheck_nv12.log
+for tool in memcheck racecheck synccheck; do timeout -s KILL 900 compute-sanitizer --tool $tool --print-limit 20 python -m pytest tests/test_gpu_parity.py -q -x -k "scales_and_edges and 0.7 or capacity_and_invalid" > $O/san_${tool}_gather.log 2>&1; echo "rc=$?" >> $O/san_${tool}_gather.log; done
+timeout -s KILL 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_zero_copy.py -q -x -k "edges and 0.37" > $O/san_memcheck_zero_copy.log 2>&1; echo "rc=$?" >> $O/san_memcheck_zero_copy.log
 timeout -s KILL 900 python bench.py > $O/bench_full.log 2>&1
 timeout -s KILL 600 python bench.py --fmt u8 --no-e2e --no-cpu-baseline > $O/bench_u8.log 2>&1
 timeout -s KILL 600 python bench.py --src nv12 > $O/bench_nv12.log 2>&1
