@@ -426,7 +426,12 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
   if (tid == 0) {
     for (int s = 0; s < nst; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kCW);
+      // every consumer thread releases the stage it read: with one arrive per
+      // warp after __syncwarp, racecheck cannot see lanes 1-31's header reads
+      // ordered before the producer's next write of that stage (the end
+      // marker) and reports a hazard; 32 arrives per warp cost <1 % (c2 f32
+      // 1.358 -> 1.368 ms, u8 1.176 -> 1.162)
+      mbar_init(&empty[s], kCW * 32);
     }
     fence_mbar_init();
   }
@@ -664,8 +669,7 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
         default: consume_tile<FMT, 8, SRC>(A, hdr, soff, wid, lane); break;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    mbar_arrive(&empty[s]);
   }
 }
 
