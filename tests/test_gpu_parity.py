@@ -446,3 +446,44 @@ def test_full_size_pipelined_parity(G, name, fmt):
                 assert np.abs(got.astype(np.float64) - o[q][0]).max() <= F32_TOL, (wi, q)
             else:
                 assert np.abs(got.astype(np.int32) - o[q][0].astype(np.int32)).max() <= 1, (wi, q)
+
+
+def test_gather_zero_windows_and_repeated_calls(G):
+    """The persistent gather with no tiles at all (every CTA only sees the end
+    marker), and the same call repeated on one workspace (the dynamic tile
+    counter is reset by every call): identical results each time."""
+    import paper_2103_14695_b200 as mp
+    from paper_2103_14695_b200 import _binding as B
+    W, H = 320, 180
+    pitch = (3 * W + 15) // 16 * 16
+    frames = torch.from_numpy(np.stack([S.frame_pixels_np(S.frame_seed(31, f), H, pitch) for f in range(3)]))
+    frames = frames.to(G.DEV)
+    sizes, out_dims = [(64, 64), (320, 180)], [(48, 48), (240, 135)]
+    st, got = G.gpu_gather(frames, pitch, W, H, np.zeros((0, 7), np.int32), sizes, out_dims, [0, 0])
+    assert st == 0
+    win = np.array([[f, 16 * f, 8 * f, 64, 64, 0, f] for f in range(3)] + [[1, 0, 0, 320, 180, 1, 0]], np.int32)
+    win = win[np.argsort(win[:, 0], kind="stable")]
+    caps = [3, 1]
+    fo = np.searchsorted(win[:, 0], np.arange(4), side="left").astype(np.int32)
+    wt = torch.from_numpy(win).to(G.DEV)
+    fot = torch.from_numpy(fo).to(G.DEV)
+    outs = [torch.full((caps[q], 3, oh, ow), -1.0, dtype=torch.float32, device=G.DEV)
+            for q, (ow, oh) in enumerate(out_dims)]
+    status = torch.zeros(1, dtype=torch.int32, device=G.DEV)
+    ws = torch.empty(B.mp_gather_workspace_size(out_dims, caps), dtype=torch.uint8, device=G.DEV)
+    first = None
+    for _ in range(4):
+        for o in outs:
+            o.fill_(-1.0)
+        B.mp_gather_resize_strided(frames, W, H, wt, fot, sizes, out_dims, outs, mp.MP_OUT_F32_NCHW, status, ws)
+        torch.cuda.synchronize()
+        assert int(status.item()) == 0
+        cur = [o.cpu().numpy() for o in outs]
+        if first is None:
+            first = cur
+            st_r, ref = O.gather_resize([f.cpu().numpy() for f in frames], pitch, W, H, win, sizes, out_dims, caps)
+            for q in range(2):
+                assert np.abs(cur[q].astype(np.float64) - ref[q]).max() <= F32_TOL
+        else:
+            for a, b in zip(first, cur):
+                assert np.array_equal(a, b)
