@@ -49,6 +49,7 @@ constexpr int kMaxTR = 8 * kCW > 96 ? 8 * kCW : 96;   // Rw <= 8 rows per consum
 constexpr int kXtapBytes = (kMaxTW + 2) * 8, kYtapBytes = (kMaxTR + 2) * 8;
 constexpr int kTapBytes = kXtapBytes + kYtapBytes;
 constexpr int kStageDataBudget = 40 * 1024;        // dense classes, RGB f32 output (three stages, kStagesF32)
+constexpr int kStageDataBudgetWide = 56 * 1024;    // RGB f32 classes with ow > 512 (full-frame windows)
 constexpr int kStageDataBudgetNV12 = 44 * 1024;    // dense classes, NV12 f32 output (two stages: 3 x 40 KB measured
                                                    // 1.311 -> 1.346 ms on c2)
 constexpr int kStageDataBudgetU8 = 80 * 1024;      // dense classes, u8 output: the consumer is the bound (4x fewer
@@ -771,7 +772,12 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
     // downscale, NEXT-3).  No halo rows, so short (Rw = 1) tiles are fine.
     const bool sparse = allow_sparse && h > 2 * oh;
     const int min_rw = sparse ? 1 : 3;
-    const long long cbudget = (sparse && !bud) ? (long long)kSparseStageBudget : budget;
+    // RGB f32 classes wider than 512 output columns (the full-frame fallback
+    // windows of dense scenes) stage taller tiles: the ring's stage size is
+    // the largest class's, and the narrow classes keep their 40-KB geometry
+    const long long cbudget = (sparse && !bud) ? (long long)kSparseStageBudget
+                              : (!bud && fmt == MP_OUT_F32_NCHW && src == kSrcRGB24 && ow > 512)
+                                    ? (long long)kStageDataBudgetWide : budget;
     int TW = 0, TR = 0, bw = 0, bh = 0;
     auto fit_rows = [&](int tw, int& rw, int& cbw, int& cbh) {
       for (rw = 8; rw >= 1; rw--) {
