@@ -894,7 +894,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-e2e-staged", action="store_true", help="skip the whole-frame-copy e2e variant")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--depth", type=int, default=2, help="batches in flight (buffer sets) in the stream pipeline")
+    ap.add_argument("--depth", type=int, default=3, help="batches in flight (buffer sets) in the stream pipeline")
     ap.add_argument("--graphs", type=int, default=1, help="replay plan/merge as CUDA graphs")
     ap.add_argument("--merge-on-gather", type=int, default=0,
                     help="run remap/NMS on the gather stream right after the gather (no co-running)")
