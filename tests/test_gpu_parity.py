@@ -337,9 +337,10 @@ def test_full_size_bench_config_parity(G):
         assert np.abs(got - o[q][0]).max() <= F32_TOL, (wi, np.abs(got - o[q][0]).max())
 
 
-def test_pipelined_runner_with_graphs_parity(G):
+@pytest.mark.parametrize("depth", [2, 3])
+def test_pipelined_runner_with_graphs_parity(G, depth):
     """The launch configuration bench.py times: PipelinedRunner, 3 streams,
-    2 buffer sets, plan/merge replayed as CUDA graphs — windows, kept boxes
+    2 or 3 buffer sets (bench default 3), plan/merge replayed as CUDA graphs — windows, kept boxes
     (bit-exact) and sampled pixels equal the oracle's after several steps."""
     import paper_2103_14695_b200 as mp
     cfg = S.CONFIGS["c1_540p"]
@@ -353,7 +354,7 @@ def test_pipelined_runner_with_graphs_parity(G):
     caps = [int(c) for c in ref["class_count"]]
     n = len(ref["windows"])
     pipes = []
-    for _ in range(2):
+    for _ in range(depth):
         p = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
                               cfg.iou_thr, device=G.DEV)
         p.reserve(F, n, caps=caps, max_boxes=max(len(boxes), 1))
@@ -390,7 +391,7 @@ def test_pipelined_runner_with_graphs_parity(G):
 @pytest.mark.parametrize("name", ["c3_1080p_dense", "c4_4k_drone"])
 def test_full_size_pipelined_parity(G, name, fmt):
     """configs[2] and configs[3] at full size in the launch configuration
-    bench.py times for them (PipelinedRunner: 3 streams, 2 buffer sets,
+    bench.py times for them (PipelinedRunner: 3 streams, 3 buffer sets,
     plan/merge as CUDA graphs, several steps): windows and kept boxes
     bit-exact against the oracle, pixels on a seeded sample of windows
     (f32 within 1e-3, u8 within 1 LSB)."""
@@ -407,7 +408,7 @@ def test_full_size_pipelined_parity(G, name, fmt):
     caps = [int(c) for c in ref["class_count"]]
     n = len(ref["windows"])
     pipes = []
-    for _ in range(2):
+    for _ in range(3):   # bench.py's default --depth
         p = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
                               cfg.iou_thr, fmt=fmt, device=G.DEV)
         p.reserve(F, n, caps=caps, max_boxes=max(len(boxes), 1))
