@@ -328,7 +328,8 @@ def run_b200(args):
                                cfg.iou_thr, fmt=fmt, device=dev, **pkw)
         p2.reserve(F, n_win, caps=counts, max_boxes=max(len(boxes), 1))
         pipes.append(p2)
-    runner = mp.PipelinedRunner(pipes, device=dev, merge_on_gather_stream=bool(args.merge_on_gather))
+    runner = mp.PipelinedRunner(pipes, device=dev, merge_on_gather_stream=bool(args.merge_on_gather),
+                                side_streams=args.side_streams)
     stream = torch.cuda.current_stream(dev)
     if args.graphs:
         runner.capture_graphs(scores, boxes_t, wbo_t)
@@ -352,7 +353,8 @@ def run_b200(args):
         dist.barrier()
     torch.cuda.synchronize()
     t0.record(stream)
-    runner.s_plan.wait_stream(stream)
+    for sp in runner.s_plans:
+        sp.wait_stream(stream)
     if runner.s_proxy is not None:
         runner.s_proxy.wait_stream(stream)
     h0 = time.perf_counter()
@@ -438,7 +440,8 @@ def run_b200(args):
                        "raw_boxes_per_step": int(len(boxes)), "kept_boxes_per_step": n_kept,
                        "l2": l2_note,
                        "parallelism": f"clip-sharded x{world}",
-                       "pipeline": f"plan/gather/merge on 3 CUDA streams, {args.depth} buffer sets, "
+                       "pipeline": f"plan/gather/merge on {1 + 2 * len(runner.s_plans)} CUDA streams, "
+                                   f"{args.depth} buffer sets, "
                                    f"plan/merge as CUDA graphs: {bool(args.graphs)}"},
             "roofline": {"bound": "hbm", "kernel": "gather_resize (prep + gather_kernel)",
                          "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
@@ -896,6 +899,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=3, help="batches in flight (buffer sets) in the stream pipeline")
     ap.add_argument("--graphs", type=int, default=1, help="replay plan/merge as CUDA graphs")
+    ap.add_argument("--side-streams", type=int, default=1,
+                    help="plan and remap/NMS streams (batches of different buffer sets overlap when > 1)")
     ap.add_argument("--merge-on-gather", type=int, default=0,
                     help="run remap/NMS on the gather stream right after the gather (no co-running)")
     ap.add_argument("--src", default="rgb24", choices=["rgb24", "nv12"],

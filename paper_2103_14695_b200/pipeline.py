@@ -180,16 +180,23 @@ class PipelinedRunner:
         plan(i) -> gather(i) -> [detector] -> merge(i);  plan(i) waits merge(i-depth).
     """
 
-    def __init__(self, pipes, device="cuda", merge_on_gather_stream: bool = False):
+    def __init__(self, pipes, device="cuda", merge_on_gather_stream: bool = False, side_streams: int = 1):
         self.pipes = list(pipes)
         self.depth = len(self.pipes)
         dev = torch.device(device)
-        self.s_plan = torch.cuda.Stream(dev)
+        # side_streams > 1: plan and remap/NMS of consecutive batches run on
+        # their own streams (set k uses stream k mod side_streams), so the
+        # plans (and merges) of two batches may overlap each other — their
+        # latency beside the persistent gather then no longer caps the step
+        n = max(1, min(int(side_streams), self.depth))
+        self.s_plans = [torch.cuda.Stream(dev) for _ in range(n)]
+        self.s_plan = self.s_plans[0]
         self.s_gather = torch.cuda.Stream(dev)
         # merge_on_gather_stream: remap/NMS(i) runs right after gather(i) on the
         # gather stream instead of concurrently with gather(i+1) (the persistent
         # gather leaves co-running latency-bound kernels little of each SM)
-        self.s_merge = self.s_gather if merge_on_gather_stream else torch.cuda.Stream(dev)
+        self.s_merges = [self.s_gather] if merge_on_gather_stream else [torch.cuda.Stream(dev) for _ in range(n)]
+        self.s_merge = self.s_merges[0]
         self.s_proxy = torch.cuda.Stream(dev) if self.pipes[0].proxy_dims else None
         self.done = [None] * self.depth
         self.i = 0
@@ -200,15 +207,16 @@ class PipelinedRunner:
         replays them.  The gather stays a plain launch (2 kernels) so its
         duration can be timed with events on its stream."""
         self.g_plan, self.g_merge = [], []
-        for p in self.pipes:
+        for k, p in enumerate(self.pipes):
+            sp, sm = self.s_plans[k % len(self.s_plans)], self.s_merges[k % len(self.s_merges)]
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=self.s_plan):
-                p.plan(scores, stream=self.s_plan)
+            with torch.cuda.graph(g, stream=sp):
+                p.plan(scores, stream=sp)
             self.g_plan.append(g)
             if boxes is not None:
                 g2 = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g2, stream=self.s_merge):
-                    p.merge(boxes, win_box_off, stream=self.s_merge)
+                with torch.cuda.graph(g2, stream=sm):
+                    p.merge(boxes, win_box_off, stream=sm)
                 self.g_merge.append(g2)
         torch.cuda.synchronize()
 
@@ -219,8 +227,10 @@ class PipelinedRunner:
         proxy-input downscale on their streams."""
         k = self.i % self.depth
         p = self.pipes[k]
+        s_plan = self.s_plans[k % len(self.s_plans)]
+        s_merge = self.s_merges[k % len(self.s_merges)]
         if self.done[k] is not None:
-            self.s_plan.wait_event(self.done[k])
+            s_plan.wait_event(self.done[k])
         if self.s_proxy is not None:
             if self.done[k] is not None:
                 self.s_proxy.wait_event(self.done[k])
@@ -231,14 +241,14 @@ class PipelinedRunner:
                 proxy_events[1].record(self.s_proxy)
             downscaled = torch.cuda.Event()
             downscaled.record(self.s_proxy)
-            self.s_plan.wait_event(downscaled)
+            s_plan.wait_event(downscaled)
         if getattr(self, "g_plan", None):
-            with torch.cuda.stream(self.s_plan):
+            with torch.cuda.stream(s_plan):
                 self.g_plan[k].replay()
         else:
-            p.plan(scores, stream=self.s_plan)
+            p.plan(scores, stream=s_plan)
         planned = torch.cuda.Event()
-        planned.record(self.s_plan)
+        planned.record(s_plan)
         self.s_gather.wait_event(planned)
         if gather_events is not None:
             gather_events[0].record(self.s_gather)
@@ -247,15 +257,15 @@ class PipelinedRunner:
             gather_events[1].record(self.s_gather)
         gathered = torch.cuda.Event()
         gathered.record(self.s_gather)
-        self.s_merge.wait_event(gathered)
+        s_merge.wait_event(gathered)
         if boxes is not None:
             if getattr(self, "g_merge", None):
-                with torch.cuda.stream(self.s_merge):
+                with torch.cuda.stream(s_merge):
                     self.g_merge[k].replay()
             else:
-                p.merge(boxes, win_box_off, stream=self.s_merge)
+                p.merge(boxes, win_box_off, stream=s_merge)
         done = torch.cuda.Event()
-        done.record(self.s_merge)
+        done.record(s_merge)
         self.done[k] = done
         self.i += 1
         return p
