@@ -57,14 +57,15 @@ int main(void) {
   size_t ws = mp_plan_workspace_size(&p, F);
   EXPECT(ws > 0);
   CK(cudaMalloc((void**)&d_scores, sizeof(h_scores)));
-  CK(cudaMalloc((void**)&d_win, 16 * sizeof(mp_window)));
+  enum { MAXW = 16 };   /* window buffer capacity */
+  CK(cudaMalloc((void**)&d_win, MAXW * sizeof(mp_window)));
   CK(cudaMalloc((void**)&d_fo, (F + 1) * sizeof(int32_t)));
   CK(cudaMalloc((void**)&d_cc, 2 * sizeof(int32_t)));
   CK(cudaMalloc((void**)&d_st, sizeof(int32_t)));
   CK(cudaMalloc(&d_ws, ws));
   CK(cudaMemcpy(d_scores, h_scores, sizeof(h_scores), cudaMemcpyHostToDevice));
   CK(cudaMemset(d_st, 0, sizeof(int32_t)));
-  MP(mp_plan_windows(&p, d_scores, F, NULL, d_win, 16, d_fo, d_cc, d_st, d_ws, ws, NULL));
+  MP(mp_plan_windows(&p, d_scores, F, NULL, d_win, MAXW, d_fo, d_cc, d_st, d_ws, ws, NULL));
   mp_window h_win[16];
   int32_t h_fo[2], h_cc[2], h_st;
   CK(cudaMemcpy(h_fo, d_fo, sizeof(h_fo), cudaMemcpyDeviceToHost));
@@ -91,8 +92,8 @@ int main(void) {
   size_t gws = mp_gather_workspace_size(2, out_dims, caps);
   void* d_gws;
   CK(cudaMalloc(&d_gws, gws));
-  MP(mp_gather_resize_strided(d_frame, (int64_t)H * pitch, pitch, W, H, F, d_win, d_fo, 2, sizes, out_dims, outs,
-                              caps, MP_OUT_F32_NCHW, d_st, d_gws, gws, NULL));
+  MP(mp_gather_resize_strided(d_frame, (int64_t)H * pitch, pitch, W, H, F, d_win, d_fo, MAXW, 2, sizes, out_dims,
+                              outs, caps, MP_OUT_F32_NCHW, d_st, d_gws, gws, NULL));
   float h_out[3 * 32 * 32];
   CK(cudaMemcpy(h_out, d_out0, sizeof(h_out), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(&h_st, d_st, sizeof(h_st), cudaMemcpyDeviceToHost));
@@ -117,7 +118,7 @@ int main(void) {
   size_t nws = mp_remap_nms_workspace_size(F, 3);
   void* d_nws;
   CK(cudaMalloc(&d_nws, nws));
-  MP(mp_remap_nms(d_boxes, d_wbo, d_win, d_fo, F, 2, out_dims, W, H, 0.25f, 0.5f, d_keep, d_src, 3, d_kfo, d_st, 3,
+  MP(mp_remap_nms(d_boxes, d_wbo, d_win, d_fo, MAXW, F, 2, out_dims, W, H, 0.25f, 0.5f, d_keep, d_src, 3, d_kfo, d_st, 3,
                   d_nws, nws, NULL));
   mp_box h_keep[3];
   int32_t h_src[3], h_kfo[2];

@@ -133,8 +133,13 @@ size_t mp_gather_workspace_size(int32_t k, const mp_size* out_dims, const int32_
  *                only the window footprints over PCIe (zero-copy; bit-identical
  *                results, no staging copy of the whole frame).
  *  pitch         bytes per frame row, multiple of 16, >= 3*W.
- *  d_windows     device mp_window[n_win], n_win = d_frame_off[F] (read on
- *                device); each window must lie inside the frame, have
+ *  d_windows     device mp_window[max_windows]; the windows gathered are the
+ *                first n_win = min(d_frame_off[F], max_windows) (read on
+ *                device).  d_frame_off[F] > max_windows (a plan that overflowed
+ *                this buffer reports its true total) sets *d_status =
+ *                MP_ERR_CAPACITY; the records in the buffer are still gathered
+ *                and nothing past the buffer is read.
+ *                Each window must lie inside the frame, have
  *                (w,h) == sizes[size_idx], and slots of a class must be
  *                0..count-1 (as mp_plan_windows produces; violations set
  *                *d_status = MP_ERR_INVALID and skip the window).
@@ -146,7 +151,7 @@ size_t mp_gather_workspace_size(int32_t k, const mp_size* out_dims, const int32_
  */
 mp_status mp_gather_resize(const uint8_t* const* d_frame_ptrs, int32_t pitch, int32_t W,
                            int32_t H, int32_t F, const mp_window* d_windows,
-                           const int32_t* d_frame_off, int32_t k, const mp_size* sizes,
+                           const int32_t* d_frame_off, int32_t max_windows, int32_t k, const mp_size* sizes,
                            const mp_size* out_dims, void* const* d_out, const int32_t* out_cap,
                            mp_out_format fmt, int32_t* d_status, void* d_ws, size_t ws_bytes,
                            void* stream);
@@ -165,7 +170,7 @@ mp_status mp_gather_resize(const uint8_t* const* d_frame_ptrs, int32_t pitch, in
  */
 mp_status mp_gather_resize_strided(const uint8_t* d_frames, int64_t frame_stride, int32_t pitch, int32_t W,
                                    int32_t H, int32_t F, const mp_window* d_windows,
-                                   const int32_t* d_frame_off, int32_t k, const mp_size* sizes,
+                                   const int32_t* d_frame_off, int32_t max_windows, int32_t k, const mp_size* sizes,
                                    const mp_size* out_dims, void* const* d_out, const int32_t* out_cap,
                                    mp_out_format fmt, int32_t* d_status, void* d_ws, size_t ws_bytes,
                                    void* stream);
@@ -206,7 +211,7 @@ typedef enum {
  */
 mp_status mp_gather_resize_nv12(const uint8_t* d_frames, int64_t frame_stride, int32_t pitch, int32_t W,
                                 int32_t H, int32_t F, const mp_window* d_windows, const int32_t* d_frame_off,
-                                int32_t k, const mp_size* sizes, const mp_size* out_dims, void* const* d_out,
+                                int32_t max_windows, int32_t k, const mp_size* sizes, const mp_size* out_dims, void* const* d_out,
                                 const int32_t* out_cap, mp_out_format fmt, mp_color_matrix matrix,
                                 int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
 
@@ -224,18 +229,24 @@ size_t mp_remap_nms_workspace_size(int32_t F, int32_t max_boxes);
  *  d_boxes        device mp_box[n_box]; n_box = d_win_box_off[n_win] <= max_boxes.
  *  d_win_box_off  device int32 [n_win+1]: boxes of window i are
  *                 [d_win_box_off[i], d_win_box_off[i+1]) (window order).
- *  d_windows, d_frame_off  as produced by mp_plan_windows (n_win = d_frame_off[F]).
+ *  d_windows, d_frame_off  as produced by mp_plan_windows; d_windows holds
+ *                 max_windows records and frame f's windows are
+ *                 [min(d_frame_off[f], max_windows), min(d_frame_off[f+1], max_windows))
+ *                 (windows a plan could not store do not exist; nothing past the
+ *                 buffer is read).  n_win = min(d_frame_off[F], max_windows).
  *  out_dims       host [k] detector-input dims per size class.
  *  d_out, d_out_src  device [max_out]: kept boxes (frame px) and the index of
  *                 the input box each came from; frame-major, keep order.
  *  d_out_frame_off device int32 [F+1]: CSR of kept boxes (true totals).
  *  max_boxes      capacity of d_boxes; frames whose boxes extend past it are
  *                 skipped with *d_status = MP_ERR_INVALID.
- *  Limits: at most 2048 raw boxes per frame (else *d_status = MP_ERR_CAPACITY
- *  and that frame keeps nothing).
+ *  No per-frame limit: frames with up to 2048 raw boxes are merged in shared
+ *  memory; frames with more take a global-memory path inside the same
+ *  launch (same arithmetic and results, O(n^2) IoUs over L2 — slow for very
+ *  large n).  The workspace grows with max_boxes (~80 bytes per raw box).
  */
 mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_box_off,
-                       const mp_window* d_windows, const int32_t* d_frame_off, int32_t F,
+                       const mp_window* d_windows, const int32_t* d_frame_off, int32_t max_windows, int32_t F,
                        int32_t k, const mp_size* out_dims, int32_t W, int32_t H,
                        float score_thr, float iou_thr, mp_box* d_out, int32_t* d_out_src,
                        int32_t max_out, int32_t* d_out_frame_off, int32_t* d_status,
@@ -321,7 +332,11 @@ mp_status mp_window_set_cost(const mp_plan_params* p, const float* d_scores, int
  * matchings that use only pairs with score >= floor_ (NaN never matched), via
  * the square assignment of size S = max(m, n) on cost -w (w = score if
  * allowed else 0, zero padding) with the textbook shortest-augmenting-path
- * Hungarian method in fp64 (rows in order, arg-min ties -> smallest column).
+ * Hungarian method in fp64 (rows added in order; Dijkstra arg-min ties -> a
+ * free (unassigned) column first, since it ends the search, then the smallest
+ * column index — any tie rule yields a shortest augmenting path, so the total
+ * is optimal either way; the oracle uses the same rule, so matchings are
+ * identical, not just equally good).
  *
  *  d_scores    device float; problem b's [m][n] row-major matrix starts at
  *              d_scores + problems[b].score_off (rows = track prefixes,

@@ -60,12 +60,12 @@ def _load():
     L.mp_gather_workspace_size.restype = sz
     L.mp_gather_workspace_size.argtypes = [i32, vp, vp]
     L.mp_gather_resize.restype = C.c_int
-    L.mp_gather_resize.argtypes = [vp, i32, i32, i32, i32, vp, vp, i32, vp, vp, vp, vp, C.c_int, vp, vp, sz, vp]
+    L.mp_gather_resize.argtypes = [vp, i32, i32, i32, i32, vp, vp, i32, i32, vp, vp, vp, vp, C.c_int, vp, vp, sz, vp]
     L.mp_gather_resize_strided.restype = C.c_int
-    L.mp_gather_resize_strided.argtypes = [vp, C.c_int64, i32, i32, i32, i32, vp, vp, i32, vp, vp, vp, vp, C.c_int,
+    L.mp_gather_resize_strided.argtypes = [vp, C.c_int64, i32, i32, i32, i32, vp, vp, i32, i32, vp, vp, vp, vp, C.c_int,
                                            vp, vp, sz, vp]
     L.mp_gather_resize_nv12.restype = C.c_int
-    L.mp_gather_resize_nv12.argtypes = [vp, C.c_int64, i32, i32, i32, i32, vp, vp, i32, vp, vp, vp, vp, C.c_int,
+    L.mp_gather_resize_nv12.argtypes = [vp, C.c_int64, i32, i32, i32, i32, vp, vp, i32, i32, vp, vp, vp, vp, C.c_int,
                                         C.c_int, vp, vp, sz, vp]
     L.mp_proxy_sweep_workspace_size.restype = sz
     L.mp_proxy_sweep_workspace_size.argtypes = [C.POINTER(mp_plan_params), i32]
@@ -96,7 +96,7 @@ def _load():
     L.mp_remap_nms_workspace_size.restype = sz
     L.mp_remap_nms_workspace_size.argtypes = [i32, i32]
     L.mp_remap_nms.restype = C.c_int
-    L.mp_remap_nms.argtypes = [vp, vp, vp, vp, i32, i32, vp, i32, i32, f32, f32, vp, vp, i32, vp, vp, i32, vp,
+    L.mp_remap_nms.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, i32, i32, f32, f32, vp, vp, i32, vp, vp, i32, vp,
                                sz, vp]
     return L
 
@@ -150,6 +150,15 @@ def _stream(stream):
     return C.c_void_p(s.cuda_stream)
 
 
+def _nwin(windows) -> int:
+    """Capacity (records) of an int32 [n, 7] windows tensor."""
+    if windows is None:
+        return 0
+    if windows.dim() != 2 or windows.shape[1] != 7:
+        raise ValueError("windows must be int32 [n, 7] (mp_window records)")
+    return int(windows.shape[0])
+
+
 def _sizes(sizes: Sequence) -> C.Array:
     arr = (mp_size * len(sizes))()
     for i, (w, h) in enumerate(sizes):
@@ -194,7 +203,14 @@ def mp_plan_windows(params: PlanParams, scores, F, mask, windows, frame_off, cla
     _dev(class_count, torch.int32, "class_count")
     _dev(status, torch.int32, "status")
     _dev(ws, torch.uint8, "ws")
-    max_w = 0 if windows is None else windows.shape[0]
+    R, Cc = params.grid
+    if scores.numel() < int(F) * R * Cc:
+        raise ValueError(f"scores must hold F x {R} x {Cc} cells (got {scores.numel()} for F = {F})")
+    if mask is not None and mask.numel() < int(F) * R * ((Cc + 31) // 32):
+        raise ValueError("mask too small for F frames")
+    if frame_off.numel() < int(F) + 1:
+        raise ValueError("frame_off needs F + 1 entries")
+    max_w = _nwin(windows)
     st = _lib.mp_plan_windows(C.byref(params.c), _p(scores), int(F), _p(mask), _p(windows), max_w,
                               _p(frame_off), _p(class_count), _p(status), _p(ws),
                               0 if ws is None else ws.numel(), _stream(stream))
@@ -213,6 +229,8 @@ def mp_gather_resize(frame_ptrs, pitch, W, H, F, windows, frame_off, sizes, out_
     (HBM or pinned host) of uint8 [H][pitch] frames; outs = list of k class tensors (f32 [cap,3,oh,ow] or
     u8 [cap,oh,ow,3]); capacity = outs[k].shape[0]."""
     _dev(frame_ptrs, torch.int64, "frame_ptrs")
+    if frame_ptrs.numel() < int(F):
+        raise ValueError("frame_ptrs needs F entries")
     _dev(windows, torch.int32, "windows")
     _dev(frame_off, torch.int32, "frame_off")
     _dev(status, torch.int32, "status")
@@ -225,7 +243,8 @@ def mp_gather_resize(frame_ptrs, pitch, W, H, F, windows, frame_off, sizes, out_
         _dev(o, odt, f"outs[{q}]")
     ptrs = (C.c_void_p * k)(*[o.data_ptr() for o in outs])
     cap = (C.c_int32 * k)(*[int(o.shape[0]) for o in outs])
-    st = _lib.mp_gather_resize(_p(frame_ptrs), int(pitch), int(W), int(H), int(F), _p(windows), _p(frame_off), k,
+    st = _lib.mp_gather_resize(_p(frame_ptrs), int(pitch), int(W), int(H), int(F), _p(windows), _p(frame_off),
+                               _nwin(windows), k,
                                _sizes(sizes), _sizes(out_dims), ptrs, cap, int(fmt), _p(status), _p(ws),
                                ws.numel(), _stream(stream))
     if st != MP_OK:
@@ -252,8 +271,8 @@ def mp_gather_resize_strided(frames, W, H, windows, frame_off, sizes, out_dims, 
     ptrs = (C.c_void_p * k)(*[o.data_ptr() for o in outs])
     cap = (C.c_int32 * k)(*[int(o.shape[0]) for o in outs])
     st = _lib.mp_gather_resize_strided(_p(frames), int(frames.stride(0)), int(pitch), int(W), int(H), int(F),
-                                       _p(windows), _p(frame_off), k, _sizes(sizes), _sizes(out_dims), ptrs, cap,
-                                       int(fmt), _p(status), _p(ws), ws.numel(), _stream(stream))
+                                       _p(windows), _p(frame_off), _nwin(windows), k, _sizes(sizes), _sizes(out_dims),
+                                       ptrs, cap, int(fmt), _p(status), _p(ws), ws.numel(), _stream(stream))
     if st != MP_OK:
         raise MPError(st, "mp_gather_resize_strided")
 
@@ -280,8 +299,8 @@ def mp_gather_resize_nv12(frames, W, H, windows, frame_off, sizes, out_dims, out
     ptrs = (C.c_void_p * k)(*[o.data_ptr() for o in outs])
     cap = (C.c_int32 * k)(*[int(o.shape[0]) for o in outs])
     st = _lib.mp_gather_resize_nv12(_p(frames), int(frames.stride(0)), int(pitch), int(W), int(H), int(F),
-                                    _p(windows), _p(frame_off), k, _sizes(sizes), _sizes(out_dims), ptrs, cap,
-                                    int(fmt), int(matrix), _p(status), _p(ws), ws.numel(), _stream(stream))
+                                    _p(windows), _p(frame_off), _nwin(windows), k, _sizes(sizes), _sizes(out_dims),
+                                    ptrs, cap, int(fmt), int(matrix), _p(status), _p(ws), ws.numel(), _stream(stream))
     if st != MP_OK:
         raise MPError(st, "mp_gather_resize_nv12")
 
@@ -303,7 +322,8 @@ def mp_remap_nms(boxes, win_box_off, windows, frame_off, F, out_dims, W, H, scor
     _dev(out_frame_off, torch.int32, "out_frame_off")
     _dev(status, torch.int32, "status")
     _dev(ws, torch.uint8, "ws")
-    st = _lib.mp_remap_nms(_p(boxes), _p(win_box_off), _p(windows), _p(frame_off), int(F), len(out_dims),
+    st = _lib.mp_remap_nms(_p(boxes), _p(win_box_off), _p(windows), _p(frame_off), _nwin(windows), int(F),
+                           len(out_dims),
                            _sizes(out_dims), int(W), int(H), C.c_float(score_thr), C.c_float(iou_thr), _p(out),
                            _p(out_src), int(out.shape[0]), _p(out_frame_off), _p(status),
                            int(boxes.shape[0]), _p(ws), ws.numel(), _stream(stream))

@@ -64,6 +64,7 @@ struct GatherArgs {
   int k, W, H, pitch, F, fmt, stage_bytes, stages, debug, tensor, src;
   int wait_mode;             // bit 0: producer sleeps on empty slots, bit 1: consumers sleep on full slots
   int rpf;                   // row-sparse: rows per frame in the 2-D row view of the frame batch
+  int max_windows;           // capacity of the windows buffer: n_win = min(frame_off[F], max_windows)
   int ncol[kMaxClasses];
   int box_w[kMaxClasses], box_h[kMaxClasses];
   int w[kMaxClasses], h[kMaxClasses], ow[kMaxClasses], oh[kMaxClasses];
@@ -169,7 +170,11 @@ __global__ void __launch_bounds__(kPrepThreads) gather_prep_kernel(GatherArgs A,
     else tap(A.h[q], A.oh[q], d, i0, lam);
     ws_tap[e] = make_int2(i0, __float_as_int(lam));
   }
-  const int n_win = frame_off[A.F];
+  // a plan that overflowed its window buffer reports the true total in
+  // frame_off[F]; only the max_windows records in the buffer exist
+  const int n_all = frame_off[A.F];
+  const int n_win = min(n_all, A.max_windows);
+  if (gtid == 0 && n_all > A.max_windows) set_status(d_status, MP_ERR_CAPACITY);
   for (int i = gtid; i < n_win; i += gstride) {
     const mp_window w = win[i];
     const int q = w.size_idx;
@@ -467,7 +472,7 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
     struct WinRef {
       int frame, x, y, valid;
     };
-    const int n_win = frame_off[A.F];
+    const int n_win = min(frame_off[A.F], A.max_windows);
     TileInfo cur, nxt;
     WinRef dcur = WinRef{0, 0, 0, 0}, dnxt = dcur;
     int clo_cur = 0, rlo_cur = 0, rhi_cur = 0, clo_nxt = 0, rlo_nxt = 0, rhi_nxt = 0;
@@ -958,13 +963,15 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
 
 extern "C" mp_status mp_gather_resize(const uint8_t* const* d_frame_ptrs, int32_t pitch, int32_t W, int32_t H,
                                       int32_t F, const mp_window* d_windows, const int32_t* d_frame_off,
-                                      int32_t k, const mp_size* sizes, const mp_size* out_dims,
+                                      int32_t max_windows, int32_t k, const mp_size* sizes, const mp_size* out_dims,
                                       void* const* d_out, const int32_t* out_cap, mp_out_format fmt,
                                       int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
   GatherArgs A;
   if (!build_gather_args(kSrcRGB24, false, pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A))
     return MP_ERR_INVALID;
   if (!d_frame_off || !d_status || (F > 0 && (!d_frame_ptrs || !d_windows))) return MP_ERR_INVALID;
+  if (max_windows < 0) return MP_ERR_INVALID;
+  A.max_windows = max_windows;
   TmapArray tm;
   memset(&tm, 0, sizeof(tm));
   A.tensor = 0;
@@ -1020,7 +1027,8 @@ static bool row_view_ok(int64_t frame_stride, int pitch, int F) {
 
 extern "C" mp_status mp_gather_resize_strided(const uint8_t* d_frames, int64_t frame_stride, int32_t pitch,
                                               int32_t W, int32_t H, int32_t F, const mp_window* d_windows,
-                                              const int32_t* d_frame_off, int32_t k, const mp_size* sizes,
+                                              const int32_t* d_frame_off, int32_t max_windows, int32_t k,
+                                              const mp_size* sizes,
                                               const mp_size* out_dims, void* const* d_out, const int32_t* out_cap,
                                               mp_out_format fmt, int32_t* d_status, void* d_ws, size_t ws_bytes,
                                               void* stream) {
@@ -1030,6 +1038,8 @@ extern "C" mp_status mp_gather_resize_strided(const uint8_t* d_frames, int64_t f
     return MP_ERR_INVALID;
   A.rpf = rows ? (int)(frame_stride / pitch) : 0;
   if (!d_frame_off || !d_status || (F > 0 && (!d_frames || !d_windows))) return MP_ERR_INVALID;
+  if (max_windows < 0) return MP_ERR_INVALID;
+  A.max_windows = max_windows;
   if (F > 0 && (((uintptr_t)d_frames) & 15)) return MP_ERR_INVALID;
   if (frame_stride < (int64_t)H * pitch || (frame_stride & 15) || frame_stride >= (int64_t(1) << 40))
     return MP_ERR_INVALID;
@@ -1072,7 +1082,8 @@ static bool nv12_coefficients(int matrix, float* c) {
 
 extern "C" mp_status mp_gather_resize_nv12(const uint8_t* d_frames, int64_t frame_stride, int32_t pitch, int32_t W,
                                            int32_t H, int32_t F, const mp_window* d_windows,
-                                           const int32_t* d_frame_off, int32_t k, const mp_size* sizes,
+                                           const int32_t* d_frame_off, int32_t max_windows, int32_t k,
+                                           const mp_size* sizes,
                                            const mp_size* out_dims, void* const* d_out, const int32_t* out_cap,
                                            mp_out_format fmt, mp_color_matrix matrix, int32_t* d_status,
                                            void* d_ws, size_t ws_bytes, void* stream) {
@@ -1083,6 +1094,8 @@ extern "C" mp_status mp_gather_resize_nv12(const uint8_t* d_frames, int64_t fram
   A.rpf = rows ? (int)(frame_stride / pitch) : 0;
   if (!nv12_coefficients((int)matrix, A.cvt)) return MP_ERR_INVALID;
   if (!d_frame_off || !d_status || (F > 0 && (!d_frames || !d_windows))) return MP_ERR_INVALID;
+  if (max_windows < 0) return MP_ERR_INVALID;
+  A.max_windows = max_windows;
   if (F > 0 && (((uintptr_t)d_frames) & 15)) return MP_ERR_INVALID;
   if (frame_stride < (int64_t)(H + H / 2) * pitch || (frame_stride & 15) || frame_stride >= (int64_t(1) << 40))
     return MP_ERR_INVALID;

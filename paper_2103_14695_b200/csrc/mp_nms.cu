@@ -12,8 +12,11 @@
 //   nms_small_kernel   4/SM     queued frames with <= 512 raw boxes, one CTA each:
 //                               block compaction, bitonic sort, n x ceil(n/64)
 //                               IoU bitmask, warp-0 greedy scan
-//   nms_large_kernel   1/SM     queued frames (<= 2048 raw boxes; bitmask up to
-//                               1024 candidates, tiled 64-candidate blocks beyond)
+//   nms_large_kernel   1/SM     queued frames (<= 2048 raw boxes in shared memory:
+//                               bitmask up to 1024 candidates, tiled 64-candidate
+//                               blocks beyond; frames with more raw boxes run the
+//                               same tiled greedy over global-memory scratch, with
+//                               a merge sort of the keys — no per-frame limit)
 //   nms_scan_kernel    1 CTA    kept-box CSR per frame, capacity check
 //   nms_scatter_kernel          compact kept boxes into the caller's buffers
 #include "mp_internal.cuh"
@@ -22,6 +25,7 @@ namespace mpk {
 
 struct NmsArgs {
   int F, k, max_out, max_boxes;
+  int max_windows;   // capacity of the windows buffer (a plan may report more in frame_off)
   float score_thr, iou_thr;
   int ow[kMaxClasses], oh[kMaxClasses];
 };
@@ -324,10 +328,175 @@ __device__ void nms_frame(const NmsArgs& A, int f, int b_lo, int b_hi, int w_lo,
   if (tid == 0) ws_kept[f] = nk;
 }
 
+// Global-memory scratch of the unbounded path, indexed by raw-box position
+// (a frame's candidates live at its raw-box range [b_lo, b_hi)).
+struct NmsGlobal {
+  float4* bx;
+  int* cls;
+  float* score;
+  int* src;
+  unsigned long long* key;
+  unsigned long long* key2;
+  int* keep;
+  unsigned char* supp;
+};
+
+// Number of keys in the ascending run k[lo, hi) that are < x.
+__device__ __forceinline__ int count_less(const unsigned long long* __restrict__ k, int lo, int hi,
+                                          unsigned long long x) {
+  const int base = lo;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (k[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo - base;
+}
+
+// Frames with more raw boxes than fit in shared memory: the same steps and
+// arithmetic as nms_frame (remap + ordered compaction, sort by the unique
+// (score desc, index) keys, tiled greedy with 64-candidate blocks), with the
+// candidates in global scratch and the keys sorted by a bottom-up merge sort
+// (each key's output position = its offset in its run + its rank in the
+// partner run).  Slow (O(n^2) IoUs over L2) but exact and unbounded.
+__device__ void nms_frame_global(const NmsArgs& A, int f, int b_lo, int b_hi, int w_lo, int w_hi, const NmsSmem& S,
+                                 const NmsGlobal& g, const mp_box* __restrict__ boxes,
+                                 const int* __restrict__ win_box_off, const mp_window* __restrict__ windows,
+                                 mp_box* __restrict__ ws_box, int* __restrict__ ws_src, int* __restrict__ ws_kept) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  float4* gbx = g.bx + b_lo;
+  int* gcls = g.cls + b_lo;
+  float* gscore = g.score + b_lo;
+  int* gsrc = g.src + b_lo;
+  unsigned char* supp = g.supp + b_lo;
+  int* keep = g.keep + b_lo;
+  // ---- a6: remap + ordered compaction (candidate order = input order)
+  int n = 0;
+  for (int base = b_lo; base < b_hi; base += blockDim.x) {
+    const int b = base + tid;
+    bool ok = false;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    mp_box bb;
+    if (b < b_hi) {
+      const int wi = window_of(win_box_off, w_lo, w_hi, b);
+      const mp_window w = windows[wi];
+      bb = boxes[b];
+      const int q = w.size_idx;
+      ok = (q >= 0 && q < A.k) && remap(bb, w, A.ow[q], A.oh[q], A.score_thr, o);
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, ok);
+    if (lane == 0) S.tmp[wid] = __popc(m);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int q = 0; q < nw; q++) {
+      const int c = S.tmp[q];
+      before += (q < wid) ? c : 0;
+      tot += c;
+    }
+    if (ok) {
+      const int p = n + before + __popc(m & lanemask_lt());
+      gbx[p] = o;
+      gcls[p] = bb.cls;
+      gscore[p] = bb.score;
+      gsrc[p] = b;
+      g.key[b_lo + p] = ((unsigned long long)score_desc_bits(bb.score) << 32) | (unsigned)p;
+    }
+    n += tot;
+    __syncthreads();
+  }
+  // ---- merge sort of the unique keys (ascending = score desc, index asc)
+  unsigned long long* ka = g.key + b_lo;
+  unsigned long long* kb = g.key2 + b_lo;
+  for (int w = 1; w < n; w <<= 1) {
+    for (int i = tid; i < n; i += blockDim.x) {
+      const int a = (i / (2 * w)) * (2 * w);
+      const int mid = min(a + w, n), end = min(a + 2 * w, n);
+      const unsigned long long x = ka[i];
+      const int pos = i < mid ? i + count_less(ka, mid, end, x) : a + (i - mid) + count_less(ka, a, mid, x);
+      kb[pos] = x;
+    }
+    __syncthreads();
+    unsigned long long* t = ka;
+    ka = kb;
+    kb = t;
+  }
+  for (int p = tid; p < n; p += blockDim.x) supp[p] = 0;
+  __syncthreads();
+  // ---- a7: tiled greedy (identical result to the sequential scan)
+  int nk = 0;
+  for (int b0 = 0; b0 < n; b0 += 64) {
+    const int b1 = min(n, b0 + 64);
+    for (int i = b0 + tid; i < b1; i += blockDim.x) {
+      const int qi = (int)(ka[i] & 0xffffffffu);
+      const float4 bi = gbx[qi];
+      const int ci = gcls[qi];
+      unsigned long long bits = 0;
+      for (int j = i + 1; j < b1; j++) {
+        const int qj = (int)(ka[j] & 0xffffffffu);
+        if (gcls[qj] == ci && iou_rn(bi, gbx[qj]) > A.iou_thr) bits |= 1ull << (j - b0);
+      }
+      S.bmask[i - b0] = bits;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long removed = 0;
+      for (int i = b0; i < b1; i++)
+        if (supp[i]) removed |= 1ull << (i - b0);
+      int nb = 0;
+      for (int i = b0; i < b1; i++) {
+        if (!((removed >> (i - b0)) & 1ull)) {
+          keep[nk + nb] = i;
+          S.bkeep[nb++] = i;
+          removed |= S.bmask[i - b0];
+        }
+      }
+      S.tmp[33] = nb;
+    }
+    __syncthreads();
+    const int nb = S.tmp[33];
+    for (int j = b1 + tid; j < n; j += blockDim.x) {
+      if (supp[j]) continue;
+      const int qj = (int)(ka[j] & 0xffffffffu);
+      const float4 bj = gbx[qj];
+      const int cj = gcls[qj];
+      for (int r = 0; r < nb; r++) {
+        const int qk = (int)(ka[S.bkeep[r]] & 0xffffffffu);
+        if (gcls[qk] == cj && iou_rn(gbx[qk], bj) > A.iou_thr) {
+          supp[j] = 1;
+          break;
+        }
+      }
+    }
+    nk += nb;
+    __syncthreads();
+  }
+  // ---- output in keep order to the frame's scratch region
+  for (int r = tid; r < nk; r += blockDim.x) {
+    const int q = (int)(ka[keep[r]] & 0xffffffffu);
+    const float4 o = gbx[q];
+    mp_box ob;
+    ob.x1 = o.x;
+    ob.y1 = o.y;
+    ob.x2 = o.z;
+    ob.y2 = o.w;
+    ob.score = gscore[q];
+    ob.cls = gcls[q];
+    ws_box[b_lo + r] = ob;
+    ws_src[b_lo + r] = gsrc[q];
+  }
+  if (tid == 0) ws_kept[f] = nk;
+}
+
 __device__ __forceinline__ bool frame_range(const NmsArgs& A, int f, const int* frame_off, const int* win_box_off,
                                             int& w_lo, int& w_hi, int& b_lo, int& b_hi) {
-  w_lo = frame_off[f];
-  w_hi = frame_off[f + 1];
+  // windows past the buffer's capacity (a plan that overflowed it still
+  // reports true offsets) do not exist: clamp, so no read leaves the buffers
+  w_lo = min(max(frame_off[f], 0), A.max_windows);
+  w_hi = min(max(frame_off[f + 1], 0), A.max_windows);
+  if (w_hi < w_lo) {
+    b_lo = b_hi = 0;
+    return false;
+  }
   b_lo = win_box_off[w_lo];
   b_hi = win_box_off[w_hi];
   return b_lo >= 0 && b_hi >= b_lo && b_hi <= A.max_boxes;
@@ -490,7 +659,7 @@ __global__ void __launch_bounds__(kLargeThreads) nms_large_kernel(NmsArgs A, con
                                                                   const int* __restrict__ frame_off,
                                                                   mp_box* __restrict__ ws_box, int* __restrict__ ws_src,
                                                                   int* __restrict__ ws_kept, const int* __restrict__ large_cnt,
-                                                                  const int* __restrict__ large_list,
+                                                                  const int* __restrict__ large_list, NmsGlobal g,
                                                                   int* __restrict__ d_status) {
   extern __shared__ __align__(16) unsigned char smem[];
   NmsSmem S;
@@ -500,15 +669,11 @@ __global__ void __launch_bounds__(kLargeThreads) nms_large_kernel(NmsArgs A, con
     const int f = large_list[li];
     int w_lo, w_hi, b_lo, b_hi;
     frame_range(A, f, frame_off, win_box_off, w_lo, w_hi, b_lo, b_hi);
-    if (b_hi - b_lo > kLargeCap) {
-      if (threadIdx.x == 0) {
-        ws_kept[f] = 0;
-        set_status(d_status, MP_ERR_CAPACITY);
-      }
-      continue;
-    }
-    nms_frame(A, f, b_lo, b_hi, w_lo, w_hi, S, kLargeCap, kLargeMaskCap, boxes, win_box_off, windows, ws_box,
-              ws_src, ws_kept);
+    if (b_hi - b_lo > kLargeCap)
+      nms_frame_global(A, f, b_lo, b_hi, w_lo, w_hi, S, g, boxes, win_box_off, windows, ws_box, ws_src, ws_kept);
+    else
+      nms_frame(A, f, b_lo, b_hi, w_lo, w_hi, S, kLargeCap, kLargeMaskCap, boxes, win_box_off, windows, ws_box,
+                ws_src, ws_kept);
     __syncthreads();
   }
 }
@@ -531,12 +696,14 @@ __global__ void __launch_bounds__(256) nms_scatter_kernel(int F, const int* __re
                                                           const mp_box* __restrict__ ws_box,
                                                           const int* __restrict__ ws_src, const int* __restrict__ ws_kept,
                                                           const int* __restrict__ out_frame_off, mp_box* __restrict__ out,
-                                                          int* __restrict__ out_src, int max_out) {
+                                                          int* __restrict__ out_src, int max_out, int max_windows) {
   const int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (f >= F) return;
-  const int b_lo = win_box_off[frame_off[f]];
-  const int n = ws_kept[f], base = out_frame_off[f];
+  const int n = ws_kept[f];
+  if (n == 0) return;   // (frames with invalid ranges keep nothing)
+  const int b_lo = win_box_off[min(max(frame_off[f], 0), max_windows)];
+  const int base = out_frame_off[f];
   for (int r = lane; r < n; r += 32) {
     const int d = base + r;
     if (d >= max_out) break;
@@ -546,7 +713,8 @@ __global__ void __launch_bounds__(256) nms_scatter_kernel(int F, const int* __re
 }
 
 struct NmsWs {
-  size_t box_off, src_off, kept_off, lcnt_off, llist_off, mlist_off, total;
+  size_t box_off, src_off, kept_off, lcnt_off, llist_off, mlist_off;
+  size_t gbx_off, gcls_off, gscore_off, gsrc_off, gkey_off, gkey2_off, gkeep_off, gsupp_off, total;
 };
 
 static NmsWs nms_ws_layout(int F, int max_boxes) {
@@ -558,7 +726,17 @@ static NmsWs nms_ws_layout(int F, int max_boxes) {
   L.lcnt_off = al(L.kept_off + sizeof(int) * (size_t)F);   // [0] large count, [1] mid count
   L.llist_off = al(L.lcnt_off + 2 * sizeof(int));
   L.mlist_off = al(L.llist_off + sizeof(int) * (size_t)F);
-  L.total = al(L.mlist_off + sizeof(int) * (size_t)F) + 256;
+  // unbounded path (frames with > kLargeCap raw boxes): per raw box 49 bytes
+  const size_t nb = (size_t)max_boxes;
+  L.gbx_off = al(L.mlist_off + sizeof(int) * (size_t)F);
+  L.gcls_off = al(L.gbx_off + sizeof(float4) * nb);
+  L.gscore_off = al(L.gcls_off + sizeof(int) * nb);
+  L.gsrc_off = al(L.gscore_off + sizeof(float) * nb);
+  L.gkey_off = al(L.gsrc_off + sizeof(int) * nb);
+  L.gkey2_off = al(L.gkey_off + 8 * nb);
+  L.gkeep_off = al(L.gkey2_off + 8 * nb);
+  L.gsupp_off = al(L.gkeep_off + sizeof(int) * nb);
+  L.total = al(L.gsupp_off + nb) + 256;
   return L;
 }
 
@@ -572,11 +750,13 @@ extern "C" size_t mp_remap_nms_workspace_size(int32_t F, int32_t max_boxes) {
 }
 
 extern "C" mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_box_off, const mp_window* d_windows,
-                                  const int32_t* d_frame_off, int32_t F, int32_t k, const mp_size* out_dims,
+                                  const int32_t* d_frame_off, int32_t max_windows, int32_t F, int32_t k,
+                                  const mp_size* out_dims,
                                   int32_t W, int32_t H, float score_thr, float iou_thr, mp_box* d_out,
                                   int32_t* d_out_src, int32_t max_out, int32_t* d_out_frame_off, int32_t* d_status,
                                   int32_t max_boxes, void* d_ws, size_t ws_bytes, void* stream) {
-  if (F < 0 || k < 1 || k > kMaxClasses || !out_dims || W < 1 || H < 1 || max_out < 0 || max_boxes < 0)
+  if (F < 0 || k < 1 || k > kMaxClasses || !out_dims || W < 1 || H < 1 || max_out < 0 || max_boxes < 0 ||
+      max_windows < 0)
     return MP_ERR_INVALID;
   if (!d_out_frame_off || !d_status || !d_frame_off || !d_win_box_off) return MP_ERR_INVALID;
   if (max_out > 0 && (!d_out || !d_out_src)) return MP_ERR_INVALID;
@@ -588,6 +768,7 @@ extern "C" mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_bo
   A.k = k;
   A.max_out = max_out;
   A.max_boxes = max_boxes;
+  A.max_windows = max_windows;
   A.score_thr = score_thr;
   A.iou_thr = iou_thr;
   for (int q = 0; q < k; q++) {
@@ -605,6 +786,15 @@ extern "C" mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_bo
   int* llist = (int*)(ws + L.llist_off);
   int* mcnt = lcnt + 1;
   int* mlist = (int*)(ws + L.mlist_off);
+  NmsGlobal g;
+  g.bx = (float4*)(ws + L.gbx_off);
+  g.cls = (int*)(ws + L.gcls_off);
+  g.score = (float*)(ws + L.gscore_off);
+  g.src = (int*)(ws + L.gsrc_off);
+  g.key = (unsigned long long*)(ws + L.gkey_off);
+  g.key2 = (unsigned long long*)(ws + L.gkey2_off);
+  g.keep = (int*)(ws + L.gkeep_off);
+  g.supp = (unsigned char*)(ws + L.gsupp_off);
   cudaStream_t s = (cudaStream_t)stream;
   if (F > 0) {
     MP_CUDA_TRY(cudaMemsetAsync(lcnt, 0, 2 * sizeof(int), s));
@@ -623,14 +813,14 @@ extern "C" mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_bo
                                                              d_status);
     MP_CUDA_TRY(cudaGetLastError());
     nms_large_kernel<<<sms, kLargeThreads, sm_large, s>>>(A, d_boxes, d_win_box_off, d_windows, d_frame_off,
-                                                          ws_box, ws_src, ws_kept, lcnt, llist, d_status);
+                                                          ws_box, ws_src, ws_kept, lcnt, llist, g, d_status);
     MP_CUDA_TRY(cudaGetLastError());
   }
   nms_scan_kernel<<<1, 1024, 0, s>>>(F, ws_kept, d_out_frame_off, max_out, d_status);
   MP_CUDA_TRY(cudaGetLastError());
   if (F > 0) {
     nms_scatter_kernel<<<(F + 7) / 8, 256, 0, s>>>(F, d_frame_off, d_win_box_off, ws_box, ws_src, ws_kept,
-                                                   d_out_frame_off, d_out, d_out_src, max_out);
+                                                   d_out_frame_off, d_out, d_out_src, max_out, max_windows);
     MP_CUDA_TRY(cudaGetLastError());
   }
   return MP_OK;

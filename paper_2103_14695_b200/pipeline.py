@@ -102,7 +102,10 @@ class WindowPipeline:
 
     # ------------------------------------------------------------ steps
     def plan(self, scores: torch.Tensor, stream=None):
-        F = scores.shape[0]
+        R, C = self.params.grid
+        if tuple(scores.shape) != (self.F, R, C):
+            raise ValueError(f"scores must be [{self.F}, {R}, {C}] (reserved F x grid), got {tuple(scores.shape)}")
+        F = self.F
         B.mp_plan_windows(self.params, scores, F, self.mask, self.windows, self.frame_off, self.class_count,
                           self.status, self.plan_ws, stream)
 
@@ -173,106 +176,205 @@ class PipelinedRunner:
     plan(i) waits for it (the proxy consumes that downscale), so the downscale
     of batch i+1 overlaps the gather of batch i.
 
-    Each in-flight batch owns one WindowPipeline (double buffering: `depth`
-    sets of plan/gather/NMS buffers), so no stage of batch i+1 overwrites a
-    buffer a later stage of batch i still reads.  Ordering is enforced only
-    with CUDA events (no host synchronisation):
-        plan(i) -> gather(i) -> [detector] -> merge(i);  plan(i) waits merge(i-depth).
+    Each in-flight batch owns one WindowPipeline (`depth` sets of plan/gather/
+    NMS buffers), so no stage of batch i+1 overwrites a buffer a later stage of
+    batch i still reads.  Ordering is enforced only with CUDA events (no host
+    synchronisation):
+        caller's stream -> plan(i) -> gather(i) -> [detector] -> merge(i);
+        plan(i) waits merge(i-depth).
+
+    Two ways to drive it:
+      * `enqueue(scores, frames)` (plan + gather of one batch, returns its
+        buffer-set index k; the detector reads `pipes[k].outs` after
+        `wait_gathered(k)`), then `merge(k, boxes, win_box_off,
+        detector_done=event)` once the detector has produced the boxes; the
+        merge waits for `detector_done`, so the next batch that reuses set k
+        cannot overwrite `outs` while the detector still reads them;
+      * `step(scores, frames, boxes, win_box_off)` = both at once (stand-in
+        detections known in advance, as in bench.py).
+    Every call first makes the side streams wait for the caller's current
+    stream (inputs written there, e.g. non_blocking H2D copies, are complete)
+    and records the caller's tensors on the side streams (record_stream), so
+    the caching allocator does not hand their memory out while they are read.
     """
 
     def __init__(self, pipes, device="cuda", merge_on_gather_stream: bool = False, side_streams: int = 1):
         self.pipes = list(pipes)
         self.depth = len(self.pipes)
-        dev = torch.device(device)
+        self.dev = torch.device(device)
+        dev = self.dev
         # side_streams > 1: plan and remap/NMS of consecutive batches run on
         # their own streams (set k uses stream k mod side_streams), so the
-        # plans (and merges) of two batches may overlap each other — their
-        # latency beside the persistent gather then no longer caps the step
+        # plans (and merges) of two batches may overlap each other
         n = max(1, min(int(side_streams), self.depth))
         self.s_plans = [torch.cuda.Stream(dev) for _ in range(n)]
         self.s_plan = self.s_plans[0]
         self.s_gather = torch.cuda.Stream(dev)
         # merge_on_gather_stream: remap/NMS(i) runs right after gather(i) on the
-        # gather stream instead of concurrently with gather(i+1) (the persistent
-        # gather leaves co-running latency-bound kernels little of each SM)
+        # gather stream instead of concurrently with gather(i+1)
         self.s_merges = [self.s_gather] if merge_on_gather_stream else [torch.cuda.Stream(dev) for _ in range(n)]
         self.s_merge = self.s_merges[0]
         self.s_proxy = torch.cuda.Stream(dev) if self.pipes[0].proxy_dims else None
-        self.done = [None] * self.depth
+        self.done = [None] * self.depth       # merge(i) finished -> set k reusable
+        self.gathered = [None] * self.depth   # gather(i) finished -> set k's outs readable
+        self.pending = [False] * self.depth   # set k enqueued, merge not yet enqueued
+        self.static = None                    # graph mode: runner-owned inputs per set
         self.i = 0
 
+    # ------------------------------------------------------------ graphs
     def capture_graphs(self, scores, boxes=None, win_box_off=None):
-        """Capture each pipeline's plan and merge calls (4 + 5 launches, all
-        latency-bound) as CUDA graphs over fixed input tensors; `step` then
-        replays them.  The gather stays a plain launch (2 kernels) so its
-        duration can be timed with events on its stream."""
-        self.g_plan, self.g_merge = [], []
+        """Capture each buffer set's plan and merge calls (latency-bound
+        launches) as CUDA graphs over runner-OWNED static input tensors
+        (copies of the examples given here).  `enqueue`/`merge` then copy each
+        batch's inputs into them before the replay — or skip the copy when the
+        caller already wrote into `inputs(k)` in place.  The gather stays a
+        plain launch so its duration can be timed with events on its stream."""
+        if any(self.pending):
+            raise RuntimeError("capture_graphs with batches in flight")
+        torch.cuda.synchronize(self.dev)
+        self.g_plan, self.g_merge, self.static = [], [], []
         for k, p in enumerate(self.pipes):
             sp, sm = self.s_plans[k % len(self.s_plans)], self.s_merges[k % len(self.s_merges)]
+            st = {"scores": scores.detach().clone(),
+                  "boxes": None if boxes is None else boxes.detach().clone(),
+                  "win_box_off": None if win_box_off is None else win_box_off.detach().clone()}
+            self.static.append(st)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=sp):
-                p.plan(scores, stream=sp)
+                p.plan(st["scores"], stream=sp)
             self.g_plan.append(g)
             if boxes is not None:
                 g2 = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g2, stream=sm):
-                    p.merge(boxes, win_box_off, stream=sm)
+                    p.merge(st["boxes"], st["win_box_off"], stream=sm)
                 self.g_merge.append(g2)
-        torch.cuda.synchronize()
+        torch.cuda.synchronize(self.dev)
 
-    def step(self, scores, frames, boxes=None, win_box_off=None, gather_events=None, proxy_events=None):
-        """Enqueue one batch.  `boxes`/`win_box_off` are the detector's output
-        for this batch (None skips the merge).  gather_events / proxy_events:
-        optional (start, end) CUDA events recorded around the gather / the
-        proxy-input downscale on their streams."""
+    def inputs(self, k: Optional[int] = None):
+        """Graph mode: the static (scores, boxes, win_box_off) tensors of
+        buffer set k (default: the set the next `enqueue` uses).  A caller that
+        writes its inputs there in place (on its current stream) saves the
+        per-batch copy."""
+        if self.static is None:
+            raise RuntimeError("inputs() needs capture_graphs()")
+        st = self.static[self.i % self.depth if k is None else k]
+        return st["scores"], st["boxes"], st["win_box_off"]
+
+    # ------------------------------------------------------------ helpers
+    def _caller_ready(self):
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.dev))
+        return ev
+
+    @staticmethod
+    def _use(t, stream):
+        if t is not None and t.is_cuda:
+            t.record_stream(stream)
+
+    @staticmethod
+    def _stage(dst, src, stream):
+        """Copy a caller tensor into a static graph input on `stream` (no-op
+        when the caller passed the static tensor itself)."""
+        if src is None or dst is None or src.data_ptr() == dst.data_ptr():
+            return
+        if src.shape != dst.shape or src.dtype != dst.dtype:
+            raise ValueError(f"graph input shape/dtype changed: {tuple(src.shape)} {src.dtype} vs captured "
+                             f"{tuple(dst.shape)} {dst.dtype}")
+        with torch.cuda.stream(stream):
+            dst.copy_(src, non_blocking=True)
+        PipelinedRunner._use(src, stream)
+
+    # ------------------------------------------------------------ pipeline
+    def enqueue(self, scores, frames, gather_events=None, proxy_events=None) -> int:
+        """Enqueue plan + gather of one batch; returns its buffer set k.
+        gather_events / proxy_events: optional (start, end) CUDA events
+        recorded around the gather / the proxy-input downscale."""
         k = self.i % self.depth
+        if self.pending[k]:
+            raise RuntimeError(f"buffer set {k} still awaits merge() of batch {self.i - self.depth}")
         p = self.pipes[k]
         s_plan = self.s_plans[k % len(self.s_plans)]
-        s_merge = self.s_merges[k % len(self.s_merges)]
-        if self.done[k] is not None:
-            s_plan.wait_event(self.done[k])
-        if self.s_proxy is not None:
+        ready = self._caller_ready()
+        for s in (s_plan, self.s_gather) + ((self.s_proxy,) if self.s_proxy is not None else ()):
+            s.wait_event(ready)
             if self.done[k] is not None:
-                self.s_proxy.wait_event(self.done[k])
+                s.wait_event(self.done[k])   # set k's buffers (windows, outs) are free again
+        if self.s_proxy is not None:
             if proxy_events is not None:
                 proxy_events[0].record(self.s_proxy)
             p.proxy_input(frames, stream=self.s_proxy)
+            self._use(frames, self.s_proxy)
             if proxy_events is not None:
                 proxy_events[1].record(self.s_proxy)
             downscaled = torch.cuda.Event()
             downscaled.record(self.s_proxy)
             s_plan.wait_event(downscaled)
-        if getattr(self, "g_plan", None):
+        if self.static is not None:
+            self._stage(self.static[k]["scores"], scores, s_plan)
             with torch.cuda.stream(s_plan):
                 self.g_plan[k].replay()
         else:
             p.plan(scores, stream=s_plan)
+            self._use(scores, s_plan)
         planned = torch.cuda.Event()
         planned.record(s_plan)
         self.s_gather.wait_event(planned)
         if gather_events is not None:
             gather_events[0].record(self.s_gather)
         p.gather(frames, stream=self.s_gather)
+        self._use(frames, self.s_gather)
         if gather_events is not None:
             gather_events[1].record(self.s_gather)
         gathered = torch.cuda.Event()
         gathered.record(self.s_gather)
-        s_merge.wait_event(gathered)
+        self.gathered[k] = gathered
+        self.pending[k] = True
+        self.i += 1
+        return k
+
+    def wait_gathered(self, k: int, stream=None):
+        """Make `stream` (default: current) wait until set k's class tensors
+        (pipes[k].outs, the detector's inputs) are written."""
+        s = torch.cuda.current_stream(self.dev) if stream is None else stream
+        s.wait_event(self.gathered[k])
+
+    def merge(self, k: int, boxes=None, win_box_off=None, detector_done=None):
+        """Enqueue remap/NMS of buffer set k's batch (boxes None: no merge, the
+        set is just released).  detector_done: event recorded after the
+        detector's last read of pipes[k].outs and write of the boxes."""
+        if not self.pending[k]:
+            raise RuntimeError(f"buffer set {k} has no batch awaiting merge")
+        p = self.pipes[k]
+        s_merge = self.s_merges[k % len(self.s_merges)]
+        s_merge.wait_event(self.gathered[k])
+        s_merge.wait_event(self._caller_ready())
+        if detector_done is not None:
+            s_merge.wait_event(detector_done)
         if boxes is not None:
-            if getattr(self, "g_merge", None):
+            if self.static is not None and self.g_merge:
+                self._stage(self.static[k]["boxes"], boxes, s_merge)
+                self._stage(self.static[k]["win_box_off"], win_box_off, s_merge)
                 with torch.cuda.stream(s_merge):
                     self.g_merge[k].replay()
             else:
                 p.merge(boxes, win_box_off, stream=s_merge)
+                self._use(boxes, s_merge)
+                self._use(win_box_off, s_merge)
         done = torch.cuda.Event()
         done.record(s_merge)
         self.done[k] = done
-        self.i += 1
-        return p
+        self.pending[k] = False
+
+    def step(self, scores, frames, boxes=None, win_box_off=None, gather_events=None, proxy_events=None):
+        """enqueue + merge of one batch whose detector output is already known
+        (`boxes`/`win_box_off`; None skips the merge).  Returns its pipeline."""
+        k = self.enqueue(scores, frames, gather_events, proxy_events)
+        self.merge(k, boxes, win_box_off)
+        return self.pipes[k]
 
     def wait_all(self, stream=None):
         """Make `stream` (default: current) wait for everything enqueued."""
-        s = torch.cuda.current_stream() if stream is None else stream
-        for e in self.done:
+        s = torch.cuda.current_stream(self.dev) if stream is None else stream
+        for e in self.done + self.gathered:
             if e is not None:
                 s.wait_event(e)

@@ -92,7 +92,7 @@ def main():
     def tma():
         st = B._lib.mp_gather_resize_strided(
             C.c_void_p(frames_h.data_ptr()), int(frames_h.stride(0)), int(cfg.pitch), cfg.W, cfg.H, F,
-            B._p(p.windows), B._p(p.frame_off), k, B._sizes(p.sizes), B._sizes(p.out_dims), optrs, cap,
+            B._p(p.windows), B._p(p.frame_off), B._nwin(p.windows), k, B._sizes(p.sizes), B._sizes(p.out_dims), optrs, cap,
             int(p.fmt), B._p(p.status), B._p(p.gather_ws), p.gather_ws.numel(), B._stream(None))
         if st != 0:
             raise B.MPError(st, "strided host")

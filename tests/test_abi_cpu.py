@@ -74,14 +74,18 @@ def test_invalid_host_params_rejected_before_launch(lib):
     st = L.mp_plan_windows(ctypes.byref(big.c), None, 1, None, None, 0, None, None, None, None, 0, None)
     assert st == lib.MP_ERR_INVALID
     # remap_nms: k out of range
-    st = L.mp_remap_nms(None, None, None, None, 1, 0, None, 10, 10, ctypes.c_float(0.2), ctypes.c_float(0.5),
+    st = L.mp_remap_nms(None, None, None, None, 0, 1, 0, None, 10, 10, ctypes.c_float(0.2), ctypes.c_float(0.5),
                         None, None, 0, None, None, 0, None, 0, None)
     assert st == lib.MP_ERR_INVALID
     # gather: pitch not a multiple of 16
     sz = (lib.mp_size * 1)(lib.mp_size(10, 10))
     cap = (ctypes.c_int32 * 1)(1)
     ptr = (ctypes.c_void_p * 1)(None)
-    st = L.mp_gather_resize(None, 31, 10, 10, 1, None, None, 1, sz, sz, ptr, cap, 0, None, None, 0, None)
+    st = L.mp_gather_resize(None, 31, 10, 10, 1, None, None, 0, 1, sz, sz, ptr, cap, 0, None, None, 0, None)
+    assert st == lib.MP_ERR_INVALID
+    # negative window capacity
+    st = L.mp_remap_nms(None, None, None, None, -1, 1, 1, sz, 10, 10, ctypes.c_float(0.2), ctypes.c_float(0.5),
+                        None, None, 0, None, None, 0, None, 0, None)
     assert st == lib.MP_ERR_INVALID
 
 

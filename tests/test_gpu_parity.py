@@ -488,3 +488,85 @@ def test_gather_zero_windows_and_repeated_calls(G):
         else:
             for a, b in zip(first, cur):
                 assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("fmt", [0, 1], ids=["f32", "u8"])
+def test_full_size_c2_bench_launch_config_every_window(G, fmt):
+    """configs[1] (the bench workload: 1800 x 1080p frames) in exactly the
+    launch configuration bench.py times — PipelinedRunner, 3 buffer sets, 3
+    streams, plan/merge replayed as CUDA graphs over the runner's static
+    inputs, several steps — with EVERY window's pixels compared against the
+    oracle (run frame-parallel over the host's cores in chunks of frames;
+    slots of a chunk are contiguous per class), plus windows, CSR, masks-free
+    plan outputs and kept boxes bit-exact."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    import paper_2103_14695_b200 as mp
+    cfg = S.CONFIGS["c2_1080p_sparse"]
+    F = cfg.frames
+    clip = 0
+    scene = S.make_scene(cfg, clip, F)
+    scores = S.score_grids(cfg, clip, scene)
+    ref = O.plan_windows(cfg.W, cfg.H, 32, 32, cfg.b_proxy, cfg.sizes, cfg.cost, scores)
+    boxes, wbo = S.standin_boxes(cfg, clip, scene, ref["windows"])
+    r = O.remap_nms(boxes, wbo, ref["windows"], ref["frame_off"], cfg.out_dims, cfg.W, cfg.H, cfg.score_thr,
+                    cfg.iou_thr)
+    caps = [int(c) for c in ref["class_count"]]
+    n = len(ref["windows"])
+    pipes = []
+    for _ in range(3):
+        p = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
+                              cfg.iou_thr, fmt=fmt, device=G.DEV)
+        p.reserve(F, n, caps=caps, max_boxes=max(len(boxes), 1))
+        pipes.append(p)
+    runner = mp.PipelinedRunner(pipes, device=G.DEV)
+    frames = S.frame_pixels_torch([S.frame_seed(clip, f) for f in range(F)], cfg.H, cfg.pitch, device=G.DEV)
+    runner.capture_graphs(torch.from_numpy(scores).to(G.DEV), G.boxes_to_t(boxes), torch.from_numpy(wbo).to(G.DEV))
+    for _ in range(4):
+        sc_k, bx_k, wb_k = runner.inputs()
+        runner.step(sc_k, frames, bx_k, wb_k)
+    runner.wait_all()
+    torch.cuda.synchronize()
+    del frames
+    p = pipes[(runner.i - 1) % 3]      # the last step's buffer set
+    p.check_status()
+    assert np.array_equal(p.frame_off.cpu().numpy(), ref["frame_off"])
+    assert np.array_equal(p.windows[:n].cpu().numpy(), ref["windows"])
+    nk = int(p.nms_frame_off[F].item())
+    assert np.array_equal(p.nms_frame_off.cpu().numpy(), r["frame_off"])
+    assert np.array_equal(p.nms_src[:nk].cpu().numpy(), r["src"])
+    assert np.array_equal(p.nms_out[:nk].cpu().numpy().view(np.uint32),
+                          r["boxes"].view(np.float32).reshape(-1, 6).view(np.uint32))
+    win, fo = ref["windows"], ref["frame_off"]
+    k = len(cfg.sizes)
+    chunk = 60
+
+    def oracle_chunk(a):
+        b = min(F, a + chunk)
+        w = win[fo[a]:fo[b]].copy()
+        first = [int(np.searchsorted(np.nonzero(win[:, 5] == q)[0], fo[a])) for q in range(k)]
+        cnt = [int((w[:, 5] == q).sum()) for q in range(k)]
+        w[:, 0] -= a
+        for q in range(k):
+            w[w[:, 5] == q, 6] -= first[q]
+        frs = [S.frame_pixels_np(S.frame_seed(clip, f), cfg.H, cfg.pitch) for f in range(a, b)]
+        st, o = O.gather_resize(frs, cfg.pitch, cfg.W, cfg.H, w, cfg.sizes, cfg.out_dims, cnt,
+                                O.F32_NCHW if fmt == 0 else O.U8_NHWC)
+        assert st == 0
+        return a, first, cnt, o
+
+    checked = 0
+    with ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 1))) as ex:
+        for a, first, cnt, o in ex.map(oracle_chunk, range(0, F, chunk)):
+            for q in range(k):
+                if cnt[q] == 0:
+                    continue
+                got = p.outs[q][first[q]:first[q] + cnt[q]].cpu().numpy()
+                if fmt == 0:
+                    err = np.abs(got - o[q]).max()
+                    assert err <= F32_TOL, (a, q, err)
+                else:
+                    d = np.abs(got.astype(np.int16) - o[q].astype(np.int16)).max()
+                    assert d <= 1, (a, q, d)
+                checked += cnt[q]
+    assert checked == n
