@@ -264,6 +264,87 @@ def run_reference(args):
     return 0
 
 
+# --------------------------------------------------------------------------- multi-rank plumbing
+def relaunch(n: int) -> int:
+    """Re-exec this command under torch.distributed.run with n ranks on this
+    node (rendezvous on 127.0.0.1, a free port); returns the launcher's exit
+    code.  Rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dist_env():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def init_rank(backend="nccl"):
+    """One process per GPU: set the device, bind host threads to the GPU's
+    NUMA node (pinned host pools then sit next to its PCIe link), init the
+    process group.  Returns (world, rank, device, numa record)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_14695_b200.sharding import bind_host_to_gpu
+    world, rank, local = dist_env()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    numa = bind_host_to_gpu(local)
+    if world > 1:
+        dist.init_process_group(backend, device_id=dev)
+    return world, rank, dev, numa
+
+
+def clip_costs(cfg, n_clips, pool_pos):
+    """Per-clip cost estimates for longest-processing-time sharding: the
+    positive-cell count of the clip's data at B = 0.5 (more positive cells ->
+    more / larger windows, more boxes).  pool_pos[e] = that count for pool
+    entry e; clip c uses entry c mod len(pool_pos)."""
+    return [float(pool_pos[c % len(pool_pos)]) for c in range(n_clips)]
+
+
+def run_dry(args):
+    """CPU-only check of the multi-rank plumbing (no GPU, gloo): every rank
+    takes its clips of the configs[4] job from assign_clips (LPT over
+    per-clip cost estimates), and the per-clip coverage vector and the
+    counters are all-reduced as the GPU run does over NCCL."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_14695_b200.sharding import Counters, assign_clips, reduce_counters
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    cfg = S.CONFIGS["c5_1080p_clips"]
+    n_clips = args.clips or cfg.clips
+    cost = clip_costs(cfg, n_clips, [S.clip_cost_estimate(cfg, e) for e in range(max(1, args.clip_pool))])
+    mine = assign_clips(n_clips, world, rank, cost)
+    cover = torch.zeros(n_clips, dtype=torch.int64)
+    cover[mine] = 1
+    load = torch.tensor([sum(cost[c] for c in mine)], dtype=torch.float64)
+    loads = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+    if world > 1:
+        dist.all_reduce(cover)
+        dist.all_gather(loads, load)
+    else:
+        loads = [load]
+    c = Counters(frames=len(mine) * cfg.frames * len(S.B_SWEEP), clips=len(mine))
+    glob, _ = reduce_counters(c, 0.0)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "workload": cfg.name, "clips": glob.clips,
+                          "frames": glob.frames, "coverage_ok": bool((cover == 1).all()),
+                          "rank_loads": [float(x.item()) for x in loads]}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 # --------------------------------------------------------------------------- B200 leg
 def run_b200(args):
     import torch
@@ -271,14 +352,8 @@ def run_b200(args):
 
     import paper_2103_14695_b200 as mp
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
+    world, rank, dev, numa = init_rank()
+    local = dev.index
     cfg = S.CONFIGS[args.config]
     F = cfg.frames
     clip = rank
@@ -422,16 +497,21 @@ def run_b200(args):
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            threads = os.cpu_count() or 1
-            inp, n = oracle_baseline(cfg, clip, threads, 15.0, args.src)
-            dt = oracle_run(cfg, inp, n, threads)
+            threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+            inp, n = oracle_baseline(cfg, clip, threads, 5.0, args.src)
+            oracle_run(cfg, inp, n, threads)                                  # warm-up
+            dts = [oracle_run(cfg, inp, n, threads) for _ in range(3)]        # median of 3
+            dt = float(np.median(dts))
             n1 = max(1, n // max(threads, 1))          # the same oracle on one host thread
-            dt1 = oracle_run(cfg, inp, n1, 1)
+            oracle_run(cfg, inp, n1, 1)
+            dt1 = float(np.median([oracle_run(cfg, inp, n1, 1) for _ in range(3)]))
             cpu = {"value": n / dt, "unit": "frames/s", "cores": threads, "kind": "oracle",
-                   "value_1thread": n1 / dt1, "sample_1thread": f"first {n1} frames, 1 thread",
+                   "runs": [n / d for d in dts], "value_1thread": n1 / dt1,
+                   "sample_1thread": f"first {n1} frames, 1 thread, median of 3 after a warm-up",
                    "sample": f"first {n} of {F} frames of clip {clip} ({cfg.name}), "
                              f"{'proxy-input downscale+' if nv12 else ''}plan+gather+remap/NMS, {args.src} "
-                             f"frames, {threads} threads, {host_cpu_desc()}"}
+                             f"frames, {threads} threads, median of 3 runs after a warm-up run, "
+                             f"{host_cpu_desc()}"}
         line = {
             "metric": "frames/sec of proxy-guided window pipeline", "value": value, "unit": "frames/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -442,7 +522,7 @@ def run_b200(args):
                        "b_proxy": cfg.b_proxy, "windows_per_step": n_win, "class_count": counts,
                        "raw_boxes_per_step": int(len(boxes)), "kept_boxes_per_step": n_kept,
                        "l2": l2_note,
-                       "parallelism": f"clip-sharded x{world}",
+                       "parallelism": f"clip-sharded x{world}", "host_numa": numa,
                        "pipeline": f"plan/gather/merge on {1 + 2 * len(runner.s_plans)} CUDA streams, "
                                    f"{args.depth} buffer sets, "
                                    f"plan/merge as CUDA graphs: {bool(args.graphs)}"},
@@ -466,6 +546,141 @@ def run_b200(args):
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def _gen_pool_entry(args_):
+    name, e = args_
+    cfg = S.CONFIGS[name]
+    sc = S.make_scene(cfg, e)
+    return S.score_grids(cfg, e, sc), sc
+
+
+def run_clips(args):
+    """configs[4]: the 1000 x 1080p-clip job sharded over the ranks, with the
+    B_proxy sweep 0.1..0.9.  Each rank takes its clips from assign_clips
+    (longest-processing-time over per-clip cost estimates), and for every B
+    runs the whole path (plan -> gather/resize -> remap/NMS, detector stand-in
+    excluded) over each of its clips as one 1800-frame batch through the
+    PipelinedRunner.  No data-path collective; the counters and the per-B
+    elapsed times are all-reduced (SUM / MAX) at the end.  Strong scaling:
+    the total work (clips x frames x thresholds) is fixed.
+
+    Inputs (untimed): a pool of --clip-pool generated clips (scenes + score
+    grids, host), clip c using entry c mod pool; one 1800-frame RGB24 frame
+    batch in HBM shared by all clips (11.2 GB >> L2); per (entry, B) the
+    stand-in detector's boxes, generated on the device from that entry's
+    plan (synth.standin_boxes_torch)."""
+    import torch
+    import torch.distributed as dist
+    from concurrent.futures import ProcessPoolExecutor
+
+    from paper_2103_14695_b200.sharding import Counters, assign_clips, reduce_counters
+    cfg = S.CONFIGS["c5_1080p_clips"]
+    F = cfg.frames
+    n_clips = args.clips or cfg.clips
+    P = max(1, min(args.clip_pool, n_clips))
+    world, rank, local = dist_env()
+    # host generation before any CUDA context exists (worker processes fork)
+    workers = max(1, min(P, len(os.sched_getaffinity(0)) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))))
+    with ProcessPoolExecutor(max_workers=workers) as ex:
+        pool = list(ex.map(_gen_pool_entry, [(cfg.name, e) for e in range(P)]))
+    world, rank, dev, numa = init_rank()
+    import paper_2103_14695_b200 as mp
+    pos = [int((sc > 0.5).sum()) for sc, _ in pool]
+    cost = clip_costs(cfg, n_clips, pos)
+    mine = assign_clips(n_clips, world, rank, cost)
+    fmt = mp.MP_OUT_F32_NCHW if args.fmt == "f32" else mp.MP_OUT_U8_NHWC
+    frames = S.frame_pixels_torch([S.frame_seed(10_000 + rank, f) for f in range(F)], cfg.H, cfg.pitch, device=dev)
+    scores = [torch.from_numpy(sc).to(dev) for sc, _ in pool]
+    objs = []
+    for _, scene in pool:
+        ob = np.concatenate(scene.boxes) if sum(len(b) for b in scene.boxes) else np.zeros((0, 4))
+        oc = np.concatenate(scene.cls) if len(ob) else np.zeros(0, np.int32)
+        off = np.concatenate([[0], np.cumsum([len(b) for b in scene.boxes])]).astype(np.int64)
+        objs.append((ob, oc, off))
+    R, C = cfg.grid
+    stream = torch.cuda.current_stream(dev)
+    per_b = []
+    mine_counters = Counters()
+    for b in S.B_SWEEP:
+        # untimed: plan every pool entry at B, stand-in boxes from its windows, buffer sizes
+        probe = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, b, cfg.score_thr, cfg.iou_thr,
+                                  fmt=fmt, device=dev)
+        probe.reserve(F, F * R * ((C + 1) // 2))
+        det, n_win, counts, ent_ctr = [], [], [], []
+        for e in range(P):
+            probe.plan(scores[e])
+            torch.cuda.synchronize(dev)
+            probe.check_status()
+            nw = int(probe.frame_off[F].item())
+            win = probe.windows[:nw].clone()
+            bx, wbo = S.standin_boxes_torch(cfg, e, *objs[e], win, dev)
+            det.append((bx, wbo))
+            n_win.append(nw)
+            counts.append(probe.class_count.cpu().tolist())
+            wn = win.cpu().numpy()
+            ab = algorithmic_bytes(cfg, wn, probe.frame_off.cpu().numpy(), int(wbo[-1].item()), 0, F,
+                                   4 if args.fmt == "f32" else 1) if len(wn) else dict(read_union=0, out=0)
+            ent_ctr.append(Counters(frames=F, windows=nw, fallback_frames=int((wn[:, 5] == len(cfg.sizes) - 1).sum())
+                                    if len(wn) else 0, crop_bytes=int(ab["read_union"]), out_bytes=int(ab["out"]),
+                                    boxes_in=int(wbo[-1].item()), clips=1))
+        del probe
+        caps = [max(c[q] for c in counts) for q in range(len(cfg.sizes))]
+        nb = max(max(int(d[0].shape[0]) for d in det), 1)
+        pipes = []
+        for _ in range(args.depth):
+            pp = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, b, cfg.score_thr, cfg.iou_thr,
+                                   fmt=fmt, device=dev)
+            pp.reserve(F, max(max(n_win), 1), caps=caps, max_boxes=nb)
+            pipes.append(pp)
+        runner = mp.PipelinedRunner(pipes, device=dev)
+        for i in range(min(args.warmup, len(mine)) or 1):
+            e = mine[i % len(mine)] % P if mine else 0
+            runner.step(scores[e], frames, *det[e])
+        runner.wait_all()
+        torch.cuda.synchronize(dev)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0.record(stream)
+        for c in mine:
+            e = c % P
+            runner.step(scores[e], frames, *det[e])
+            mine_counters.add(ent_ctr[e])
+        runner.wait_all(stream)
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        for pp in pipes:
+            pp.check_status()
+        ms = t0.elapsed_time(t1) if mine else 0.0
+        tm = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        per_b.append((b, float(tm.item())))
+        del runner, pipes, det
+        torch.cuda.empty_cache()
+    total_ms = sum(t for _, t in per_b)
+    glob, _ = reduce_counters(mine_counters, total_ms, device=dev)
+    if rank == 0:
+        print(json.dumps({
+            "metric": "frames/sec of proxy-guided window pipeline", "value": glob.frames / (total_ms * 1e-3),
+            "unit": "frames/s", "n_gpus": world, "steps": 1, "warmup": args.warmup, "ms_per_step": total_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "clips": n_clips, "frames_per_clip": F, "thresholds": list(S.B_SWEEP),
+                       "clip_pool": P, "out_format": args.fmt, "sharding": "assign_clips LPT on positive-cell counts",
+                       "parallelism": f"clip-sharded x{world}", "host_numa": numa,
+                       "l2": "frames (11.2 GB) exceed L2; no flush",
+                       "stand_in": "device-generated, one jittered copy per object >= 25% inside a window"},
+            "per_threshold_ms": {str(b): t for b, t in per_b},
+            "counters": dataclasses.asdict(glob),
+            "gpu_launches": glob.clips * (mp.launches_per_call(0) + mp.launches_per_call(1) + mp.launches_per_call(2))
+        }), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -555,16 +770,18 @@ def run_wsel(args):
     cand = window_sets.candidate_sizes(cfg.W, cfg.H, Sset)
     p = mp.PlanParams(cfg.W, cfg.H, Sset, [cost(*x) for x in Sset])
     tot = torch.empty(len(cand), dtype=torch.int64, device=dev)
-    ws = torch.empty(mp.mp_window_set_cost_workspace_size(len(cand)), dtype=torch.uint8, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
     cc = [cost(*c) for c in cand]
+    cand_t = torch.tensor(cand, dtype=torch.int32, device=dev)
+    cc_t = torch.tensor(cc, dtype=torch.int64, device=dev)
     for _ in range(max(1, args.warmup)):
-        mp.mp_window_set_cost(p, lab, F, cand, cc, tot, ws)
+        mp.mp_window_set_cost(p, lab, F, cand_t, cc_t, tot, st)
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for _ in range(args.steps):
-        mp.mp_window_set_cost(p, lab, F, cand, cc, tot, ws)
+        mp.mp_window_set_cost(p, lab, F, cand_t, cc_t, tot, st)
     t1.record(stream)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
@@ -909,12 +1126,28 @@ def main():
     ap.add_argument("--src", default="rgb24", choices=["rgb24", "nv12"],
                     help="frame format: rgb24 rows (default) or NV12 decoder output with the proxy-input "
                          "downscale in the step (NEXT-3)")
-    ap.add_argument("--mode", default="path", choices=["path", "sweep", "wsel", "assign", "refine"],
-                    help="path: the hot path a1-a7 (default); sweep: NEXT-1 proxy-module sweep; "
+    ap.add_argument("--mode", default="path", choices=["path", "clips", "sweep", "wsel", "assign", "refine"],
+                    help="path: the hot path a1-a7 (default); clips: configs[4], 1000 clips sharded over the "
+                         "ranks with a B_proxy sweep; sweep: NEXT-1 proxy-module sweep; "
                          "wsel: NEXT-2 window-size selection step; assign: NEXT-4a batched Hungarian; "
                          "refine: NEXT-4b track refinement")
+    ap.add_argument("--clips", type=int, default=0, help="--mode clips: number of clips (default configs[4]'s 1000)")
+    ap.add_argument("--clip-pool", type=int, default=8,
+                    help="--mode clips: distinct generated clips the job draws on (clip c uses entry c mod pool)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU-only check of the multi-rank plumbing (gloo): clip assignment and counter reduction")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    env_world = os.environ.get("WORLD_SIZE")
+    if args.impl == "b200" and args.gpus > 1 and env_world is None:
+        # the contract's `bench.py --gpus N` without an outer launcher: start
+        # N ranks (one process per GPU) ourselves; rank 0 prints the line
+        return relaunch(args.gpus)
+    if args.impl == "b200" and env_world is not None and int(env_world) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={env_world} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.mode == "sweep":
@@ -925,6 +1158,8 @@ def main():
         return run_assign(args)
     if args.mode == "refine":
         return run_refine(args)
+    if args.mode == "clips":
+        return run_clips(args)
     return run_b200(args)
 
 

@@ -304,21 +304,22 @@ mp_status mp_proxy_sweep(const mp_plan_params* p, const float* d_scores, int32_t
  * the arg-min (ties: smaller area, then smaller w — reading R22) and repeats
  * k-1 times (paper_2103_14695_b200.window_sets.select_window_sizes).
  *
- *  p          the current set S (must contain (W,H)); p->b_proxy thresholds
- *             d_scores (pass a perfect-proxy 0/1 grid and e.g. 0.5).
- *  cand       host [n_cand] candidate sizes; cand_cost host [n_cand] their T;
- *             every S + {cand[c]} must be a valid set (R13, distinct sizes),
- *             else MP_ERR_INVALID.  |S| <= 15.
- *  d_tot      device int64 [n_cand] (overwritten).
- *  d_ws       device scratch, mp_window_set_cost_workspace_size(n_cand) bytes.
- *  This offline call copies the candidate table to the device and
- *  synchronises the stream once (not graph-capturable).
+ *  p           the current set S (must contain (W,H)), |S| <= 15; p->b_proxy
+ *              thresholds d_scores (pass a perfect-proxy 0/1 grid and e.g. 0.5).
+ *  d_cand      device mp_size [n_cand] candidate sizes; d_cand_cost device
+ *              int64 [n_cand] their T.  Each S + {cand[c]} must be a valid set
+ *              (R13/R14: inside the frame, distinct from S, T > 0, strictly
+ *              monotone in area against S) — checked ON THE DEVICE: an invalid
+ *              candidate gets tot[c] = INT64_MAX (never the arg-min) and
+ *              *d_status = MP_ERR_INVALID.
+ *  d_tot       device int64 [n_cand] (overwritten).
+ *  Launches: window_set_init + window_set_cost; no host copy or
+ *  synchronisation (graph-capturable).  Split the candidates across GPUs
+ *  and take the arg-min of the per-GPU arg-mins (window_sets.py).
  */
-size_t mp_window_set_cost_workspace_size(int32_t n_cand);
-
-mp_status mp_window_set_cost(const mp_plan_params* p, const float* d_scores, int32_t F, const mp_size* cand,
-                             const int64_t* cand_cost, int32_t n_cand, int64_t* d_tot, void* d_ws,
-                             size_t ws_bytes, void* stream);
+mp_status mp_window_set_cost(const mp_plan_params* p, const float* d_scores, int32_t F, const mp_size* d_cand,
+                             const int64_t* d_cand_cost, int32_t n_cand, int64_t* d_tot, int32_t* d_status,
+                             void* stream);
 
 /* ---------------------------------------------------------------------------
  * NEXT-4a: Hungarian matching of detections to track prefixes (PAPER.md:207

@@ -12,7 +12,7 @@ from ._binding import (MP_BT601_FULL, MP_BT601_LIMITED, MP_BT709_FULL, MP_BT709_
                        mp_gather_resize, mp_gather_resize_nv12, mp_gather_resize_strided, mp_gather_workspace_size,
                        mp_plan_windows, mp_plan_workspace_size,
                        mp_proxy_sweep, mp_proxy_sweep_workspace_size, mp_remap_nms, mp_remap_nms_workspace_size,
-                       mp_window_set_cost, mp_window_set_cost_workspace_size, status_string,
+                       mp_window_set_cost, status_string,
                        ASSIGN_PROBLEM_DTYPE, assign_problems, mp_hungarian, mp_hungarian_workspace_size,
                        mp_track_resample, mp_dbscan, mp_dbscan_workspace_size, mp_cluster_centers,
                        mp_refine_workspace_size, mp_refine_tracks)

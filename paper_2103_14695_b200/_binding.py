@@ -71,10 +71,8 @@ def _load():
     L.mp_proxy_sweep_workspace_size.argtypes = [C.POINTER(mp_plan_params), i32]
     L.mp_proxy_sweep.restype = C.c_int
     L.mp_proxy_sweep.argtypes = [C.POINTER(mp_plan_params), vp, i32, vp, i32, vp, vp, vp, vp, sz, vp]
-    L.mp_window_set_cost_workspace_size.restype = sz
-    L.mp_window_set_cost_workspace_size.argtypes = [i32]
     L.mp_window_set_cost.restype = C.c_int
-    L.mp_window_set_cost.argtypes = [C.POINTER(mp_plan_params), vp, i32, vp, vp, i32, vp, vp, sz, vp]
+    L.mp_window_set_cost.argtypes = [C.POINTER(mp_plan_params), vp, i32, vp, vp, i32, vp, vp, vp]
     L.mp_hungarian_workspace_size.restype = sz
     L.mp_hungarian_workspace_size.argtypes = [i32]
     L.mp_hungarian.restype = C.c_int
@@ -105,7 +103,7 @@ _lib = _load()
 
 EXPORTED = ("mp_plan_workspace_size", "mp_plan_windows", "mp_gather_workspace_size", "mp_gather_resize",
             "mp_gather_resize_strided", "mp_proxy_sweep_workspace_size", "mp_proxy_sweep",
-            "mp_window_set_cost_workspace_size", "mp_window_set_cost",
+            "mp_window_set_cost",
             "mp_remap_nms_workspace_size", "mp_remap_nms", "mp_status_string", "mp_launches_per_call")
 
 
@@ -352,21 +350,21 @@ def mp_proxy_sweep(params: PlanParams, scores, F, thresholds, dets, det_off, out
         raise MPError(st, "mp_proxy_sweep")
 
 
-def mp_window_set_cost_workspace_size(n_cand: int) -> int:
-    return int(_lib.mp_window_set_cost_workspace_size(int(n_cand)))
-
-
-def mp_window_set_cost(params: PlanParams, scores, F, cand, cand_cost, tot, ws, stream=None) -> None:
+def mp_window_set_cost(params: PlanParams, scores, F, cand, cand_cost, tot, status, stream=None) -> None:
     """NEXT-2 greedy-step objective: tot[c] = sum_t
-    est(R(I_t; S + {cand[c]})).  cand: host list of (w, h); cand_cost: host
-    list of T; tot int64 CUDA tensor [n_cand]."""
+    est(R(I_t; S + {cand[c]})).  cand int32 CUDA tensor [n_cand, 2] (w, h);
+    cand_cost int64 CUDA [n_cand]; tot int64 CUDA [n_cand]; status int32
+    CUDA [1] (MP_ERR_INVALID for invalid candidates, whose tot = INT64_MAX)."""
     _dev(scores, torch.float32, "scores")
+    _dev(cand, torch.int32, "cand")
+    _dev(cand_cost, torch.int64, "cand_cost")
     _dev(tot, torch.int64, "tot")
-    _dev(ws, torch.uint8, "ws")
-    n = len(cand)
-    cs = (C.c_int64 * max(n, 1))(*[int(c) for c in cand_cost])
-    st = _lib.mp_window_set_cost(C.byref(params.c), _p(scores), int(F), _sizes(cand) if n else None, cs, n, _p(tot),
-                                 _p(ws), ws.numel(), _stream(stream))
+    _dev(status, torch.int32, "status")
+    n = int(cand.shape[0])
+    if cand.dim() != 2 or cand.shape[1] != 2 or cand_cost.numel() < n or tot.numel() < n:
+        raise ValueError("cand must be [n, 2] int32 with n costs and n totals")
+    st = _lib.mp_window_set_cost(C.byref(params.c), _p(scores), int(F), _p(cand), _p(cand_cost), n, _p(tot),
+                                 _p(status), _stream(stream))
     if st != MP_OK:
         raise MPError(st, "mp_window_set_cost")
 

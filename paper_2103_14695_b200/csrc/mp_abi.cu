@@ -17,6 +17,7 @@ extern "C" const char* mp_status_string(mp_status st) {
 //   gather: gather_prep + gather_kernel
 //   remap_nms: memset (not a kernel) + tiny + small + large + scan + scatter
 //   proxy_sweep: memset (not a kernel) + proxy_sweep_kernel
+//   window_set_cost: window_set_init + window_set_cost
 //   hungarian: memset (not a kernel) + hung_warp_kernel + hung_mid_kernel (max_dim > 64)
 //              + hung_block_kernel (max_dim > 160)
 //   track_resample: 1;  dbscan: memset + adj + core + union + root + scan + label + scan + noise (8);
@@ -27,7 +28,7 @@ extern "C" int32_t mp_launches_per_call(int32_t which) {
     case 1: return 2;
     case 2: return 5;
     case 3: return 1;
-    case 4: return 1;
+    case 4: return 2;
     case 5: return 3;
     case 6: return 1;
     case 7: return 8;

@@ -969,7 +969,8 @@ extern "C" mp_status mp_gather_resize(const uint8_t* const* d_frame_ptrs, int32_
   GatherArgs A;
   if (!build_gather_args(kSrcRGB24, false, pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A))
     return MP_ERR_INVALID;
-  if (!d_frame_off || !d_status || (F > 0 && (!d_frame_ptrs || !d_windows))) return MP_ERR_INVALID;
+  if (!d_frame_off || !d_status || (F > 0 && (!d_frame_ptrs || (max_windows > 0 && !d_windows))))
+    return MP_ERR_INVALID;
   if (max_windows < 0) return MP_ERR_INVALID;
   A.max_windows = max_windows;
   TmapArray tm;
@@ -1037,7 +1038,8 @@ extern "C" mp_status mp_gather_resize_strided(const uint8_t* d_frames, int64_t f
   if (!build_gather_args(kSrcRGB24, rows, pitch, W, H, F, k, sizes, out_dims, d_out, out_cap, fmt, &A))
     return MP_ERR_INVALID;
   A.rpf = rows ? (int)(frame_stride / pitch) : 0;
-  if (!d_frame_off || !d_status || (F > 0 && (!d_frames || !d_windows))) return MP_ERR_INVALID;
+  if (!d_frame_off || !d_status || (F > 0 && (!d_frames || (max_windows > 0 && !d_windows))))
+    return MP_ERR_INVALID;
   if (max_windows < 0) return MP_ERR_INVALID;
   A.max_windows = max_windows;
   if (F > 0 && (((uintptr_t)d_frames) & 15)) return MP_ERR_INVALID;
@@ -1093,7 +1095,8 @@ extern "C" mp_status mp_gather_resize_nv12(const uint8_t* d_frames, int64_t fram
     return MP_ERR_INVALID;
   A.rpf = rows ? (int)(frame_stride / pitch) : 0;
   if (!nv12_coefficients((int)matrix, A.cvt)) return MP_ERR_INVALID;
-  if (!d_frame_off || !d_status || (F > 0 && (!d_frames || !d_windows))) return MP_ERR_INVALID;
+  if (!d_frame_off || !d_status || (F > 0 && (!d_frames || (max_windows > 0 && !d_windows))))
+    return MP_ERR_INVALID;
   if (max_windows < 0) return MP_ERR_INVALID;
   A.max_windows = max_windows;
   if (F > 0 && (((uintptr_t)d_frames) & 15)) return MP_ERR_INVALID;

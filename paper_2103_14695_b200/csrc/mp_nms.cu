@@ -760,7 +760,7 @@ extern "C" mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_bo
     return MP_ERR_INVALID;
   if (!d_out_frame_off || !d_status || !d_frame_off || !d_win_box_off) return MP_ERR_INVALID;
   if (max_out > 0 && (!d_out || !d_out_src)) return MP_ERR_INVALID;
-  if (F > 0 && (!d_windows || (max_boxes > 0 && !d_boxes))) return MP_ERR_INVALID;
+  if (F > 0 && ((max_windows > 0 && !d_windows) || (max_boxes > 0 && !d_boxes))) return MP_ERR_INVALID;
   if (!(iou_thr == iou_thr) || !(score_thr == score_thr)) return MP_ERR_INVALID;
   NmsArgs A;
   memset(&A, 0, sizeof(A));

@@ -707,30 +707,61 @@ __global__ void __launch_bounds__(kSweepThreads) proxy_sweep_kernel(PlanArgs P, 
 constexpr int kSelThreads = 128;
 constexpr int kSelCandPerBlock = 16;
 
+// R13/R14 for S + {candidate}: 1 <= w <= W, 1 <= h <= H, distinct from every
+// size of S, T > 0, and strictly monotone in area against every size of S.
+__device__ __forceinline__ bool cand_valid(const PlanArgs& P, int w, int h, long long t) {
+  if (w < 1 || h < 1 || w > P.W || h > P.H || t <= 0) return false;
+  const long long ac = (long long)w * h;
+  for (int q = 0; q < P.k; q++) {
+    if (P.sw[q] == w && P.sh[q] == h) return false;
+    const long long aq = (long long)P.sw[q] * P.sh[q];
+    if (aq < ac && !(P.cost[q] < t)) return false;
+    if (ac < aq && !(t < P.cost[q])) return false;
+  }
+  return true;
+}
+
+// tot[c] = 0 for valid candidates, INT64_MAX (never the arg-min) and
+// *d_status = MP_ERR_INVALID for invalid ones.
+__global__ void window_set_init_kernel(PlanArgs P, const mp_size* __restrict__ cand,
+                                       const long long* __restrict__ cand_cost, int n_cand,
+                                       long long* __restrict__ tot, int* __restrict__ d_status) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_cand; c += gridDim.x * blockDim.x) {
+    const mp_size cd = cand[c];
+    const bool ok = cand_valid(P, cd.w, cd.h, cand_cost[c]);
+    tot[c] = ok ? 0 : 0x7fffffffffffffffLL;
+    if (!ok) set_status(d_status, MP_ERR_INVALID);
+  }
+}
+
 // grid (F, ceil(n_cand / kSelCandPerBlock)): the CTA plans frame f once per
 // candidate size, with S' = S + {candidate} (order re-derived by (area, w, h)),
 // in estimate-only mode, and adds est(R(I_f; S')) to tot[c].
 __global__ void __launch_bounds__(kSelThreads) window_set_cost_kernel(PlanArgs P, const float* __restrict__ scores,
-                                                                      const int4* __restrict__ cand, int n_cand,
+                                                                      const mp_size* __restrict__ cand,
+                                                                      const long long* __restrict__ cand_cost,
+                                                                      int n_cand,
                                                                       unsigned long long* __restrict__ tot) {
   __shared__ long long s_est;
   const int f = blockIdx.x;
   const int c0 = blockIdx.y * kSelCandPerBlock, c1 = min(n_cand, c0 + kSelCandPerBlock);
   for (int c = c0; c < c1; c++) {
-    const int4 cd = cand[c];   // (w, h, cost lo, cost hi)
+    const mp_size cd = cand[c];
+    const long long ct = cand_cost[c];
+    if (!cand_valid(P, cd.w, cd.h, ct)) continue;   // (uniform across the CTA)
     PlanArgs Q = P;
     const int kk = P.k;
-    Q.sw[kk] = cd.x;
-    Q.sh[kk] = cd.y;
-    Q.cost[kk] = (long long)(((unsigned long long)(unsigned)cd.w << 32) | (unsigned)cd.z);
+    Q.sw[kk] = cd.w;
+    Q.sh[kk] = cd.h;
+    Q.cost[kk] = ct;
     Q.k = kk + 1;
     // insert the candidate into the (area, w, h) order
-    const long long ac = (long long)cd.x * cd.y;
+    const long long ac = (long long)cd.w * cd.h;
     int pos = kk;
     for (int q = 0; q < kk; q++) {
       const int i = P.order[q];
       const long long ai = (long long)P.sw[i] * P.sh[i];
-      if (ac < ai || (ac == ai && (cd.x < P.sw[i] || (cd.x == P.sw[i] && cd.y < P.sh[i])))) {
+      if (ac < ai || (ac == ai && (cd.w < P.sw[i] || (cd.w == P.sw[i] && cd.h < P.sh[i])))) {
         pos = q;
         break;
       }
@@ -915,63 +946,29 @@ extern "C" mp_status mp_proxy_sweep(const mp_plan_params* p, const float* d_scor
   return MP_OK;
 }
 
-extern "C" size_t mp_window_set_cost_workspace_size(int32_t n_cand) {
-  return n_cand < 0 ? 0 : ((size_t)n_cand * sizeof(int4) + 255) / 256 * 256 + 256;
-}
-
 extern "C" mp_status mp_window_set_cost(const mp_plan_params* p, const float* d_scores, int32_t F,
-                                        const mp_size* cand, const int64_t* cand_cost, int32_t n_cand,
-                                        int64_t* d_tot, void* d_ws, size_t ws_bytes, void* stream) {
+                                        const mp_size* d_cand, const int64_t* d_cand_cost, int32_t n_cand,
+                                        int64_t* d_tot, int32_t* d_status, void* stream) {
   PlanArgs A;
   mp_status err;
   if (!build_plan_args(p, &A, &err)) return err;
   if (A.k >= kMaxClasses) return MP_ERR_UNSUPPORTED;
-  if (F < 0 || n_cand < 0 || (n_cand > 0 && (!cand || !cand_cost || !d_tot))) return MP_ERR_INVALID;
+  if (F < 0 || n_cand < 0 || (n_cand > 0 && (!d_cand || !d_cand_cost || !d_tot || !d_status))) return MP_ERR_INVALID;
   if (F > 0 && !d_scores) return MP_ERR_INVALID;
   if (n_cand == 0) return MP_OK;
-  if (!d_ws || ws_bytes < mp_window_set_cost_workspace_size(n_cand)) return MP_ERR_INVALID;
-  // every S + {candidate} must itself be a valid size set (R13/R14)
-  int4* h = (int4*)malloc(sizeof(int4) * (size_t)n_cand);
-  if (!h) return MP_ERR_INVALID;
-  for (int c = 0; c < n_cand; c++) {
-    mp_size sz[kMaxClasses];
-    int64_t cs[kMaxClasses];
-    for (int q = 0; q < p->k; q++) {
-      sz[q] = p->sizes[q];
-      cs[q] = p->cost[q];
-    }
-    sz[p->k] = cand[c];
-    cs[p->k] = cand_cost[c];
-    mp_plan_params pc = *p;
-    pc.k = p->k + 1;
-    pc.sizes = sz;
-    pc.cost = cs;
-    PlanArgs tmp;
-    if (!build_plan_args(&pc, &tmp, &err)) {
-      free(h);
-      return MP_ERR_INVALID;
-    }
-    h[c] = make_int4(cand[c].w, cand[c].h, (int)(uint32_t)((uint64_t)cand_cost[c] & 0xffffffffu),
-                     (int)(uint32_t)((uint64_t)cand_cost[c] >> 32));
-  }
   cudaStream_t s = (cudaStream_t)stream;
-  int4* d_cand = (int4*)d_ws;
-  // host -> device copy of the candidate table: stream-ordered from pageable
-  // memory (the call is therefore not graph-capturable; it is an offline step)
-  cudaError_t e = cudaMemcpyAsync(d_cand, h, sizeof(int4) * (size_t)n_cand, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  free(h);
-  if (e != cudaSuccess) {
-    (void)cudaGetLastError();
-    return MP_ERR_CUDA;
-  }
-  MP_CUDA_TRY(cudaMemsetAsync(d_tot, 0, sizeof(int64_t) * (size_t)n_cand, s));
-  if (F == 0) return MP_OK;
   const size_t smem = plan_smem_bytes(A.R, A.words, A.maxc, nullptr, nullptr);
   if (smem > 227 * 1024) return MP_ERR_UNSUPPORTED;
+  // candidates are validated on the device (R13/R14 against S): no host copy,
+  // no synchronisation, graph-capturable
+  window_set_init_kernel<<<(n_cand + 255) / 256, 256, 0, s>>>(A, d_cand, (const long long*)d_cand_cost, n_cand,
+                                                               (long long*)d_tot, d_status);
+  MP_CUDA_TRY(cudaGetLastError());
+  if (F == 0) return MP_OK;
   MP_CUDA_TRY(cudaFuncSetAttribute(window_set_cost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid(F, (n_cand + kSelCandPerBlock - 1) / kSelCandPerBlock);
-  window_set_cost_kernel<<<grid, kSelThreads, smem, s>>>(A, d_scores, d_cand, n_cand, (unsigned long long*)d_tot);
+  window_set_cost_kernel<<<grid, kSelThreads, smem, s>>>(A, d_scores, d_cand, (const long long*)d_cand_cost, n_cand,
+                                                         (unsigned long long*)d_tot);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }

@@ -75,3 +75,54 @@ def reduce_counters(c: Counters, elapsed_ms: float, device="cpu", group=None):
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
         dist.all_reduce(e, op=dist.ReduceOp.MAX, group=group)
     return Counters.from_tensor(t.cpu()), float(e.item())
+
+
+# --------------------------------------------------------------------------- host placement
+def gpu_numa_node(device_index: int, sysfs: str = "/sys") -> Optional[int]:
+    """NUMA node of a CUDA device (from its PCI bus id in sysfs), or None when
+    unknown (no GPU, no NUMA info, or a single-node host reporting -1)."""
+    try:
+        props = torch.cuda.get_device_properties(device_index)
+        bus = "%04x:%02x:%02x.0" % (props.pci_domain_id, props.pci_bus_id, props.pci_device_id)
+    except Exception:   # no CUDA device / attribute missing
+        return None
+    return pci_numa_node(bus, sysfs)
+
+
+def pci_numa_node(bus_id: str, sysfs: str = "/sys") -> Optional[int]:
+    import os
+    try:
+        v = int(open(os.path.join(sysfs, "bus", "pci", "devices", bus_id.lower(), "numa_node")).read().strip())
+    except (OSError, ValueError):
+        return None
+    return v if v >= 0 else None
+
+
+def node_cpus(node: int, sysfs: str = "/sys") -> List[int]:
+    """CPU ids of a NUMA node from its sysfs cpulist ("0-15,64-79")."""
+    import os
+    txt = open(os.path.join(sysfs, "devices", "system", "node", f"node{node}", "cpulist")).read().strip()
+    cpus: List[int] = []
+    for part in filter(None, txt.split(",")):
+        a, _, b = part.partition("-")
+        cpus.extend(range(int(a), int(b or a) + 1))
+    return cpus
+
+
+def bind_host_to_gpu(device_index: int, sysfs: str = "/sys") -> dict:
+    """Restrict this process's host threads to the CPUs of the GPU's NUMA
+    node, so pinned host buffers allocated afterwards (first touch) sit on
+    the socket whose PCIe root complex serves that GPU — zero-copy frame
+    reads (the e2e leg) then never cross the inter-socket link.  Returns a
+    record of what was done (no-op without NUMA information)."""
+    import os
+    node = gpu_numa_node(device_index, sysfs)
+    if node is None:
+        return {"numa_node": None, "bound": False}
+    try:
+        cpus = sorted(set(node_cpus(node, sysfs)) & set(os.sched_getaffinity(0)))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        return {"numa_node": node, "bound": bool(cpus), "cpus": len(cpus)}
+    except (OSError, AttributeError, ValueError):
+        return {"numa_node": node, "bound": False}

@@ -71,3 +71,87 @@ def test_gpu_window_selection_parity(name, frames, k, step):
     got_sizes, got_hist = window_sets.select_window_sizes(torch.from_numpy(lab).cuda(), cfg.W, cfg.H, k, cost_fn,
                                                           step=step)
     assert got_sizes == ref_sizes and got_hist == ref_hist
+
+
+# --------------------------------------------------------------------------- NEXT-2 across ranks (gloo)
+def _oracle_evaluator(lab, W, H):
+    """Test-side evaluation of one greedy step's objective with the oracle
+    (the GPU kernel cannot run here); the distributed selection logic around
+    it is the product code of window_sets.py."""
+    def ev(S_, S_cost, cand, cand_cost):
+        if not cand:
+            return []
+        st, tot = O.window_set_cost(W, H, 32, 32, 0.5, S_, S_cost, lab, cand, cand_cost)
+        assert st == 0
+        return [int(t) for t in tot]
+    return ev
+
+
+def _wsel_worker(rank, world, port, out):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2103_14695_b200 import window_sets
+    cfg, lab = _labels("c1_540p", 4, 6)
+    sizes, hist = window_sets.select_window_sizes(None, cfg.W, cfg.H, 3, cost_fn, step=64,
+                                                  evaluate=_oracle_evaluator(lab, cfg.W, cfg.H))
+    out.put((rank, sizes, hist))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_window_selection_split_across_ranks(world):
+    """Candidates split round-robin over `world` gloo ranks, one all-gather of
+    per-rank arg-min keys per greedy step: every rank returns the oracle's
+    single-process selection (sizes and objectives)."""
+    import socket
+    import torch.multiprocessing as mpr
+    pytest.importorskip("paper_2103_14695_b200", exc_type=ImportError)
+    cfg, lab = _labels("c1_540p", 4, 6)
+    ref_sizes, ref_hist = O.select_window_sizes(cfg.W, cfg.H, 32, 32, lab, 3, cost_fn, step=64)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mpr.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_wsel_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, sizes, hist in res:
+        assert sizes == ref_sizes and hist == ref_hist, rank
+
+
+@pytest.mark.gpu
+def test_gpu_window_set_cost_device_validation():
+    """Candidates are validated on the device (no host copy / sync): an
+    invalid one (a size already in S, outside the frame, non-monotone cost)
+    gets tot = INT64_MAX and sets MP_ERR_INVALID; valid ones equal the
+    oracle's objectives."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2103_14695_b200 as mp
+    cfg, lab = _labels("c1_540p", 6, 10)
+    S0 = [(cfg.W, cfg.H), (256, 256)]
+    S0c = [cost_fn(*s) for s in S0]
+    cand = [(128, 128), (256, 256), (2000, 64), (512, 512), (64, 64)]
+    cc = [cost_fn(128, 128), 80, 10, 1, cost_fn(64, 64)]      # (512,512) cost 1 < T(256^2): non-monotone
+    p = mp.PlanParams(cfg.W, cfg.H, S0, S0c)
+    tot = torch.empty(len(cand), dtype=torch.int64, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    mp.mp_window_set_cost(p, torch.from_numpy(lab).cuda(), lab.shape[0], torch.tensor(cand, dtype=torch.int32).cuda(),
+                          torch.tensor(cc, dtype=torch.int64).cuda(), tot, st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == mp.MP_ERR_INVALID
+    t = tot.cpu().tolist()
+    assert t[1] == t[2] == t[3] == (1 << 63) - 1
+    ok = [0, 4]
+    sr, ref = O.window_set_cost(cfg.W, cfg.H, 32, 32, 0.5, S0, S0c, lab, [cand[i] for i in ok], [cc[i] for i in ok])
+    assert [t[i] for i in ok] == [int(x) for x in ref]

@@ -209,6 +209,15 @@ def _lane(rng, W, H):
     return pts, np.concatenate([[0.0], np.cumsum(seg)])
 
 
+def clip_cost_estimate(cfg: Config, clip: int) -> float:
+    """A clip's expected objects per frame (the density `make_scene` draws
+    first from the clip seed) — a cheap per-clip cost estimate for
+    longest-processing-time sharding, without generating the clip."""
+    rng = np.random.default_rng(clip_seed(clip))
+    rng.integers(cfg.lanes[0], cfg.lanes[1] + 1)
+    return float(rng.uniform(*cfg.obj_range))
+
+
 def make_scene(cfg: Config, clip: int, n_frames: Optional[int] = None, frame0: int = 0) -> Scene:
     """Objects for frames [frame0, frame0+n_frames) of a clip."""
     F = cfg.frames if n_frames is None else n_frames
@@ -442,3 +451,71 @@ def track_sets(seed: int, n_train: int = 2000, n_query: int = 4000, n_lanes: int
         query.append(boxes_of(q))
         qlane.append(li)
     return lanes, train, query, np.asarray(qlane)
+
+
+# --------------------------------------------------------------------------- configs[4] clip pools
+def clip_pool(cfg: Config, pool: int) -> List[Tuple[Scene, np.ndarray]]:
+    """The `pool` distinct generated clips the configs[4] sweep draws on:
+    (scene, score grids) of clip ids 0..pool-1.  Clip c of the 1000-clip job
+    uses pool entry c mod pool (host generation of 1000 full clips would take
+    ~25 min; the kernels keep nothing from one clip to the next, so reusing
+    a clip's data costs the same work as a new clip)."""
+    out = []
+    for c in range(pool):
+        sc = make_scene(cfg, c)
+        out.append((sc, score_grids(cfg, c, sc)))
+    return out
+
+
+def standin_boxes_torch(cfg: Config, clip: int, obj_boxes, obj_cls, obj_off, windows, device):
+    """Vectorised stand-in detector on the device (torch, untimed input
+    generation for the configs[4] sweep): per window, ONE jittered copy
+    (sigma = 1 detector px) of (object ∩ window) for every object of the
+    window's frame with >= 25 % of its area inside, score U[0.3, 1], cls =
+    the object's class — the same model as `standin_boxes` without the
+    Poisson extra copies and false positives.  obj_boxes float64 [n_obj, 4]
+    (frame px), obj_cls int32 [n_obj], obj_off int64 [F+1] (per-frame CSR),
+    windows int32 [n_win, 7] (device).  Returns (boxes float32 [n_box, 6]
+    with cls bits in column 5, win_box_off int32 [n_win+1])."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(clip_seed(clip) & ((1 << 63) - 1))
+    n_win = int(windows.shape[0])
+    if n_win == 0:
+        return torch.zeros((1, 6), dtype=torch.float32, device=device), torch.zeros(1, dtype=torch.int32, device=device)
+    ob = torch.as_tensor(obj_boxes, dtype=torch.float64, device=device)
+    oc = torch.as_tensor(obj_cls, dtype=torch.int32, device=device)
+    off = torch.as_tensor(obj_off, dtype=torch.int64, device=device)
+    cnt = off[1:] - off[:-1]
+    kmax = int(cnt.max().item()) if len(cnt) else 0
+    w = windows.to(torch.int64)
+    fr = w[:, 0]
+    if kmax == 0:
+        return torch.zeros((1, 6), dtype=torch.float32, device=device), torch.zeros(n_win + 1, dtype=torch.int32,
+                                                                                    device=device)
+    j = torch.arange(kmax, device=device)
+    valid = j[None, :] < cnt[fr][:, None]                                   # [n_win, kmax]
+    idx = (off[fr][:, None] + j[None, :]).clamp(max=max(len(ob) - 1, 0))
+    b = ob[idx]                                                              # [n_win, kmax, 4]
+    x, y, ww, hh = (w[:, i].to(torch.float64)[:, None] for i in (1, 2, 3, 4))
+    ix1, iy1 = torch.maximum(b[..., 0], x), torch.maximum(b[..., 1], y)
+    ix2, iy2 = torch.minimum(b[..., 2], x + ww), torch.minimum(b[..., 3], y + hh)
+    inter = (ix2 - ix1).clamp(min=0) * (iy2 - iy1).clamp(min=0)
+    area = (b[..., 2] - b[..., 0]) * (b[..., 3] - b[..., 1])
+    keep = valid & (inter >= 0.25 * area)
+    wi, oj = torch.nonzero(keep, as_tuple=True)                              # window-major order
+    od = torch.as_tensor(cfg.out_dims, dtype=torch.float64, device=device)[w[wi, 5]]
+    sx, sy = od[:, 0] / ww[wi, 0], od[:, 1] / hh[wi, 0]
+    loc = torch.stack([(ix1[wi, oj] - x[wi, 0]) * sx, (iy1[wi, oj] - y[wi, 0]) * sy,
+                       (ix2[wi, oj] - x[wi, 0]) * sx, (iy2[wi, oj] - y[wi, 0]) * sy], 1)
+    loc = loc + torch.randn(loc.shape, generator=g, dtype=torch.float64, device=device)
+    score = 0.3 + 0.7 * torch.rand(len(wi), generator=g, dtype=torch.float64, device=device)
+    n_box = len(wi)
+    out = torch.empty((max(n_box, 1), 6), dtype=torch.float32, device=device)
+    if n_box:
+        out[:n_box, :4] = loc.to(torch.float32)
+        out[:n_box, 4] = score.to(torch.float32)
+        out[:n_box, 5] = oc[idx[wi, oj]].view(torch.float32)
+    wbo = torch.zeros(n_win + 1, dtype=torch.int32, device=device)
+    wbo[1:] = torch.cumsum(torch.bincount(wi, minlength=n_win), 0).to(torch.int32)
+    return out, wbo
