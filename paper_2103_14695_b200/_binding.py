@@ -20,7 +20,9 @@ import numpy as _np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmp_b200.so")
+# MP_LIB (development A/B runs only) points the binding at another build of
+# the same library; by default the in-tree libmp_b200.so is loaded.
+LIB_PATH = os.environ.get("MP_LIB") or os.path.join(_HERE, "libmp_b200.so")
 
 MP_OK, MP_ERR_INVALID, MP_ERR_CUDA, MP_ERR_CAPACITY, MP_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 MP_OUT_F32_NCHW, MP_OUT_U8_NHWC = 0, 1

@@ -114,6 +114,25 @@ __device__ __forceinline__ void tap(int in, int out, int d, int& i0, float& lam)
   lam = __fdiv_rn((float)rem, (float)(2 * out));
 }
 
+// Packed f32x2 FMA on 64-bit register pairs (PTX fma.rn.f32x2, sm_100+): an
+// operand kept as ONE b64 value stays in an aligned register pair, so the
+// per-column weight pairs are not re-packed (2 MOVs) before every FFMA2.
+__device__ __forceinline__ unsigned long long pk2(float2 v) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ float2 ffma2_w(float2 a, unsigned long long w, float2 c) {   // a * w + c
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a)), "l"(w), "l"(pk2(c)));
+  return upk2(r);
+}
+
 __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {   // packed a - b (FADD2 with negated operand)
   return __fadd2_rn(a, make_float2(-b.x, -b.y));
 }
@@ -139,6 +158,11 @@ __device__ __forceinline__ float clamp255(float v) {
 // float->int conversion (v + 0.5 rounded in fp32, as the R16 decision is).
 __device__ __forceinline__ float2 u8_round2(float2 v) {
   return __fadd2_rd(__fadd2_rn(v, make_float2(0.5f, 0.5f)), make_float2(8388608.0f, 8388608.0f));
+}
+
+// floor(v) of values already offset by +0.5 (see kHalf in consume_tile)
+__device__ __forceinline__ float2 u8_floor2(float2 v) {
+  return __fadd2_rd(v, make_float2(8388608.0f, 8388608.0f));
 }
 
 __device__ __forceinline__ int tiles_total(const GatherArgs& A, const int* cnt) {
@@ -231,10 +255,14 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
   const int R = (rows + kCW - 1) / kCW;
   const int rb0 = wid * R, rb1 = min(rows, rb0 + R);
   if (rb0 >= rb1 || lane >= cols) return;
-  const float2 M2 = make_float2(8388608.0f, 8388608.0f);
+  // u8 output from RGB24: the +0.5 of R16's floor(v + 0.5) is folded into the
+  // horizontal lerps (m - (2^23 - 0.5) = byte + 0.5 exactly; lerps of offset
+  // values are offset lerps), so the rounding below is one packed add
+  constexpr bool kHalf = FMT == MP_OUT_U8_NHWC && SRC == kSrcRGB24;
+  const float2 M2 = kHalf ? make_float2(8388607.5f, 8388607.5f) : make_float2(8388608.0f, 8388608.0f);
   unsigned int ba[NP], bb[NP];
   unsigned int ca[NP], cb[NP], da[NP], db[NP];   // NV12: chroma byte of the left tap, +0/+2 to the right tap
-  float2 lx[NP];
+  unsigned long long lx[NP];   // (lambda of column A, lambda of column B) as one b64 pair
 #pragma unroll
   for (int p = 0; p < NP; p++) {
     const int cA = lane + 64 * p, cB = cA + 32;
@@ -255,14 +283,14 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
       ba[p] = doff + x0 + 3 * xa.x;
       bb[p] = doff + x0 + 3 * xb.x;
     }
-    lx[p] = make_float2(__int_as_float(xa.y), __int_as_float(xb.y));
+    lx[p] = pk2(make_float2(__int_as_float(xa.y), __int_as_float(xb.y)));
   }
   float2 P[NP][3], N[NP][3];   // ping-pong horizontal lerps (3 channels x column pair)
 #define MP_HL(H, CH, A0, B0, A1, B1)                                                           \
   {                                                                                             \
     const float2 m_ = make_float2(u8m(smem[A0]), u8m(smem[B0]));                                \
     const float2 n_ = make_float2(u8m(smem[A1]), u8m(smem[B1]));                                \
-    H[p][CH] = __ffma2_rn(lx[p], fsub2(n_, m_), fsub2(m_, M2));                                  \
+    H[p][CH] = ffma2_w(fsub2(n_, m_), lx[p], fsub2(m_, M2));                                     \
   }
   // NV12 chroma: one 16-bit load per tap fetches the (U, V) pair; bytes are
   // placed into the 2^23 fp32 pattern with one byte-permute each
@@ -276,8 +304,8 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
     const float2 nu_ = make_float2(uvf(ra_, 0x7540), uvf(rb_, 0x7540));                         \
     const float2 mv_ = make_float2(uvf(la_, 0x7541), uvf(lb_, 0x7541));                         \
     const float2 nv_ = make_float2(uvf(ra_, 0x7541), uvf(rb_, 0x7541));                         \
-    H[p][1] = __ffma2_rn(lx[p], fsub2(nu_, mu_), fsub2(mu_, M2));                                \
-    H[p][2] = __ffma2_rn(lx[p], fsub2(nv_, mv_), fsub2(mv_, M2));                                \
+    H[p][1] = ffma2_w(fsub2(nu_, mu_), lx[p], fsub2(mu_, M2));                                   \
+    H[p][2] = ffma2_w(fsub2(nv_, mv_), lx[p], fsub2(mv_, M2));                                   \
   }
   // NV12 luma only (the chroma lerps are copied from PREV: same chroma row)
 #define MP_HY(O_, H, PREV)                                                                      \
@@ -387,7 +415,9 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
     const float2 ly = make_float2(__int_as_float(y.y), __int_as_float(y.y));                    \
     _Pragma("unroll") for (int p = 0; p < NP; p++) {                                            \
       MP_V(T, B)                                                                                \
-      const float2 r0 = u8_round2(v0), r1 = u8_round2(v1), r2 = u8_round2(v2);                   \
+      const float2 r0 = kHalf ? u8_floor2(v0) : u8_round2(v0);                                  \
+      const float2 r1 = kHalf ? u8_floor2(v1) : u8_round2(v1);                                  \
+      const float2 r2 = kHalf ? u8_floor2(v2) : u8_round2(v2);                                  \
       if (ok[2 * p]) {                                                                          \
         o[192 * p + 0] = (uint8_t)__float_as_uint(r0.x);                                        \
         o[192 * p + 1] = (uint8_t)__float_as_uint(r1.x);                                        \

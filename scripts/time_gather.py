@@ -74,7 +74,8 @@ def main():
             w = p.windows[:n].cpu().numpy()
             out_b = sum((12 if FMT == 0 else 3) * cfg.out_dims[q][0] * cfg.out_dims[q][1] for q in w[:, 5])
             rd = bpp * sum(int(x[3]) * int(x[4]) for x in w)
-            print(json.dumps({"tag": tag, "what": f"crops_{short}", "fmt": FMT, "ms": ms,
+            print(json.dumps({"tag": tag, "cfg": cfg.name, "rep": os.environ.get("REP"), "what": f"crops_{short}",
+                              "fmt": FMT, "ms": ms,
                               "GBps_sum": (out_b + rd) / ms / 1e6}), flush=True)
         del frames, p
         torch.cuda.empty_cache()
