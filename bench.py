@@ -346,6 +346,47 @@ def run_dry(args):
 
 
 # --------------------------------------------------------------------------- B200 leg
+def trace_summary(prof, args):
+    """Write the CUPTI trace of the timed loop (chrome JSON) and a summary:
+    every CUDA runtime/driver API call the host made inside it, the ones that
+    block the host (synchronize / blocking copies / event or stream queries),
+    and the device kernels by name.  Printed as one JSON line on stderr."""
+    import collections
+    os.makedirs(os.path.dirname(os.path.abspath(args.trace)), exist_ok=True)
+    prof.export_chrome_trace(args.trace)
+    ev = json.load(open(args.trace))
+    evs = ev.get("traceEvents", ev) if isinstance(ev, dict) else ev
+    api, kern, ranges = collections.Counter(), collections.Counter(), collections.Counter()
+    # the loop ends with t1.record (the last event-record call); the profiler's
+    # own flush (a device synchronize at stop) comes after it
+    rec_ts = [e.get("ts", 0) for e in evs if e.get("cat", "") in ("cuda_runtime", "cuda_driver")
+              and e.get("name", "").startswith(("cudaEventRecord", "cuEventRecord"))]
+    t_end = max(rec_ts) if rec_ts else float("inf")
+    in_loop_blocking = collections.Counter()
+    for e in evs:
+        cat, name = e.get("cat", ""), e.get("name", "")
+        if cat in ("cuda_runtime", "cuda_driver"):
+            api[name] += 1
+            if e.get("ts", 0) <= t_end and (any(t in name for t in ("Synchronize", "Query")) or
+                                            (name.startswith(("cudaMemcpy", "cuMemcpy")) and "Async" not in name)):
+                in_loop_blocking[name] += 1
+        elif cat == "kernel":
+            kern[name.split("(")[0]] += 1
+        elif cat in ("user_annotation", "gpu_user_annotation") or name.startswith("mp."):
+            ranges[name.split("[")[0]] += 1
+    blocking = {k: v for k, v in api.items()
+                if any(t in k for t in ("Synchronize", "Query")) or
+                (k.startswith(("cudaMemcpy", "cuMemcpy")) and "Async" not in k)}
+    out = {"trace": os.path.relpath(args.trace, ROOT), "steps": args.steps, "config": args.config,
+           "host_api_calls": dict(api), "host_blocking_calls": blocking,
+           "host_blocking_calls_before_loop_end": dict(in_loop_blocking),
+           "note": "blocking calls after the loop's last event record are the profiler's own flush at stop",
+           "kernels": dict(kern), "kernel_launches": int(sum(kern.values())), "nvtx_ranges": dict(ranges)}
+    with open(os.path.splitext(args.trace)[0] + "_summary.json", "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps(out), file=sys.stderr, flush=True)
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -404,21 +445,34 @@ def run_b200(args):
         p2.reserve(F, n_win, caps=counts, max_boxes=max(len(boxes), 1))
         pipes.append(p2)
     runner = mp.PipelinedRunner(pipes, device=dev, merge_on_gather_stream=bool(args.merge_on_gather),
-                                side_streams=args.side_streams)
+                                side_streams=args.side_streams, plan_priority=bool(args.plan_priority))
     stream = torch.cuda.current_stream(dev)
-    if args.graphs:
+    # whole-step graphs (auto: small batches, whose steps are otherwise bound
+    # by the host-side issue of ~20 launches and events per step): U
+    # consecutive steps are ONE graph launch; U divides --steps
+    step_graph = args.step_graph if args.step_graph >= 0 else int(F <= 64 and not nv12)
+    U = max(u for u in range(1, 17) if args.steps % u == 0) if step_graph else 0
+    if args.graphs and not step_graph:
         # the graphs read runner-owned static inputs (copies of these); the
         # steps below pass those tensors back, so no per-step input copy runs
         runner.capture_graphs(scores, boxes_t, wbo_t)
 
     def step_inputs():
-        return runner.inputs() if args.graphs else (scores, boxes_t, wbo_t)
+        return runner.inputs() if (args.graphs and not step_graph) else (scores, boxes_t, wbo_t)
 
     for _ in range(max(args.warmup, 0)):
         sc_k, bx_k, wb_k = step_inputs()
         runner.step(sc_k, frames, bx_k, wb_k)
     runner.wait_all()
     torch.cuda.synchronize()
+    if step_graph:
+        l2_note += f"; step graphs cycle through {min(U, n_copies)} of the copies"
+        gevs = [(torch.cuda.Event(enable_timing=True, external=True),
+                 torch.cuda.Event(enable_timing=True, external=True)) for _ in range(U)]
+        runner.capture_steps([(scores, frame_ring[u % n_copies], boxes_t, wbo_t) for u in range(U)], gevs)
+        for _ in range(max(1, -(-args.warmup // U))):
+            runner.replay_steps()
+        torch.cuda.synchronize()
     for p in pipes:
         p.check_status()
     n_kept = int(pipe.nms_frame_off[F].item())
@@ -433,20 +487,33 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    prof = None
+    if args.trace:   # evidence run (not a bench value): CUPTI trace of the timed loop
+        from torch.profiler import ProfilerActivity, profile
+        prof = profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA])
+        prof.__enter__()
     t0.record(stream)
     h0 = time.perf_counter()
-    for i in range(args.steps):   # (each step's side streams wait for `stream`: t0 precedes all work)
-        sc_k, bx_k, wb_k = step_inputs()
-        runner.step(sc_k, frame_ring[i % n_copies], bx_k, wb_k, gather_events=evs[i], proxy_events=pevs[i])
-    runner.wait_all(stream)
+    if step_graph:
+        for _ in range(args.steps // U):   # each replay: U steps, all streams joined at its end
+            runner.replay_steps()
+    else:
+        for i in range(args.steps):   # (each step's side streams wait for `stream`: t0 precedes all work)
+            sc_k, bx_k, wb_k = step_inputs()
+            runner.step(sc_k, frame_ring[i % n_copies], bx_k, wb_k, gather_events=evs[i], proxy_events=pevs[i])
+        runner.wait_all(stream)
     t1.record(stream)
     host_enqueue_ms = (time.perf_counter() - h0) * 1e3   # no host sync in the loop: << device time
+    if prof is not None:
+        prof.__exit__(None, None, None)   # stops before the synchronize below
+        trace_summary(prof, args)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
     elapsed_ms = t0.elapsed_time(t1)
-    gather_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    # (step graphs: the gather events of the last replay, recorded as graph nodes)
+    gather_ms = float(np.mean([a.elapsed_time(b) for a, b in (gevs if step_graph else evs)]))
     proxy_ms = float(np.mean([a.elapsed_time(b) for a, b in pevs])) if nv12 else None
     for p in pipes:
         p.check_status()
@@ -525,7 +592,8 @@ def run_b200(args):
                        "parallelism": f"clip-sharded x{world}", "host_numa": numa,
                        "pipeline": f"plan/gather/merge on {1 + 2 * len(runner.s_plans)} CUDA streams, "
                                    f"{args.depth} buffer sets, "
-                                   f"plan/merge as CUDA graphs: {bool(args.graphs)}"},
+                                   + (f"whole steps as CUDA graphs ({U} steps per graph launch)" if step_graph
+                                      else f"plan/merge as CUDA graphs: {bool(args.graphs)}")},
             "roofline": {"bound": "hbm", "kernel": "gather_resize (prep + gather_kernel)",
                          "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -539,8 +607,8 @@ def run_b200(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "host_enqueue_ms_per_step": host_enqueue_ms / args.steps,
-            "gpu_launches": args.steps * (mp.launches_per_call(0) + mp.launches_per_call(1) * (2 if nv12 else 1) +
-                                          mp.launches_per_call(2)),
+            "gpu_launches": args.steps * (mp.launches_per_call(0) + int(R * ((C + 1) // 2) > 1024) +
+                                          mp.launches_per_call(1) * (2 if nv12 else 1) + mp.launches_per_call(2)),
             "proxy_input": proxy,
             "counters": dataclasses.asdict(glob),
             "clocks": clocks,
@@ -1119,6 +1187,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=3, help="batches in flight (buffer sets) in the stream pipeline")
     ap.add_argument("--graphs", type=int, default=1, help="replay plan/merge as CUDA graphs")
+    ap.add_argument("--plan-priority", type=int, default=1, help="plan streams at the highest stream priority")
+    ap.add_argument("--trace", default="", help="evidence run: write a torch.profiler (CUPTI) trace of the timed "
+                                               "loop to this path plus a host-sync summary (not a bench value)")
+    ap.add_argument("--step-graph", type=int, default=-1,
+                    help="capture whole pipelined steps as one CUDA graph per up to 16 steps "
+                         "(-1 auto: batches of <= 64 frames)")
     ap.add_argument("--side-streams", type=int, default=1,
                     help="plan and remap/NMS streams (batches of different buffer sets overlap when > 1)")
     ap.add_argument("--merge-on-gather", type=int, default=0,

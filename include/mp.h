@@ -105,9 +105,14 @@ size_t mp_plan_workspace_size(const mp_plan_params* p, int32_t F);
  *                (the true total even on overflow).
  *  d_class_count device int32 [k]: number of windows of each size (true counts).
  *  d_status      device int32: set to MP_ERR_CAPACITY if total > max_windows.
- *  Limits: one CTA per frame holds the grid in shared memory (~32 bytes per
- *  possible run, R*ceil(C/2) runs): up to ~7000 runs (4K at 32 px = 4080)
- *  and R*C <= 16384 cells; larger grids return MP_ERR_UNSUPPORTED.
+ *  Execution: one CTA per frame; frames with <= 256 horizontal runs of
+ *  positive cells are planned in shared memory by a 128-thread tier, others by
+ *  a persistent 256-thread tier whose CTAs hold up to 1024 runs in shared
+ *  memory (~33 KB, so they fit beside a persistent gather CTA on the same SM)
+ *  and move the run/component arrays of larger frames (up to R*ceil(C/2)
+ *  runs) to a per-CTA global scratch slot in d_ws (same arithmetic).
+ *  Limits: R*C <= 16384 cells (4K at 32 px = 8160); larger grids return
+ *  MP_ERR_UNSUPPORTED.
  */
 mp_status mp_plan_windows(const mp_plan_params* p, const float* d_scores, int32_t F,
                           uint32_t* d_mask, mp_window* d_windows, int32_t max_windows,
@@ -240,10 +245,12 @@ size_t mp_remap_nms_workspace_size(int32_t F, int32_t max_boxes);
  *  d_out_frame_off device int32 [F+1]: CSR of kept boxes (true totals).
  *  max_boxes      capacity of d_boxes; frames whose boxes extend past it are
  *                 skipped with *d_status = MP_ERR_INVALID.
- *  No per-frame limit: frames with up to 2048 raw boxes are merged in shared
- *  memory; frames with more take a global-memory path inside the same
- *  launch (same arithmetic and results, O(n^2) IoUs over L2 — slow for very
- *  large n).  The workspace grows with max_boxes (~80 bytes per raw box).
+ *  No per-frame limit: frames with up to 1024 raw boxes are merged in shared
+ *  memory (tiers of <= 64 / <= 512 / <= 1024 raw boxes, each CTA small enough
+ *  to run beside a persistent gather on the same SM); frames with more take a
+ *  global-memory path inside the same launch (same arithmetic and results,
+ *  O(n^2) IoUs over L2 — slow for very large n).  The workspace grows with
+ *  max_boxes (~80 bytes per raw box).
  */
 mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_box_off,
                        const mp_window* d_windows, const int32_t* d_frame_off, int32_t max_windows, int32_t F,
@@ -261,8 +268,13 @@ mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_box_off,
  * rectangles in R_{i,j}."
  *
  * One call = one proxy resolution i (one score-grid geometry) and J thresholds.
- * For every threshold the frames are planned exactly as mp_plan_windows does
- * (a1-a4, same readings) and the per-threshold totals are accumulated:
+ * Single pass: one CTA per frame reads the frame's score grid once and ranks
+ * every cell against the thresholds sorted ascending (rank = number of
+ * thresholds the score exceeds; score > B_j <=> rank > position of B_j), so
+ * each threshold's mask comes from shared memory; a threshold whose mask
+ * equals the next-lower one's reuses that plan.  For every threshold the
+ * frames are planned exactly as mp_plan_windows does (a1-a4, same readings)
+ * and the per-threshold totals are accumulated:
  *   cost_sum      sum over frames and windows of T (the detector part of the
  *                 runtime estimate; the caller adds T_proxy,i)
  *   windows       number of windows
@@ -276,7 +288,8 @@ mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_box_off,
  *
  *  p             planner parameters; p->b_proxy is ignored.
  *  d_scores      device float [F][R][C].
- *  thresholds    host float [J], 1 <= J <= 64.
+ *  thresholds    host float [J], 1 <= J <= 64, any order, duplicates allowed, no NaN;
+ *                d_out row j belongs to thresholds[j].
  *  d_dets        device float [n_det][4] (x1, y1, x2, y2) frame px, the theta_best
  *                detections, frame-major; d_det_off device int32 [F+1] CSR.
  *  d_out         device mp_sweep_result [J] (overwritten).
@@ -439,7 +452,8 @@ const char* mp_status_string(mp_status st);
 /* Number of device kernels the library launches per call (diagnostic, used
  * by bench.py to count launches): which = 0 plan, 1 gather, 2 remap_nms,
  * 3 proxy_sweep, 4 window_set_cost, 5 hungarian, 6 track_resample,
- * 7 dbscan, 8 cluster_centers, 9 refine_tracks. */
+ * 7 dbscan, 8 cluster_centers, 9 refine_tracks.  The plan adds one launch
+ * (plan_huge_kernel) for grids with R*ceil(C/2) > 1024 possible runs. */
 int32_t mp_launches_per_call(int32_t which);
 
 #ifdef __cplusplus

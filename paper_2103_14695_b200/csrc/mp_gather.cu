@@ -24,6 +24,9 @@
 //                        separable lerps reusing staged rows, streaming stores.
 #include <cuda.h>
 #include <stdio.h>
+
+#include <atomic>
+#include <mutex>
 #include <stdlib.h>
 
 #include "mp_internal.cuh"
@@ -43,6 +46,9 @@ constexpr int kStages = 2;      // default ring depth (A.stages; MP_GATHER_STAGE
 constexpr int kStagesF32 = 3;   // f32 output: 3 x 40 KB (measured c2 1.424 -> 1.389 ms, c3 6.86 -> 6.35, c4 4.22 -> 4.27
                                 // against 2 x 44 KB; 2 x 40 KB is slower, 1.53)
 constexpr int kMaxStages = 8;
+// Shared memory per SM left free by the gather's ring for co-running side
+// CTAs: the largest plan / remap-NMS tier CTA is ~53 KB (+1 KB driver reserve).
+constexpr size_t kSideReserve = 56 * 1024;
 constexpr int kHdrBytes = 64;
 constexpr int kMaxTW = 256;
 constexpr int kMaxTR = 8 * kCW > 96 ? 8 * kCW : 96;   // Rw <= 8 rows per consumer warp
@@ -963,22 +969,59 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
   const char* stg = knob("MP_GATHER_STAGES");   // experiment knob
   A.stages = stg ? atoi(stg) : (fmt == MP_OUT_F32_NCHW && A.src == kSrcRGB24 ? kStagesF32 : kStages);
   if (A.stages < 2 || A.stages > kMaxStages) A.stages = kStages;
-  // fewer stages when the deepest ring does not fit (row-sparse classes stage 96 KB)
-  while (A.stages > 2 && (size_t)A.stages * A.stage_bytes + 2 * A.stages * sizeof(uint64_t) > 227 * 1024) A.stages--;
+  // fewer stages when the ring would not leave kSideReserve of the SM's shared
+  // memory to the latency-bound plan / remap-NMS CTAs of neighbouring batches
+  // (they must co-run beside this persistent kernel, or they queue behind it
+  // and serialise the pipeline), or when it does not fit at all (row-sparse
+  // classes stage 96 KB: the proxy-input downscale keeps its 2 x 96 KB ring)
+  const size_t ring_cap = (2 * (size_t)A.stage_bytes + 4 * sizeof(uint64_t) <= 227 * 1024 - kSideReserve)
+                              ? 227 * 1024 - kSideReserve : 227 * 1024;
+  while (A.stages > 2 && (size_t)A.stages * A.stage_bytes + 2 * A.stages * sizeof(uint64_t) > ring_cap) A.stages--;
   const size_t smem = (size_t)A.stages * A.stage_bytes + 2 * A.stages * sizeof(uint64_t);
   if (smem > 227 * 1024) return MP_ERR_UNSUPPORTED;
   int dev = 0, sms = 0, per_sm = 0;
   MP_CUDA_TRY(cudaGetDevice(&dev));
-  MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // per-device SM count and per-(kernel, device) attribute/occupancy results
+  // are cached: a steady-state call issues only the memset and two launches
+  static std::atomic<int> sm_cache[64];
+  if (dev >= 0 && dev < 64 && sm_cache[dev].load() > 0) {
+    sms = sm_cache[dev].load();
+  } else {
+    MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (dev >= 0 && dev < 64) sm_cache[dev].store(sms);
+  }
   // Diagnostic only (profiling the two halves of the pipeline): MP_GATHER_DEBUG=1
   // skips the consumer math, =2 skips the pixel copies.  Unset in production.
   const char* dbg = knob("MP_GATHER_DEBUG");
   A.debug = dbg ? atoi(dbg) : 0;
   const int threads = (kCW + kProducerWarps) * 32;
   auto launch = [&](auto kern) -> mp_status {
-    MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
-    if (per_sm < 1) per_sm = 1;
+    // cache key: kernel instance x device x dynamic shared memory
+    struct Occ {
+      const void* fn;
+      int dev;
+      size_t smem;
+      int per_sm;
+    };
+    static Occ occ_cache[32];
+    static int occ_n = 0;
+    static size_t attr_max[64][4];   // largest MaxDynamicSharedMemorySize set per (device, instance)
+    static std::mutex mu;            // callers may enqueue from several host threads
+    std::lock_guard<std::mutex> lock(mu);
+    const int inst = (A.src == kSrcNV12 ? 2 : 0) + (fmt == MP_OUT_F32_NCHW ? 0 : 1);
+    per_sm = 0;
+    for (int i = 0; i < occ_n; i++)
+      if (occ_cache[i].fn == (const void*)kern && occ_cache[i].dev == dev && occ_cache[i].smem == smem)
+        per_sm = occ_cache[i].per_sm;
+    if (dev < 0 || dev >= 64 || attr_max[dev][inst] < smem) {
+      MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if (dev >= 0 && dev < 64) attr_max[dev][inst] = smem;
+    }
+    if (per_sm == 0) {
+      MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+      if (per_sm < 1) per_sm = 1;
+      if (occ_n < 32) occ_cache[occ_n++] = Occ{(const void*)kern, dev, smem, per_sm};
+    }
     kern<<<sms * per_sm, threads, smem, s>>>(A, tm, d_frame_ptrs, ws_cnt, ws_list, d_windows, d_frame_off, ws_tap,
                                              d_status);
     MP_CUDA_TRY(cudaGetLastError());
@@ -1011,6 +1054,8 @@ extern "C" mp_status mp_gather_resize(const uint8_t* const* d_frame_ptrs, int32_
 }
 
 static EncodeTiledFn get_encode() {
+  static std::atomic<EncodeTiledFn> cached{nullptr};   // the driver entry point does not change
+  if (EncodeTiledFn c = cached.load()) return c;
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult qr;
   if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
@@ -1018,6 +1063,7 @@ static EncodeTiledFn get_encode() {
     (void)cudaGetLastError();
     return nullptr;
   }
+  cached.store((EncodeTiledFn)fn);
   return (EncodeTiledFn)fn;
 }
 

@@ -12,8 +12,8 @@
 //   nms_small_kernel   4/SM     queued frames with <= 512 raw boxes, one CTA each:
 //                               block compaction, bitonic sort, n x ceil(n/64)
 //                               IoU bitmask, warp-0 greedy scan
-//   nms_large_kernel   1/SM     queued frames (<= 2048 raw boxes in shared memory:
-//                               bitmask up to 1024 candidates, tiled 64-candidate
+//   nms_large_kernel   1/SM     queued frames (<= 1024 raw boxes in shared memory:
+//                               bitmask up to 256 candidates, tiled 64-candidate
 //                               blocks beyond; frames with more raw boxes run the
 //                               same tiled greedy over global-memory scratch, with
 //                               a merge sort of the keys — no per-frame limit)
@@ -31,7 +31,12 @@ struct NmsArgs {
 };
 
 constexpr int kSmallCap = 512, kSmallThreads = 256;
-constexpr int kLargeCap = 2048, kLargeMaskCap = 1024, kLargeThreads = 1024;
+// Every tier's CTA fits in what the persistent gather CTA leaves of an SM
+// (<= 54 KB of shared memory = kSideReserve in mp_gather.cu, <= 16K registers), so the
+// remap/NMS of batch i-1 runs beside gather(i) instead of queueing behind it
+// (the former 1024-thread, 207-KB large tier could not start on any SM until
+// the gather ended: c4 step = gather + NMS/plan tail).
+constexpr int kLargeCap = 1024, kLargeMaskCap = 256, kLargeThreads = 256;
 
 struct NmsSmem {
   float4* bx;
@@ -74,7 +79,7 @@ __host__ __device__ inline size_t nms_smem_bytes(int cap, int mask_cap, NmsSmem*
   const size_t maskb = sizeof(unsigned long long) * (size_t)mask_cap * ((mask_cap + 63) / 64);
   size_t u = keyb > maskb ? keyb : maskb;
   if ((size_t)cap > u) u = cap;
-  const size_t permb = (size_t)cap * (sizeof(float4) + 3 * sizeof(int));   // sorted-order permutation scratch
+  const size_t permb = (size_t)cap * sizeof(float4);   // sorted-order permutation scratch (one array at a time)
   if (permb > u) u = permb;
   s.key = (unsigned long long*)take(u);
   s.supp = (unsigned char*)s.key;
@@ -192,29 +197,27 @@ __device__ void nms_frame(const NmsArgs& A, int f, int b_lo, int b_hi, int w_lo,
   }
   for (int p = tid; p < n; p += blockDim.x) S.order[p] = (int)(S.key[p] & 0xffffffffu);
   __syncthreads();
-  // physically permute the candidates into the sorted order (through the now
-  // free key region) so the O(n^2) IoU loops read consecutive entries instead
-  // of order[]-scattered ones; order[] becomes the identity
+  // physically permute the candidates into the sorted order (one array at a
+  // time through the now free key region, 16 B per candidate) so the O(n^2)
+  // IoU loops read consecutive entries instead of order[]-scattered ones;
+  // order[] becomes the identity
   {
     float4* tb = reinterpret_cast<float4*>(S.key);
-    int* tc = reinterpret_cast<int*>(tb + n);
-    float* ts = reinterpret_cast<float*>(tc + n);
-    int* tr = reinterpret_cast<int*>(ts + n);
-    for (int p = tid; p < n; p += blockDim.x) {
-      const int q = S.order[p];
-      tb[p] = S.bx[q];
-      tc[p] = S.cls[q];
-      ts[p] = S.score[q];
-      tr[p] = S.src[q];
-    }
+    for (int p = tid; p < n; p += blockDim.x) tb[p] = S.bx[S.order[p]];
     __syncthreads();
-    for (int p = tid; p < n; p += blockDim.x) {
-      S.bx[p] = tb[p];
-      S.cls[p] = tc[p];
-      S.score[p] = ts[p];
-      S.src[p] = tr[p];
-      S.order[p] = p;
+    for (int p = tid; p < n; p += blockDim.x) S.bx[p] = tb[p];
+    __syncthreads();
+    int* ti = reinterpret_cast<int*>(S.key);
+    int* arrs[3] = {S.cls, reinterpret_cast<int*>(S.score), S.src};
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      int* v = arrs[a];
+      for (int p = tid; p < n; p += blockDim.x) ti[p] = v[S.order[p]];
+      __syncthreads();
+      for (int p = tid; p < n; p += blockDim.x) v[p] = ti[p];
+      __syncthreads();
     }
+    for (int p = tid; p < n; p += blockDim.x) S.order[p] = p;
     __syncthreads();
   }
 

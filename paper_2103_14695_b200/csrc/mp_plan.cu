@@ -98,24 +98,32 @@ __host__ __device__ inline size_t plan_smem_bytes(int R, int words, int maxc, Pl
   s.row_off = (int*)take(sizeof(int) * (R + 1));
   s.tmp = (int*)take(sizeof(int) * 40);
   s.run = (int*)take(sizeof(int) * kMaxClasses);
-  s.parent = (int*)take(sizeof(int) * maxc);
-  s.cid = (int*)take(sizeof(int) * maxc);
-  s.bc0 = (int*)take(sizeof(int) * maxc);
-  s.br0 = (int*)take(sizeof(int) * maxc);
-  s.bc1 = (int*)take(sizeof(int) * maxc);
-  s.br1 = (int*)take(sizeof(int) * maxc);
+  // per-component arrays hold one spare entry: the CTA-cooperative merge
+  // appends a merged cluster before it compacts (coop_merge, cap = maxc + 1)
+  s.parent = (int*)take(sizeof(int) * (maxc + 1));
+  s.cid = (int*)take(sizeof(int) * (maxc + 1));
+  s.bc0 = (int*)take(sizeof(int) * (maxc + 1));
+  s.br0 = (int*)take(sizeof(int) * (maxc + 1));
+  s.bc1 = (int*)take(sizeof(int) * (maxc + 1));
+  s.br1 = (int*)take(sizeof(int) * (maxc + 1));
   s.rrow = (short*)take(sizeof(short) * maxc);
   s.rcs = (short*)take(sizeof(short) * maxc);
   s.rce = (short*)take(sizeof(short) * maxc);
-  s.csz = (unsigned char*)take(maxc);
-  s.memb = (unsigned char*)take(maxc);
+  s.csz = (unsigned char*)take(maxc + 1);
+  s.memb = (unsigned char*)take(maxc + 1);
   if (out) *out = s;
   return off;
 }
 
-constexpr int kPlanThreads = 256;      // full-capacity tier
+constexpr int kPlanThreads = 128;      // full-capacity tier (128 threads: two CTAs fit beside a gather CTA)
 constexpr int kFastThreads = 128;      // fast tier: frames with <= kFastCap runs
 constexpr int kFastCap = 256;
+// full tier: runs held in shared memory (~33 KB at 1024 runs, so a CTA fits
+// in what the gather's ring leaves of an SM); beyond -> global scratch.
+// c4 (4K, 68 x 120 cells) frames have 756-888 runs.
+constexpr int kMidCap = 1024;
+constexpr int kFullGrid = 4;        // plan_full CTAs per SM (one frame each at c4: 300 frames)
+constexpr int kHugeGrid = 1;        // plan_huge CTAs per SM (each owns a global scratch slot)
 
 constexpr int kCoopMergeMin = 96;   // components above which the whole CTA runs the merge
 
@@ -139,29 +147,86 @@ extern __shared__ __align__(16) unsigned char smem_raw[];
 // a3 with the whole CTA (exactly the P:184 greedy of the warp-0 path below:
 // same nearest-neighbour metric and ties, same ascending absorption, strict
 // acceptance, remove + append); used when a frame has many components.
-// Per step: block arg-min for the nearest neighbour; every warp tests its
-// 32-cluster chunks against the initial merged box (a cluster that does not
-// fit it can never fit the grown box, R7), warp 0 then walks only those
-// candidates in ascending order; an accepted merge is compacted by the whole
-// CTA (block scan of the keep flags, chunked read-then-write moves).
-__device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n) {
+//
+// The cluster list is kept as an append-only array with dead flags instead
+// of being compacted after every accepted merge: members are flagged dead
+// and the merged cluster is appended at the end.  The alive entries keep
+// exactly the order of the compacted list (compaction is stable and appends
+// at the end), so positions compare the same way for the R5 tie rule and the
+// R7 ascending absorption, and "i -= before_i" becomes "the next alive entry
+// after i".  The array is compacted only at the start of a pass and when it
+// is full (capacity `cap`).  Dense frames accept most proposals (c4 4K
+// drone frames: ~175 steps, ~90 % accepted), so this removes the per-merge
+// block scan and chunked moves (~10 of the ~14 barriers of an accepted step).
+//
+// Per step (3 barriers): block arg-min for the nearest alive neighbour; every
+// warp ballots its 32-entry chunks against the initial merged box (a cluster
+// that does not fit it can never fit the grown box, R7); warp 0 walks only
+// those candidates in ascending order, decides, flags the members dead,
+// appends the merged cluster and finds the next i, then publishes.
+constexpr int kAbsList = 64;   // absorbed members recorded by warp 0 (beyond: block-wide mark)
+
+__device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n, int cap) {
   __shared__ unsigned long long red[64];
-  __shared__ int pub[6];
-  __shared__ long long pub_sum;
-  __shared__ uint32_t fitm[256];   // initial-fit ballots, one word per 32 clusters (n <= 8192)
+  __shared__ int pub[8];
+  __shared__ uint32_t fitm[256];   // initial-fit ballots, one word per 32 entries (len <= 8192)
+  __shared__ int absl[kAbsList];
   int par = 0;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, BS = blockDim.x, NW = BS >> 5;
   const long long* T = P.cost;
+  unsigned char* dead = S.memb;   // dead flag per entry
+  int* gen_of = S.cid;            // entry absorbed in proposal number gen_of[q] (overflow path)
+  int* scan = S.parent;           // compaction scratch (free once components are labelled)
+  int len = n, alive = n, gen = 0;
+  for (int q = tid; q < len; q += BS) {
+    dead[q] = 0;
+    gen_of[q] = -1;
+  }
+  __syncthreads();
+  // stable removal of the dead entries; returns the new position of entry
+  // `keep_pos` (alive, or == len -> the new len)
+  auto compact = [&](int keep_pos) -> int {
+    for (int q = tid; q < len; q += BS) scan[q] = dead[q] ? 0 : 1;
+    __syncthreads();
+    const int kept = block_excl_scan_smem(scan, len, S.tmp);
+    const int np = keep_pos < len ? scan[keep_pos] : kept;
+    for (int base = 0; base < len; base += BS) {
+      const int q = base + tid;
+      bool keep = false;
+      int v0 = 0, v1 = 0, v2 = 0, v3 = 0, d = 0;
+      unsigned char vs = 0;
+      if (q < len) {
+        keep = !dead[q];
+        d = scan[q];
+        v0 = S.bc0[q]; v1 = S.br0[q]; v2 = S.bc1[q]; v3 = S.br1[q]; vs = S.csz[q];
+      }
+      __syncthreads();   // elements only move to lower indices: read the chunk before writing it
+      if (keep) {
+        S.bc0[d] = v0; S.br0[d] = v1; S.bc1[d] = v2; S.br1[d] = v3; S.csz[d] = vs;
+      }
+      __syncthreads();
+    }
+    for (int q = tid; q < kept; q += BS) {
+      dead[q] = 0;
+      gen_of[q] = -1;
+    }
+    __syncthreads();
+    len = kept;
+    return np;
+  };
   bool again = true;
   while (again) {
     again = false;
+    if (len != alive) compact(len);   // each pass starts on the compacted list
     int i = 0;
-    while (i < n && n >= 2) {
+    while (i < len && alive >= 2) {
+      if (len >= cap) i = compact(i);   // full: no room to append a merged cluster
+      gen++;
       const int ic0 = S.bc0[i], ir0 = S.br0[i], ic1 = S.bc1[i], ir1 = S.br1[i];
       const int sx = ic0 + ic1, sy = ir0 + ir1;
       unsigned long long best = ~0ull;
-      for (int j = tid; j < n; j += BS) {
-        if (j == i) continue;
+      for (int j = tid; j < len; j += BS) {
+        if (j == i || dead[j]) continue;
         const int dx = sx - (S.bc0[j] + S.bc1[j]);
         const int dy = sy - (S.br0[j] + S.br1[j]);
         const unsigned long long key = ((unsigned long long)(unsigned)(dx * dx + dy * dy) << 32) | (unsigned)j;
@@ -175,14 +240,12 @@ __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n) {
       extent(P, m0, n0, m1, n1, px0, py0, bw, bh);
       const int s = smallest_size(P, bw, bh);
       const int ws = P.sw[s], hs = P.sh[s];
-      long long sum = T[S.csz[i]] + T[S.csz[j]];
-      int before_i = (j < i) ? 1 : 0, n_abs = 0;
       // initial-fit ballots (all warps)
-      const int nch = (n + 31) >> 5;
+      const int nch = (len + 31) >> 5;
       for (int c = wid; c < nch; c += NW) {
         const int q = (c << 5) + lane;
         bool fit = false;
-        if (q < n && q != i && q != j) {
+        if (q < len && q != i && q != j && !dead[q]) {
           int qx, qy, qw, qh;
           extent(P, min(m0, S.bc0[q]), min(n0, S.br0[q]), max(m1, S.bc1[q]), max(n1, S.br1[q]), qx, qy, qw, qh);
           fit = (qw <= ws) && (qh <= hs);
@@ -191,9 +254,11 @@ __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n) {
         if (lane == 0) fitm[c] = msk;
       }
       __syncthreads();
-      // absorption (k ascending, each fitting cluster at once, R7) by warp 0
-      // over the initial candidates only; the grown box is then published
       if (wid == 0) {
+        // absorption (k ascending, each fitting cluster at once, R7) over the
+        // initial candidates only
+        long long sum = T[S.csz[i]] + T[S.csz[j]];
+        int n_abs = 0;
         for (int c0 = 0; c0 < nch; c0 += 32) {
           const uint32_t word = (c0 + lane < nch) ? fitm[c0 + lane] : 0u;
           uint32_t nz = __ballot_sync(0xffffffffu, word != 0u);
@@ -222,85 +287,98 @@ __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n) {
               m1 = max(m1, S.bc1[qq]);
               n1 = max(n1, S.br1[qq]);
               sum += T[S.csz[qq]];
-              before_i += (qq < i) ? 1 : 0;
+              if (lane == 0) {
+                if (n_abs < kAbsList) absl[n_abs] = qq;
+                else gen_of[qq] = gen;
+              }
               n_abs++;
-              if (lane == 0) S.memb[qq] = 1;
               rem &= (bq == 31) ? 0u : ~((2u << bq) - 1u);
             }
           }
         }
+        // (d) accept iff strictly faster (R8): members dead, merged appended
+        const bool acc = T[s] < sum;
+        int ni = i + 1;
+        if (acc) {
+          __syncwarp();   // absl / gen_of writes of lane 0
+          if (lane == 0) {
+            dead[i] = 1;
+            dead[j] = 1;
+            S.bc0[len] = m0; S.br0[len] = n0; S.bc1[len] = m1; S.br1[len] = n1;
+            S.csz[len] = (unsigned char)s;
+            dead[len] = 0;
+            gen_of[len] = -1;
+          }
+          for (int a = lane; a < min(n_abs, kAbsList); a += 32) dead[absl[a]] = 1;
+          if (n_abs > kAbsList)
+            for (int q = lane; q < len; q += 32)
+              if (gen_of[q] == gen) dead[q] = 1;
+          __syncwarp();
+          // next alive entry after i (the appended cluster at len is alive)
+          ni = len + 1;
+          for (int base = i + 1; base <= len; base += 32) {
+            const int q = base + lane;
+            const uint32_t al = __ballot_sync(0xffffffffu, q <= len && !dead[q]);
+            if (al) {
+              ni = base + __ffs(al) - 1;
+              break;
+            }
+          }
+        } else {
+          for (int base = i + 1; base < len + 32; base += 32) {
+            const int q = base + lane;
+            const uint32_t al = __ballot_sync(0xffffffffu, q < len && !dead[q]);
+            if (al || base >= len) {
+              ni = al ? base + __ffs(al) - 1 : len;
+              break;
+            }
+          }
+        }
         if (lane == 0) {
-          S.memb[i] = 1;
-          S.memb[j] = 1;
-          pub[0] = m0;
-          pub[1] = n0;
-          pub[2] = m1;
-          pub[3] = n1;
-          pub[4] = before_i;
-          pub[5] = n_abs;
-          pub_sum = sum;
+          pub[0] = acc ? 1 : 0;
+          pub[1] = ni;
+          pub[2] = n_abs;
         }
       }
       __syncthreads();
-      m0 = pub[0];
-      n0 = pub[1];
-      m1 = pub[2];
-      n1 = pub[3];
-      before_i = pub[4];
-      n_abs = pub[5];
-      sum = pub_sum;
-      if (T[s] < sum) {
-        // stable compaction by the CTA: destinations from a block scan of the
-        // keep flags (in S.cid, free during the merge); elements only move to
-        // lower indices, so reading a chunk before writing it is safe
-        for (int q = tid; q < n; q += BS) S.cid[q] = S.memb[q] ? 0 : 1;
-        __syncthreads();
-        const int kept = block_excl_scan_smem(S.cid, n, S.tmp);
-        for (int base = 0; base < n; base += BS) {
-          const int q = base + tid;
-          bool keep = false;
-          int v0 = 0, v1 = 0, v2 = 0, v3 = 0, d = 0;
-          unsigned char vs = 0;
-          if (q < n) {
-            keep = !S.memb[q];
-            d = S.cid[q];
-            v0 = S.bc0[q]; v1 = S.br0[q]; v2 = S.bc1[q]; v3 = S.br1[q]; vs = S.csz[q];
-          }
-          __syncthreads();
-          if (keep) {
-            S.bc0[d] = v0; S.br0[d] = v1; S.bc1[d] = v2; S.br1[d] = v3; S.csz[d] = vs;
-          }
-          if (q < n) S.memb[q] = 0;
-          __syncthreads();
-        }
-        if (tid == 0) {
-          S.bc0[kept] = m0; S.br0[kept] = n0; S.bc1[kept] = m1; S.br1[kept] = n1;
-          S.csz[kept] = (unsigned char)s;
-        }
-        __syncthreads();
-        n = kept + 1;   // members removed, merged cluster appended
+      const int acc = pub[0];
+      i = pub[1];
+      if (acc) {
+        alive -= pub[2] + 1;   // members (2 + n_abs) removed, merged added
+        len++;
         again = true;
-        i -= before_i;
-      } else {
-        for (int q = tid; q < n; q += BS) S.memb[q] = 0;
-        __syncthreads();
-        i++;
       }
     }
   }
-  return n;
+  if (len != alive) compact(len);
+  return len;
 }
 
 // The whole per-frame plan (a1-a4) with the CTA; `cap` = run/component
 // capacity of the shared-memory layout.  Returns false (having queued the
-// frame) if the frame has more runs than `cap`.
+// frame) if the frame has more runs than `cap`.  GB (the huge tier): the
+// per-run and per-component arrays live in the CTA's global scratch slot
+// `gbig` (capacity maxc, L2-resident) and only the bit rows and scan scratch
+// in shared memory; a separate instantiation, so the shared-memory tiers keep
+// plain LDS/STS accesses.
+template <bool GB = false>
 __device__ __forceinline__ bool plan_frame(const PlanArgs& P, int f, int cap, const float* __restrict__ scores,
                                            uint32_t* __restrict__ mask_out, int4* __restrict__ ws_win,
                                            int* __restrict__ ws_count, int* __restrict__ ws_cls,
                                            int* __restrict__ q_cnt, int* __restrict__ q_list,
-                                           long long* est_out = nullptr) {
+                                           long long* est_out = nullptr, unsigned char* gbig = nullptr,
+                                           const unsigned char* rk = nullptr, int jpos = 0) {
   PlanSmem S;
-  plan_smem_bytes(P.R, P.words, cap, &S, smem_raw);
+  plan_smem_bytes(P.R, P.words, GB ? 0 : cap, &S, smem_raw);
+  if (GB) {
+    PlanSmem G;
+    plan_smem_bytes(P.R, P.words, P.maxc, &G, gbig);
+    S.parent = G.parent; S.cid = G.cid;
+    S.bc0 = G.bc0; S.br0 = G.br0; S.bc1 = G.bc1; S.br1 = G.br1;
+    S.rrow = G.rrow; S.rcs = G.rcs; S.rce = G.rce;
+    S.csz = G.csz; S.memb = G.memb;
+    cap = P.maxc;
+  }
   const int R = P.R, C = P.C, words = P.words;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
   const float* sc = scores + (size_t)f * R * C;
@@ -308,6 +386,16 @@ __device__ __forceinline__ bool plan_frame(const PlanArgs& P, int f, int cap, co
   // ---- a1: threshold, one warp-ballot per 32 cells of a row (R2);
   // four (row, word) loads per warp in flight before the ballots.
   const int RW = R * words;
+  if (rk) {
+    // NEXT-1 single pass: the frame's cells were ranked once against the
+    // ascending thresholds (rk[c] = #{j : score_c > B_j}), so score_c > B_jpos
+    // <=> rk[c] > jpos; the score grid is not re-read per threshold
+    for (int rw = wid; rw < RW; rw += nwarps) {
+      const int r = rw / words, c = (rw - r * words) * 32 + lane;
+      const uint32_t m = __ballot_sync(0xffffffffu, c < C && (int)rk[r * C + c] > jpos);
+      if (lane == 0) S.bits[rw] = m;
+    }
+  } else
   for (int base = wid; base < RW; base += 4 * nwarps) {
     float v[4];
 #pragma unroll
@@ -346,7 +434,8 @@ __device__ __forceinline__ bool plan_frame(const PlanArgs& P, int f, int cap, co
   }
   __syncthreads();
   const int nruns = block_excl_scan_smem(S.row_off, R, S.tmp);
-  if (nruns > cap) {   // too many runs for this tier's shared memory: queue for the full tier
+  const int ext_cap = cap + 1;   // entries of the per-component arrays
+  if (nruns > cap) {   // too many runs for this tier's shared memory: queue for the next tier
     if (tid == 0) q_list[atomicAdd(q_cnt, 1)] = f;
     return false;
   }
@@ -428,7 +517,7 @@ __device__ __forceinline__ bool plan_frame(const PlanArgs& P, int f, int cap, co
   if (ncomp > kCoopMergeMin) {
     // many components: the CTA runs the greedy (same order rules) with block-wide
     // arg-mins; warp 0 then only places the final clusters
-    n = coop_merge(P, S, ncomp);
+    n = coop_merge(P, S, ncomp, ext_cap);
     again = false;
   }
   if (wid != 0) return true;
@@ -586,14 +675,37 @@ __global__ void __launch_bounds__(kFastThreads) plan_fast_kernel(PlanArgs P, con
 }
 
 // Persistent over the frames the fast tier queued (dense / checkerboard grids).
+// Shared memory holds min(maxc, kMidCap) runs, so a CTA fits beside the
+// persistent gather CTA of the previous batch on the same SM (the pipelined
+// step runs plan(i+1) while gather(i) streams); frames with more runs are
+// queued for plan_huge_kernel.
 __global__ void __launch_bounds__(kPlanThreads) plan_full_kernel(PlanArgs P, const float* __restrict__ scores,
                                                                  uint32_t* __restrict__ mask_out,
                                                                  int4* __restrict__ ws_win, int* __restrict__ ws_count,
                                                                  int* __restrict__ ws_cls, const int* __restrict__ q_cnt,
-                                                                 const int* __restrict__ q_list) {
+                                                                 const int* __restrict__ q_list, int cap,
+                                                                 int* __restrict__ q2_cnt, int* __restrict__ q2_list) {
   const int nq = *q_cnt;
   for (int qi = blockIdx.x; qi < nq; qi += gridDim.x) {
-    plan_frame(P, q_list[qi], P.maxc, scores, mask_out, ws_win, ws_count, ws_cls, nullptr, nullptr);
+    plan_frame(P, q_list[qi], cap, scores, mask_out, ws_win, ws_count, ws_cls, q2_cnt, q2_list);
+    __syncthreads();
+  }
+}
+
+// Persistent over the frames with more than kMidCap runs (up to R*ceil(C/2)):
+// the same plan with the run/component arrays in the CTA's global scratch
+// slot (gbig + blockIdx.x * slot_bytes).
+__global__ void __launch_bounds__(kPlanThreads) plan_huge_kernel(PlanArgs P, const float* __restrict__ scores,
+                                                                 uint32_t* __restrict__ mask_out,
+                                                                 int4* __restrict__ ws_win, int* __restrict__ ws_count,
+                                                                 int* __restrict__ ws_cls, const int* __restrict__ q_cnt,
+                                                                 const int* __restrict__ q_list,
+                                                                 unsigned char* __restrict__ gbig, size_t slot_bytes) {
+  const int nq = *q_cnt;
+  unsigned char* slot = gbig + (size_t)blockIdx.x * slot_bytes;
+  for (int qi = blockIdx.x; qi < nq; qi += gridDim.x) {
+    plan_frame<true>(P, q_list[qi], P.maxc, scores, mask_out, ws_win, ws_count, ws_cls, nullptr, nullptr, nullptr,
+                     slot);
     __syncthreads();
   }
 }
@@ -647,13 +759,20 @@ __global__ void __launch_bounds__(256) plan_scatter_kernel(PlanArgs P, int F, co
 constexpr int kSweepMaxJ = 64;
 constexpr int kSweepThreads = 256;
 struct SweepThr {
-  float v[kSweepMaxJ];
+  float v[kSweepMaxJ];   // thresholds in ascending order
+  int idx[kSweepMaxJ];   // their positions in the caller's list (output rows)
 };
 
-// One CTA per frame; for each threshold the frame is planned exactly as in
-// mp_plan_windows (plan_frame, full capacity), then the frame's detections are
-// tested against its windows; per-threshold totals are reduced in shared
-// memory and added to the output with one int64 atomic per field per CTA.
+// One CTA per frame, single pass over the score grid: the
+// frame's cells are read ONCE and ranked against the J ascending thresholds
+// (rank = number of thresholds the score exceeds; NaN -> 0) into shared
+// memory; the mask of threshold j is then {rank > j}.  For each threshold the
+// frame is planned exactly as in mp_plan_windows (plan_frame, full capacity,
+// a1 from the ranks), then the frame's detections are tested against its
+// windows.  A threshold whose mask equals the previous one's (no cell has
+// rank == j) has the same plan, so its totals are the previous ones (no
+// re-plan).  Per-threshold totals are reduced in shared memory and added to
+// the output with one int64 atomic per field per CTA.
 __global__ void __launch_bounds__(kSweepThreads) proxy_sweep_kernel(PlanArgs P, const float* __restrict__ scores,
                                                                     SweepThr thr, int J,
                                                                     const float4* __restrict__ dets,
@@ -663,15 +782,42 @@ __global__ void __launch_bounds__(kSweepThreads) proxy_sweep_kernel(PlanArgs P, 
                                                                     unsigned long long* __restrict__ out) {
   __shared__ unsigned long long acc[5];
   __shared__ float s_thr[kSweepMaxJ];
+  __shared__ int s_hist[kSweepMaxJ + 1];
   const int f = blockIdx.x, tid = threadIdx.x;
   if (tid < J) s_thr[tid] = thr.v[tid];
+  if (tid <= J) s_hist[tid] = 0;
+  if (tid < 5) acc[tid] = 0;
+  __syncthreads();
+  // the one pass over the frame's scores: per-cell threshold rank (binary
+  // search over the ascending thresholds) + a histogram of the ranks
+  const size_t plan_bytes = plan_smem_bytes(P.R, P.words, P.maxc, nullptr, nullptr);
+  unsigned char* rk = smem_raw + plan_bytes;
+  const int RC = P.R * P.C;
+  const float* sc = scores + (size_t)f * RC;
+  for (int c = tid; c < RC; c += blockDim.x) {
+    const float v = __ldg(sc + c);
+    int lo = 0, hi = J;   // number of thresholds t with v > t (NaN: none)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (v > s_thr[mid]) lo = mid + 1;
+      else hi = mid;
+    }
+    rk[c] = (unsigned char)lo;
+    atomicAdd(&s_hist[lo], 1);
+  }
+  __syncthreads();
   const int d_lo = det_off[f], d_hi = det_off[f + 1];
   for (int j = 0; j < J; j++) {
+    // mask(j) = {rank > j}; it differs from mask(j-1) iff some cell has rank j
+    const bool same = j > 0 && s_hist[j] == 0;
+    if (same) {   // identical plan: the previous threshold's totals (still in acc)
+      if (tid < 5 && acc[tid]) atomicAdd(&out[5 * thr.idx[j] + tid], acc[tid]);
+      continue;
+    }
+    __syncthreads();   // (acc read by the previous threshold's atomics above)
     if (tid < 5) acc[tid] = 0;
     __syncthreads();
-    PlanArgs Pj = P;
-    Pj.b = s_thr[j];
-    plan_frame(Pj, f, P.maxc, scores, nullptr, ws_win, ws_count, ws_cls, nullptr, nullptr);
+    plan_frame(P, f, P.maxc, scores, nullptr, ws_win, ws_count, ws_cls, nullptr, nullptr, nullptr, nullptr, rk, j);
     __syncthreads();   // warp 0's scratch writes are visible to the CTA
     const int n = ws_count[f];
     const int4* wl = ws_win + (size_t)f * P.maxc;
@@ -698,8 +844,8 @@ __global__ void __launch_bounds__(kSweepThreads) proxy_sweep_kernel(PlanArgs P, 
       acc[2] = (n == 1 && wl[0].z == P.full) ? 1 : 0;
     }
     __syncthreads();
-    if (tid < 5 && acc[tid]) atomicAdd(&out[5 * j + tid], acc[tid]);
-    __syncthreads();   // scratch and acc are reused by the next threshold
+    if (tid < 5 && acc[tid]) atomicAdd(&out[5 * thr.idx[j] + tid], acc[tid]);
+    __syncthreads();   // scratch is reused by the next threshold (acc is kept for an identical next mask)
   }
 }
 
@@ -836,17 +982,34 @@ static bool build_plan_args(const mp_plan_params* p, PlanArgs* A, mp_status* err
 }
 
 struct PlanWs {
-  size_t win_off, count_off, cls_off, q_off, total;
+  size_t win_off, count_off, cls_off, q_off, big_off, slot_bytes, total;
 };
 
+static int plan_sms() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                 cudaSuccess || sms < 1) {
+    (void)cudaGetLastError();
+    return 148;
+  }
+  return sms;
+}
+
+// Global scratch slots of the full tier (one per plan_full CTA) exist only
+// when the grid's worst case (maxc runs) exceeds the shared-memory capacity.
 static PlanWs plan_ws_layout(const PlanArgs& A, int F) {
   PlanWs L;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   L.win_off = 0;
   L.count_off = al(L.win_off + sizeof(int4) * (size_t)F * A.maxc);
   L.cls_off = al(L.count_off + sizeof(int) * (size_t)F);
-  L.q_off = al(L.cls_off + sizeof(int) * (size_t)F * A.k);   // [0] queue count, [1..F] queued frames
-  L.total = al(L.q_off + sizeof(int) * (size_t)(F + 1)) + 256;
+  // [0] full-tier queue count, [1] huge-tier queue count, [2..F+1] full-tier
+  // frames, [F+2..2F+1] huge-tier frames
+  L.q_off = al(L.cls_off + sizeof(int) * (size_t)F * A.k);
+  L.big_off = al(L.q_off + sizeof(int) * (size_t)(2 * F + 2));
+  L.slot_bytes = A.maxc > kMidCap ? al(plan_smem_bytes(A.R, A.words, A.maxc, nullptr, nullptr)) : 0;
+  const size_t slots = (F > 0 && L.slot_bytes) ? (size_t)plan_sms() * kHugeGrid : 0;
+  L.total = al(L.big_off + slots * L.slot_bytes) + 256;
   return L;
 }
 
@@ -879,12 +1042,15 @@ extern "C" mp_status mp_plan_windows(const mp_plan_params* p, const float* d_sco
   int* ws_count = (int*)(ws + L.count_off);
   int* ws_cls = (int*)(ws + L.cls_off);
   int* q_cnt = (int*)(ws + L.q_off);
-  int* q_list = q_cnt + 1;
+  int* q2_cnt = q_cnt + 1;
+  int* q_list = q_cnt + 2;
+  int* q2_list = q_list + F;
   if (F > 0) {
-    const size_t smem = plan_smem_bytes(A.R, A.words, A.maxc, nullptr, nullptr);
+    const int cap_full = A.maxc < kMidCap ? A.maxc : kMidCap;
+    const size_t smem = plan_smem_bytes(A.R, A.words, cap_full, nullptr, nullptr);
     if (smem > 227 * 1024) return MP_ERR_UNSUPPORTED;
     const size_t smem_fast = plan_smem_bytes(A.R, A.words, kFastCap < A.maxc ? kFastCap : A.maxc, nullptr, nullptr);
-    MP_CUDA_TRY(cudaMemsetAsync(q_cnt, 0, sizeof(int), s));
+    MP_CUDA_TRY(cudaMemsetAsync(q_cnt, 0, 2 * sizeof(int), s));
     MP_CUDA_TRY(cudaFuncSetAttribute(plan_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_fast));
     MP_CUDA_TRY(cudaFuncSetAttribute(plan_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -892,12 +1058,15 @@ extern "C" mp_status mp_plan_windows(const mp_plan_params* p, const float* d_sco
     plan_fast_kernel<<<F, kFastThreads, smem_fast, s>>>(Af, d_scores, d_mask, ws_win, ws_count, ws_cls, q_cnt,
                                                          q_list);
     MP_CUDA_TRY(cudaGetLastError());
-    int dev = 0, sms = 0;
-    MP_CUDA_TRY(cudaGetDevice(&dev));
-    MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    plan_full_kernel<<<sms * 2, kPlanThreads, smem, s>>>(A, d_scores, d_mask, ws_win, ws_count, ws_cls, q_cnt,
-                                                         q_list);
+    plan_full_kernel<<<plan_sms() * kFullGrid, kPlanThreads, smem, s>>>(
+        A, d_scores, d_mask, ws_win, ws_count, ws_cls, q_cnt, q_list, cap_full, q2_cnt, q2_list);
     MP_CUDA_TRY(cudaGetLastError());
+    if (L.slot_bytes) {   // grids whose worst case exceeds the shared-memory tiers
+      const size_t smem_huge = plan_smem_bytes(A.R, A.words, 0, nullptr, nullptr);
+      plan_huge_kernel<<<plan_sms() * kHugeGrid, kPlanThreads, smem_huge, s>>>(
+          A, d_scores, d_mask, ws_win, ws_count, ws_cls, q2_cnt, q2_list, ws + L.big_off, L.slot_bytes);
+      MP_CUDA_TRY(cudaGetLastError());
+    }
   }
   plan_scan_kernel<<<1, 1024, 0, s>>>(F, A.k, ws_count, ws_cls, d_frame_off, d_class_count, max_windows,
                                       d_status);
@@ -932,12 +1101,30 @@ extern "C" mp_status mp_proxy_sweep(const mp_plan_params* p, const float* d_scor
   int4* ws_win = (int4*)(ws + L.win_off);
   int* ws_count = (int*)(ws + L.count_off);
   int* ws_cls = (int*)(ws + L.cls_off);
-  // thresholds travel in the (graph-capturable) kernel parameter block
+  // thresholds travel in the (graph-capturable) kernel parameter block,
+  // sorted ascending (stable: equal thresholds keep their order) with their
+  // output rows
   SweepThr th;
-  for (int j = 0; j < kSweepMaxJ; j++) th.v[j] = j < J ? thresholds[j] : 0.0f;
+  for (int j = 0; j < kSweepMaxJ; j++) {
+    th.v[j] = j < J ? thresholds[j] : 0.0f;
+    th.idx[j] = j;
+  }
+  for (int a = 1; a < J; a++) {
+    const float v = th.v[a];
+    const int ix = th.idx[a];
+    int b = a - 1;
+    while (b >= 0 && th.v[b] > v) {
+      th.v[b + 1] = th.v[b];
+      th.idx[b + 1] = th.idx[b];
+      b--;
+    }
+    th.v[b + 1] = v;
+    th.idx[b + 1] = ix;
+  }
   MP_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(mp_sweep_result) * (size_t)J, s));
   if (F == 0) return MP_OK;
-  const size_t smem = plan_smem_bytes(A.R, A.words, A.maxc, nullptr, nullptr);
+  // planner layout + one rank byte per cell
+  const size_t smem = plan_smem_bytes(A.R, A.words, A.maxc, nullptr, nullptr) + (size_t)A.R * A.C;
   if (smem > 227 * 1024) return MP_ERR_UNSUPPORTED;
   MP_CUDA_TRY(cudaFuncSetAttribute(proxy_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   proxy_sweep_kernel<<<F, kSweepThreads, smem, s>>>(A, d_scores, th, J, (const float4*)d_dets, d_det_off, ws_win,

@@ -25,6 +25,24 @@ import torch
 from . import _binding as B
 
 
+class _ranges:
+    """Host-side range of one runner call, visible to nsys / ncu (NVTX) and to
+    torch.profiler traces (record_function)."""
+
+    def __init__(self, name):
+        self.name = name
+        self.rf = torch.profiler.record_function(name)
+
+    def __enter__(self):
+        torch.cuda.nvtx.range_push(self.name)
+        self.rf.__enter__()
+
+    def __exit__(self, *exc):
+        self.rf.__exit__(*exc)
+        torch.cuda.nvtx.range_pop()
+        return False
+
+
 class WindowPipeline:
     def __init__(self, W: int, H: int, sizes: Sequence[Tuple[int, int]], cost: Sequence[int],
                  out_dims: Sequence[Tuple[int, int]], b_proxy: float = 0.5, score_thr: float = 0.25,
@@ -198,7 +216,8 @@ class PipelinedRunner:
     the caching allocator does not hand their memory out while they are read.
     """
 
-    def __init__(self, pipes, device="cuda", merge_on_gather_stream: bool = False, side_streams: int = 1):
+    def __init__(self, pipes, device="cuda", merge_on_gather_stream: bool = False, side_streams: int = 1,
+                 plan_priority: bool = True):
         self.pipes = list(pipes)
         self.depth = len(self.pipes)
         self.dev = torch.device(device)
@@ -207,7 +226,11 @@ class PipelinedRunner:
         # their own streams (set k uses stream k mod side_streams), so the
         # plans (and merges) of two batches may overlap each other
         n = max(1, min(int(side_streams), self.depth))
-        self.s_plans = [torch.cuda.Stream(dev) for _ in range(n)]
+        # plan(i+1) gates gather(i+1): with plan_priority its streams have the
+        # highest priority, so the block scheduler places its CTAs before the
+        # remap/NMS CTAs that compete for the SM space the gather leaves
+        prio = torch.cuda.Stream.priority_range()[1] if plan_priority else 0
+        self.s_plans = [torch.cuda.Stream(dev, priority=prio) for _ in range(n)]
         self.s_plan = self.s_plans[0]
         self.s_gather = torch.cuda.Stream(dev)
         # merge_on_gather_stream: remap/NMS(i) runs right after gather(i) on the
@@ -220,6 +243,8 @@ class PipelinedRunner:
         self.pending = [False] * self.depth   # set k enqueued, merge not yet enqueued
         self.static = None                    # graph mode: runner-owned inputs per set
         self.i = 0
+        self._capturing = False
+        self.g_steps = None                   # capture_steps(): U whole steps as one graph
 
     # ------------------------------------------------------------ graphs
     def capture_graphs(self, scores, boxes=None, win_box_off=None):
@@ -250,6 +275,56 @@ class PipelinedRunner:
                 self.g_merge.append(g2)
         torch.cuda.synchronize(self.dev)
 
+    def capture_steps(self, batches, gather_events=None):
+        """Capture len(batches) consecutive whole steps — plan, gather and
+        remap/NMS of each batch on the runner's streams, with the same
+        cross-batch event ordering as `step` — as ONE CUDA graph;
+        `replay_steps()` then issues all of them with a single launch (small
+        batches, e.g. configs[0]'s 30 frames, are otherwise bound by the
+        host-side issue of ~20 launches and events per step).
+
+        batches: [(scores, frames, boxes, win_box_off), ...]; the graph keeps
+        reading these tensors (and the frames' addresses, baked into the TMA
+        descriptors), so the caller keeps them alive and rewrites them in place
+        between replays.  gather_events: optional [(start, end)] per batch,
+        created with torch.cuda.Event(enable_timing=True, external=True) so
+        they are recorded as graph nodes on every replay.  A replay starts
+        after all earlier work of the capture stream and ends with every
+        stream joined (no overlap across replays)."""
+        if any(self.pending):
+            raise RuntimeError("capture_steps with batches in flight")
+        if self.static is not None:
+            raise RuntimeError("capture_steps and capture_graphs are exclusive")
+        torch.cuda.synchronize(self.dev)
+        self.done = [None] * self.depth
+        self.gathered = [None] * self.depth
+        self.i = 0
+        cap = torch.cuda.Stream(self.dev)
+        g = torch.cuda.CUDAGraph()
+        self._capturing = True
+        try:
+            with torch.cuda.graph(g, stream=cap):
+                for u, (sc, fr, bx, wbo) in enumerate(batches):
+                    ev = gather_events[u] if gather_events is not None else None
+                    self.step(sc, fr, bx, wbo, gather_events=ev)
+                self.wait_all(cap)
+        finally:
+            self._capturing = False
+            self.done = [None] * self.depth
+            self.gathered = [None] * self.depth
+            self.pending = [False] * self.depth
+            self.i = 0
+        torch.cuda.synchronize(self.dev)
+        self.g_steps = g
+        self.n_graph_steps = len(batches)
+        return g
+
+    def replay_steps(self):
+        """Launch the captured steps on the current stream (see capture_steps)."""
+        if self.g_steps is None:
+            raise RuntimeError("replay_steps needs capture_steps()")
+        self.g_steps.replay()
+
     def inputs(self, k: Optional[int] = None):
         """Graph mode: the static (scores, boxes, win_box_off) tensors of
         buffer set k (default: the set the next `enqueue` uses).  A caller that
@@ -266,9 +341,8 @@ class PipelinedRunner:
         ev.record(torch.cuda.current_stream(self.dev))
         return ev
 
-    @staticmethod
-    def _use(t, stream):
-        if t is not None and t.is_cuda:
+    def _use(self, t, stream):
+        if t is not None and t.is_cuda and not self._capturing:
             t.record_stream(stream)
 
     @staticmethod
@@ -282,7 +356,8 @@ class PipelinedRunner:
                              f"{tuple(dst.shape)} {dst.dtype}")
         with torch.cuda.stream(stream):
             dst.copy_(src, non_blocking=True)
-        PipelinedRunner._use(src, stream)
+        if src.is_cuda:
+            src.record_stream(stream)
 
     # ------------------------------------------------------------ pipeline
     def enqueue(self, scores, frames, gather_events=None, proxy_events=None) -> int:
@@ -292,6 +367,10 @@ class PipelinedRunner:
         k = self.i % self.depth
         if self.pending[k]:
             raise RuntimeError(f"buffer set {k} still awaits merge() of batch {self.i - self.depth}")
+        with _ranges(f"mp.enqueue set {k}"):
+            return self._enqueue(k, scores, frames, gather_events, proxy_events)
+
+    def _enqueue(self, k, scores, frames, gather_events, proxy_events) -> int:
         p = self.pipes[k]
         s_plan = self.s_plans[k % len(self.s_plans)]
         ready = self._caller_ready()
@@ -344,6 +423,10 @@ class PipelinedRunner:
         detector's last read of pipes[k].outs and write of the boxes."""
         if not self.pending[k]:
             raise RuntimeError(f"buffer set {k} has no batch awaiting merge")
+        with _ranges(f"mp.merge set {k}"):
+            self._merge(k, boxes, win_box_off, detector_done)
+
+    def _merge(self, k, boxes, win_box_off, detector_done):
         p = self.pipes[k]
         s_merge = self.s_merges[k % len(self.s_merges)]
         s_merge.wait_event(self.gathered[k])

@@ -6,7 +6,7 @@ coordinates, R18-R20):
   value order), negative, denormal, tied, NaN and +-inf scores reach the
   GPU sort;
 * NaN and +-inf box coordinates (R18 clips with fmin/fmax: NaN -> the bound);
-* frames with more raw boxes than the shared-memory tiers hold (> 2048):
+* frames with more raw boxes than the shared-memory tiers hold (> 1024):
   the global-memory path, alone and mixed with small frames in one call;
 * Hungarian (R24): the GPU matching of tie-heavy problems is optimal —
   its total equals scipy's linear_sum_assignment optimum, computed
@@ -65,7 +65,7 @@ def _edge_frame(rng, n, score_pool, coords=None):
 @pytest.mark.parametrize("n", [20, 64, 300, 1500])
 def test_nms_scores_le_zero_and_specials(G, thr, n):
     """Every special score value reaches the sort for thresholds <= 0 (one
-    frame per tier: warp <= 64, CTA <= 512, large <= 2048)."""
+    frame per tier: warp <= 64, CTA <= 512, large <= 1024)."""
     rng = np.random.default_rng(n + 7)
     rows = _edge_frame(rng, n, EDGE_SCORES)
     rows["score"][:len(EDGE_SCORES)] = EDGE_SCORES[:min(n, len(EDGE_SCORES))]
@@ -92,10 +92,11 @@ def test_nms_nonfinite_coordinates(G, n):
         _nms_compare(G, rows, [0, n], win, [0, 1], [(192, 160)], 1920, 1080, thr, 0.5)
 
 
-@pytest.mark.parametrize("n", [2049, 3000, 6100])
+@pytest.mark.parametrize("n", [300, 1024, 1025, 2049, 3000, 6100])
 def test_nms_beyond_shared_memory_tiers(G, n):
-    """One frame with more raw boxes than the 2048 the shared-memory tiers
-    hold: the global-memory path, tie-heavy, two IoU thresholds."""
+    """One frame around / beyond the 1024 raw boxes the shared-memory tiers
+    hold (the large tier's 256-candidate bitmask, its tiled path, then the
+    global-memory path), tie-heavy, two IoU thresholds."""
     rng = np.random.default_rng(n)
     rows = np.zeros(n, O.BOX_DTYPE)
     xy = rng.integers(0, 1800, (n, 2)).astype(np.float32)
@@ -110,12 +111,12 @@ def test_nms_beyond_shared_memory_tiers(G, n):
 
 
 def test_nms_mixed_tiers_in_one_call(G):
-    """Frames of 0, 10, 64, 65, 600, 2048, 2049, 4500 and 30 raw boxes (spread
+    """Frames of 0, 10, 64, 65, 600, 1024, 1025, 2049, 4500 and 30 raw boxes (spread
     over several windows each) in one call: every tier including the
     global-memory one runs in the same launch sequence, and each frame's
     keep list equals the oracle's."""
     rng = np.random.default_rng(77)
-    sizes = [0, 10, 64, 65, 600, 2048, 2049, 4500, 30]
+    sizes = [0, 10, 64, 65, 600, 1024, 1025, 2049, 4500, 30]
     windows, wbo, frame_off, chunks = [], [0], [0], []
     for f, n in enumerate(sizes):
         nw = 1 if n < 100 else 3

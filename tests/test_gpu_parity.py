@@ -128,10 +128,32 @@ def test_plan_capacity_and_zero_frames(G):
 
 def test_plan_unsupported_grid(G):
     import paper_2103_14695_b200 as mp
-    with pytest.raises(mp.MPError) as e:     # 128 x 128 cells: beyond one CTA's shared memory
-        G.gpu_plan(4096, 4096, 32, 32, 0.5, [(256, 256), (4096, 4096)], [80, 16400],
-                   np.zeros((1, 128, 128), np.float32))
+    with pytest.raises(mp.MPError) as e:     # 128 x 129 cells > 16384
+        G.gpu_plan(4128, 4096, 32, 32, 0.5, [(256, 256), (4128, 4096)], [80, 16400],
+                   np.zeros((1, 128, 129), np.float32))
     assert e.value.code == mp.MP_ERR_UNSUPPORTED
+
+
+def test_plan_largest_grid_global_scratch(G):
+    """128 x 128 cells (the R*C limit): frames with more than the full tier's
+    1024 shared-memory runs plan over the CTA's global scratch slot (up to
+    R*ceil(C/2) = 8192 runs) with the same results as the oracle."""
+    W = H = 4096
+    sizes, cost = [(256, 256), (1024, 1024), (4096, 4096)], [80, 1040, 10 ** 9]   # full frame never pays
+    rng = np.random.default_rng(5)
+    grids = [np.zeros((128, 128), np.float32)]
+    for n_blobs in (150, 400, 700):           # narrow blobs: 743 / 1623 / ~2700 runs (> 1024: global scratch)
+        g = np.zeros((128, 128), np.float32)
+        for _ in range(n_blobs):
+            r, c = rng.integers(0, 120), rng.integers(0, 126)
+            g[r:r + rng.integers(3, 9), c:c + rng.integers(1, 3)] = 0.9
+        grids.append(g)
+    stripes = np.zeros((128, 128), np.float32)
+    stripes[:, ::3] = 0.9                     # 128 x 43 runs, 43 components
+    grids.append(stripes)
+    scores = np.stack(grids)
+    ref, got = _plan_both(G, W, H, 32, 32, 0.5, sizes, cost, scores)
+    _assert_plan_equal(ref, got)
 
 
 def test_plan_invalid_params_raise(G):
@@ -251,10 +273,11 @@ def test_remap_nms_parity_configs(G, name, frames):
                  cfg.iou_thr)
 
 
-@pytest.mark.parametrize("n", [0, 1, 63, 64, 65, 511, 512, 513, 1023, 1024, 1025, 2048])
+@pytest.mark.parametrize("n", [0, 1, 63, 64, 65, 255, 256, 257, 511, 512, 513, 1023, 1024, 1025, 2048])
 def test_nms_parity_frame_sizes(G, n):
-    """Tie-heavy single frames around every tier boundary (small <= 512,
-    bitmask <= 1024, on-the-fly <= 2048)."""
+    """Tie-heavy single frames around every tier boundary (warp <= 64, small
+    <= 512, large <= 1024 with a <= 256-candidate bitmask then 64-candidate
+    tiles, global memory beyond)."""
     rng = np.random.default_rng(n)
     rows = np.zeros(n, O.BOX_DTYPE)
     xy = rng.integers(0, 300, (n, 2)).astype(np.float32)

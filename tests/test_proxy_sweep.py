@@ -93,3 +93,39 @@ def test_gpu_sweep_parity(name, frames):
                       out, ws)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), ref)
+
+
+@pytest.mark.gpu
+def test_gpu_sweep_single_pass_edges():
+    """The single-pass sweep ranks each cell once against the SORTED
+    thresholds and re-uses a plan when a threshold leaves the mask unchanged:
+    unsorted / duplicated / +-inf thresholds, scores exactly equal to a
+    threshold, NaN and +-inf scores, and a quantised score grid where most
+    thresholds select identical masks."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2103_14695_b200 as mp
+    cfg, scores, dets, det_off = _workload("c5_1080p_clips", 5, 60)
+    rng = np.random.default_rng(11)
+    q = np.round(scores * 4) / 4                      # values in {0, .25, .5, .75, 1}: few distinct masks
+    q = q.astype(np.float32)
+    q[rng.random(q.shape) < 0.01] = np.nan
+    q[rng.random(q.shape) < 0.005] = np.inf
+    q[rng.random(q.shape) < 0.005] = -np.inf
+    th = [0.5, 0.25, 0.5, 0.3, 0.75, -np.inf, np.inf, 0.74999994, 0.25, 1.0, 0.0, 0.6, 0.7, 0.5]
+    st, ref = O.proxy_sweep(cfg.W, cfg.H, 32, 32, cfg.sizes, cfg.cost, q, th, dets, det_off)
+    assert st == 0
+    dev = torch.device("cuda:0")
+    p = mp.PlanParams(cfg.W, cfg.H, cfg.sizes, cfg.cost)
+    F = q.shape[0]
+    out = torch.full((len(th), 5), -1, dtype=torch.int64, device=dev)
+    ws = torch.empty(mp.mp_proxy_sweep_workspace_size(p, F), dtype=torch.uint8, device=dev)
+    mp.mp_proxy_sweep(p, torch.from_numpy(q).to(dev), F, th, torch.from_numpy(dets).to(dev),
+                      torch.from_numpy(det_off).to(dev), out, ws)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert np.array_equal(got, ref)
+    # duplicated thresholds give identical rows; thresholds between two grid values too
+    assert np.array_equal(got[0], got[2]) and np.array_equal(got[1], got[8])
+    assert np.array_equal(got[11], got[12]) and np.array_equal(got[11], got[0]) and np.array_equal(got[7], got[0])
