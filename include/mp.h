@@ -107,10 +107,11 @@ size_t mp_plan_workspace_size(const mp_plan_params* p, int32_t F);
  *  d_status      device int32: set to MP_ERR_CAPACITY if total > max_windows.
  *  Execution: one CTA per frame; frames with <= 256 horizontal runs of
  *  positive cells are planned in shared memory by a 128-thread tier, others by
- *  a persistent 256-thread tier whose CTAs hold up to 1024 runs in shared
- *  memory (~33 KB, so they fit beside a persistent gather CTA on the same SM)
- *  and move the run/component arrays of larger frames (up to R*ceil(C/2)
- *  runs) to a per-CTA global scratch slot in d_ws (same arithmetic).
+ *  a persistent 128-thread tier whose CTAs hold up to 1024 runs in shared
+ *  memory (~36 KB, so they fit beside a persistent gather CTA on the same SM);
+ *  frames with more runs (up to R*ceil(C/2)) are planned by a third tier
+ *  whose run/component arrays live in a per-CTA global scratch slot in d_ws
+ *  (same arithmetic).
  *  Limits: R*C <= 16384 cells (4K at 32 px = 8160); larger grids return
  *  MP_ERR_UNSUPPORTED.
  */

@@ -324,6 +324,67 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
       H[p][2] = PREV[p][2];                                                                     \
     }                                                                                           \
   }
+  // RGB taps, two ways (measured, c2/c3/c4 gather alone, same box):
+  //  * bytes: 6 LDS.U8 + 6 IADD (2^23 + byte) per column — f32 output
+  //    (word taps there: 1.36 -> 1.43 ms at c2);
+  //  * words (u8 output, kWordTaps): a column's 6 tap bytes [a, a+6) lie in
+  //    the three aligned words from a & ~3 (the alignment of a is the same in
+  //    every staged row: rows are 16-B multiples apart); two funnel shifts
+  //    align them and one PRMT per byte builds the 2^23 + byte pattern:
+  //    3 LDS.32 + 2 SHF + 6 PRMT per column, half the shared-memory
+  //    wavefronts of the consumer-bound u8 kernel (c2 1.105 -> 1.089 ms,
+  //    c3 4.93 -> 4.87, c4 3.13 -> 3.09).
+#ifdef MP_WORD_TAPS
+  constexpr bool kWordTaps = SRC == kSrcRGB24;
+#else
+  constexpr bool kWordTaps = SRC == kSrcRGB24 && FMT == MP_OUT_U8_NHWC;
+#endif
+  unsigned int wa[NP], wb[NP], sa[NP], sb[NP];
+#pragma unroll
+  for (int p = 0; p < NP; p++) {
+    wa[p] = ba[p] & ~3u;
+    wb[p] = bb[p] & ~3u;
+    sa[p] = (ba[p] & 3u) * 8u;
+    sb[p] = (bb[p] & 3u) * 8u;
+  }
+#define MP_W6(WB, SH, LO, HI)                                                                   \
+  {                                                                                             \
+    const uint32_t w0_ = *reinterpret_cast<const uint32_t*>(&smem[WB]);                         \
+    const uint32_t w1_ = *reinterpret_cast<const uint32_t*>(&smem[(WB) + 4]);                   \
+    const uint32_t w2_ = *reinterpret_cast<const uint32_t*>(&smem[(WB) + 8]);                   \
+    LO = __funnelshift_r(w0_, w1_, SH);                                                         \
+    HI = __funnelshift_r(w1_, w2_, SH);                                                         \
+  }
+#define MP_MB(W, K) __int_as_float(__byte_perm((W), 0x4B000000u, 0x7440u | (K)))
+#define MP_HRGB(O_, H)                                                                          \
+  if (kWordTaps) {                                                                              \
+    _Pragma("unroll") for (int p = 0; p < NP; p++) {                                            \
+      uint32_t la_, ha_, lb_, hb_;                                                              \
+      MP_W6(wa[p] + (O_), sa[p], la_, ha_)                                                      \
+      MP_W6(wb[p] + (O_), sb[p], lb_, hb_)                                                      \
+      {                                                                                         \
+        const float2 m_ = make_float2(MP_MB(la_, 0), MP_MB(lb_, 0));                            \
+        const float2 n_ = make_float2(MP_MB(la_, 3), MP_MB(lb_, 3));                            \
+        H[p][0] = ffma2_w(fsub2(n_, m_), lx[p], fsub2(m_, M2));                                 \
+      }                                                                                         \
+      {                                                                                         \
+        const float2 m_ = make_float2(MP_MB(la_, 1), MP_MB(lb_, 1));                            \
+        const float2 n_ = make_float2(MP_MB(ha_, 0), MP_MB(hb_, 0));                            \
+        H[p][1] = ffma2_w(fsub2(n_, m_), lx[p], fsub2(m_, M2));                                 \
+      }                                                                                         \
+      {                                                                                         \
+        const float2 m_ = make_float2(MP_MB(la_, 2), MP_MB(lb_, 2));                            \
+        const float2 n_ = make_float2(MP_MB(ha_, 1), MP_MB(hb_, 1));                            \
+        H[p][2] = ffma2_w(fsub2(n_, m_), lx[p], fsub2(m_, M2));                                 \
+      }                                                                                         \
+    }                                                                                           \
+  } else {                                                                                      \
+    _Pragma("unroll") for (int p = 0; p < NP; p++) {                                            \
+      const unsigned int pa_ = ba[p] + (O_), pb_ = bb[p] + (O_);                                \
+      _Pragma("unroll") for (int ch = 0; ch < 3; ch++)                                          \
+          MP_HL(H, ch, pa_ + ch, pb_ + ch, pa_ + 3 + ch, pb_ + 3 + ch)                          \
+    }                                                                                           \
+  }
   // horizontal lerps of one staged source row: luma/RGB row at byte offset
   // O_, its chroma row (NV12) at OC_ (both relative to the staged boxes)
 #define MP_H(O_, OC_, H)                                                                        \
@@ -337,11 +398,7 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
         MP_HC(H, ca[p] + oc_, cb[p] + oc_)                                                      \
       }                                                                                         \
     } else {                                                                                    \
-      _Pragma("unroll") for (int p = 0; p < NP; p++) {                                          \
-        const unsigned int pa_ = ba[p] + o_, pb_ = bb[p] + o_;                                  \
-        _Pragma("unroll") for (int ch = 0; ch < 3; ch++)                                        \
-            MP_HL(H, ch, pa_ + ch, pb_ + ch, pa_ + 3 + ch, pb_ + 3 + ch)                        \
-      }                                                                                         \
+      MP_HRGB(o_, H)                                                                            \
     }                                                                                           \
   }
   // dense staging: source row r of the box (rows r_lo..); its chroma row is
@@ -447,6 +504,9 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
 #undef MP_HY
 #undef MP_HC
 #undef MP_HL
+#undef MP_HRGB
+#undef MP_W6
+#undef MP_MB
 }
 
 template <int FMT, int SRC>

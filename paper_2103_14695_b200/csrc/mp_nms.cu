@@ -9,14 +9,16 @@
 //                               ballot compaction, rank sort of the (score
 //                               desc, index) keys, 64-bit IoU row masks, greedy
 //                               scan; larger frames are queued
-//   nms_small_kernel   4/SM     queued frames with <= 512 raw boxes, one CTA each:
-//                               block compaction, bitonic sort, n x ceil(n/64)
-//                               IoU bitmask, warp-0 greedy scan
-//   nms_large_kernel   1/SM     queued frames (<= 1024 raw boxes in shared memory:
-//                               bitmask up to 256 candidates, tiled 64-candidate
-//                               blocks beyond; frames with more raw boxes run the
-//                               same tiled greedy over global-memory scratch, with
-//                               a merge sort of the keys — no per-frame limit)
+//   nms_small_kernel   6/SM     queued frames with <= 512 raw boxes, one 128-thread CTA
+//                               each (persistent): block compaction, bitonic sort,
+//                               then above 96 candidates (iou_thr >= 0) a
+//                               spatial-grid sparse adjacency + warp-0 greedy,
+//                               else an n x ceil(n/64) IoU bitmask (<= 128
+//                               candidates) or 64-candidate tiles
+//   nms_large_kernel   2/SM     queued frames with <= 1024 raw boxes, the same
+//                               steps (128 threads); frames with more raw boxes
+//                               run the tiled greedy over global-memory scratch,
+//                               with a merge sort of the keys — no per-frame limit
 //   nms_scan_kernel    1 CTA    kept-box CSR per frame, capacity check
 //   nms_scatter_kernel          compact kept boxes into the caller's buffers
 #include "mp_internal.cuh"
@@ -30,13 +32,13 @@ struct NmsArgs {
   int ow[kMaxClasses], oh[kMaxClasses];
 };
 
-constexpr int kSmallCap = 512, kSmallThreads = 256;
+constexpr int kSmallCap = 512, kSmallMaskCap = 128, kSmallThreads = 128;
 // Every tier's CTA fits in what the persistent gather CTA leaves of an SM
 // (<= 54 KB of shared memory = kSideReserve in mp_gather.cu, <= 16K registers), so the
 // remap/NMS of batch i-1 runs beside gather(i) instead of queueing behind it
 // (the former 1024-thread, 207-KB large tier could not start on any SM until
 // the gather ended: c4 step = gather + NMS/plan tail).
-constexpr int kLargeCap = 1024, kLargeMaskCap = 256, kLargeThreads = 256;
+constexpr int kLargeCap = 1024, kLargeMaskCap = 128, kLargeThreads = 128;
 
 struct NmsSmem {
   float4* bx;
@@ -50,6 +52,7 @@ struct NmsSmem {
   int* tmp;
   unsigned long long* bmask;  // tiled path: one 64-candidate block's IoU masks
   int* bkeep;                 // tiled path: candidates kept in the current block
+  unsigned int ubytes;        // bytes of the key region (grid path scratch)
 };
 
 __host__ __device__ inline int pow2_at_least(int n) {
@@ -83,6 +86,7 @@ __host__ __device__ inline size_t nms_smem_bytes(int cap, int mask_cap, NmsSmem*
   if (permb > u) u = permb;
   s.key = (unsigned long long*)take(u);
   s.supp = (unsigned char*)s.key;
+  s.ubytes = (unsigned int)u;
   if (S) *S = s;
   return off;
 }
@@ -133,6 +137,152 @@ __device__ __forceinline__ int window_of(const int* __restrict__ off, int lo, in
     else hi = mid;
   }
   return lo;
+}
+
+// ---- a7 over a spatial grid (iou_thr >= 0): a pair can only suppress if the
+// boxes intersect with positive area (IoU > thr >= 0 needs inter > 0; remap
+// drops degenerate boxes), so each candidate is tested only against the
+// candidates whose top-left corner lies in its own or a neighbouring cell of a
+// grid whose cells are wider / taller than every candidate box.  The tested
+// pairs produce a sparse adjacency (j > i, same class, iou_rn > thr — the very
+// predicate of the bitmask paths), and warp 0 runs the greedy over it in score
+// order: the same keep list as the dense paths, with O(n) instead of O(n^2)
+// IoUs for the spread-out boxes of traffic / drone frames (c4: ~880 raw boxes
+// per frame).  Scratch = the key region (free after the permutation).
+// Returns the kept count, or -1 if the adjacency does not fit (the caller
+// then runs a dense path).
+constexpr int kGridMaxCells = 1024;
+constexpr int kGridMin = 96;   // candidates above which the grid path runs (below: the bitmask)
+
+__device__ int nms_grid(const NmsArgs& A, const NmsSmem& S, int n) {
+  const int tid = threadIdx.x, lane = tid & 31, BS = blockDim.x;
+  // cell table size: 1/16 of the scratch (cell ends are ints), <= kGridMaxCells
+  const int Gmax = min(kGridMaxCells, (int)(S.ubytes / 16));
+  const int G = Gmax;
+  int* red = S.tmp + 40;   // fp32 bits of min x1, min y1, max x1, max y1, max w, max h (all >= 0)
+  if (tid < 6) red[tid] = tid < 2 ? 0x7f7fffff : 0;
+  __syncthreads();
+  {
+    float v[6] = {3.4e38f, 3.4e38f, 0.f, 0.f, 0.f, 0.f};
+    for (int p = tid; p < n; p += BS) {
+      const float4 b = S.bx[p];
+      v[0] = fminf(v[0], b.x);
+      v[1] = fminf(v[1], b.y);
+      v[2] = fmaxf(v[2], b.x);
+      v[3] = fmaxf(v[3], b.y);
+      v[4] = fmaxf(v[4], __fsub_rn(b.z, b.x));
+      v[5] = fmaxf(v[5], __fsub_rn(b.w, b.y));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      v[0] = fminf(v[0], __shfl_xor_sync(0xffffffffu, v[0], o));
+      v[1] = fminf(v[1], __shfl_xor_sync(0xffffffffu, v[1], o));
+#pragma unroll
+      for (int t = 2; t < 6; t++) v[t] = fmaxf(v[t], __shfl_xor_sync(0xffffffffu, v[t], o));
+    }
+    if (lane == 0) {
+      atomicMin(&red[0], __float_as_int(v[0]));
+      atomicMin(&red[1], __float_as_int(v[1]));
+#pragma unroll
+      for (int t = 2; t < 6; t++) atomicMax(&red[t], __float_as_int(v[t]));
+    }
+  }
+  __syncthreads();
+  const float mnx = __int_as_float(red[0]), mny = __int_as_float(red[1]);
+  const float spx = __int_as_float(red[2]) - mnx, spy = __int_as_float(red[3]) - mny;
+  // cells strictly wider / taller than any box (margin for the rounding of
+  // the widths and of the cell index): an intersecting j has its corner in
+  // the cell of i's corner or a neighbour.  As many cells as fit the scratch
+  // (<= Gmax, about one candidate per cell for spread-out boxes): the
+  // minimal cells, scaled up evenly when there would be more.
+  const float mwx = __int_as_float(red[4]) * 1.0625f + 1.0f, mwy = __int_as_float(red[5]) * 1.0625f + 1.0f;
+  float fx = spx / mwx + 1.0f, fy = spy / mwy + 1.0f;
+  if (fx * fy > (float)Gmax) {
+    const float sc = sqrtf((float)Gmax / (fx * fy));
+    fx = fmaxf(1.0f, fx * sc);
+    fy = fmaxf(1.0f, fy * sc);
+  }
+  int gx = max(1, min((int)fx, Gmax));
+  int gy = max(1, min((int)fy, Gmax / gx));
+  const float cwx = fmaxf(mwx, spx / (float)gx), cwy = fmaxf(mwy, spy / (float)gy);
+  gx = min(gx, (int)(spx / cwx) + 1);
+  gy = min(gy, (int)(spy / cwy) + 1);
+  auto cell_x = [&](float x) { return min(gx - 1, (int)((x - mnx) / cwx)); };
+  auto cell_y = [&](float y) { return min(gy - 1, (int)((y - mny) / cwy)); };
+  // key-region layout: cell ends [G], members u16 [n], adjacency offsets [n+1],
+  // suppression flags u8 [n], adjacency u16 [rest]
+  unsigned char* base = reinterpret_cast<unsigned char*>(S.key);
+  int* cend = reinterpret_cast<int*>(base);
+  unsigned short* cellm = reinterpret_cast<unsigned short*>(base + 4 * G);
+  int* off = reinterpret_cast<int*>(base + ((4 * G + 2 * n + 15) & ~15));
+  unsigned char* supp = reinterpret_cast<unsigned char*>(off) + (((n + 1) * 4 + 15) & ~15);
+  unsigned short* adj = reinterpret_cast<unsigned short*>(supp + ((n + 15) & ~15));
+  const int cap_adj = (int)(((long long)S.ubytes - (long long)(reinterpret_cast<unsigned char*>(adj) - base)) / 2);
+  for (int c = tid; c < G; c += BS) cend[c] = 0;
+  __syncthreads();
+  for (int p = tid; p < n; p += BS) atomicAdd(&cend[cell_y(S.bx[p].y) * gx + cell_x(S.bx[p].x)], 1);
+  __syncthreads();
+  block_excl_scan_smem(cend, gx * gy, S.tmp);   // cend[c] = start of cell c
+  for (int p = tid; p < n; p += BS) {
+    const int c = cell_y(S.bx[p].y) * gx + cell_x(S.bx[p].x);
+    cellm[atomicAdd(&cend[c], 1)] = (unsigned short)p;   // afterwards cend[c] = end of cell c
+  }
+  __syncthreads();
+  const float thr = A.iou_thr;
+  // pass 0: count each candidate's suppressees; pass 1: write them
+  for (int pass = 0; pass < 2; pass++) {
+    for (int i = tid; i < n; i += BS) {
+      const float4 bi = S.bx[i];
+      const int ci = S.cls[i];
+      const int cx = cell_x(bi.x), cy = cell_y(bi.y);
+      int d = 0, w = pass ? off[i] : 0;
+      for (int yy = max(cy - 1, 0); yy <= min(cy + 1, gy - 1); yy++) {
+        for (int xx = max(cx - 1, 0); xx <= min(cx + 1, gx - 1); xx++) {
+          const int c = yy * gx + xx;
+          for (int k = (c ? cend[c - 1] : 0); k < cend[c]; k++) {
+            const int j = cellm[k];
+            if (j > i && S.cls[j] == ci && iou_rn(bi, S.bx[j]) > thr) {
+              if (pass) adj[w + d] = (unsigned short)j;
+              d++;
+            }
+          }
+        }
+      }
+      if (!pass) off[i] = d;
+    }
+    __syncthreads();
+    if (!pass) {
+      const int total = block_excl_scan_smem(off, n, S.tmp);
+      if (total > cap_adj) return -1;   // (uniform)
+      for (int p = tid; p < n; p += BS) supp[p] = 0;
+      if (tid == 0) off[n] = total;
+      __syncthreads();
+    }
+  }
+  // greedy in score order (warp 0): per chunk of 32 candidates, repeatedly
+  // take the first candidate neither suppressed nor already kept, keep it and
+  // flag its suppressees (later chunk members included, re-read next round)
+  if (threadIdx.x < 32) {
+    int nk = 0;
+    for (int b0 = 0; b0 < n; b0 += 32) {
+      const int i = b0 + lane;
+      uint32_t taken = 0;
+      while (true) {
+        const uint32_t free = __ballot_sync(0xffffffffu, i < n && !supp[i]) & ~taken;
+        if (!free) break;
+        const int b = __ffs(free) - 1;
+        const int k = b0 + b;
+        taken |= 1u << b;
+        if (lane == 0) S.keep[nk] = k;
+        nk++;
+        for (int e = off[k] + lane; e < off[k + 1]; e += 32) supp[adj[e]] = 1;
+        __syncwarp();
+      }
+    }
+    if (lane == 0) S.tmp[32] = nk;
+  }
+  __syncthreads();
+  return S.tmp[32];
 }
 
 // Process one frame with the whole CTA.  Returns nothing; writes kept boxes to
@@ -222,8 +372,12 @@ __device__ void nms_frame(const NmsArgs& A, int f, int b_lo, int b_hi, int w_lo,
   }
 
   // ---- a7: greedy class-aware NMS
-  int nk = 0;
-  if (n <= mask_cap) {
+  int nk = -1;
+  if (n > kGridMin && A.iou_thr >= 0.0f) nk = nms_grid(A, S, n);
+  if (nk >= 0) {
+    // kept by the grid path
+  } else if (n <= mask_cap) {
+    nk = 0;
     const int words = (n + 63) >> 6;
     unsigned long long* mask = S.key;
     for (int idx = tid; idx < n * words; idx += blockDim.x) {
@@ -260,6 +414,7 @@ __device__ void nms_frame(const NmsArgs& A, int f, int b_lo, int b_hi, int w_lo,
     __syncthreads();
     nk = S.tmp[32];
   } else {
+    nk = 0;
     // Tiled greedy for large frames (identical result to the sequential scan):
     // for each block of 64 sorted candidates, (a) the block's 64x64 IoU masks,
     // (b) one thread resolves the block sequentially against those masks and
@@ -640,7 +795,7 @@ __global__ void __launch_bounds__(kSmallThreads) nms_small_kernel(NmsArgs A, con
                                                                   int* __restrict__ large_list, int* __restrict__ d_status) {
   extern __shared__ __align__(16) unsigned char smem[];
   NmsSmem S;
-  nms_smem_bytes(kSmallCap, kSmallCap, &S, smem);
+  nms_smem_bytes(kSmallCap, kSmallMaskCap, &S, smem);
   const int nm = *mid_cnt;
   for (int li = blockIdx.x; li < nm; li += gridDim.x) {
     const int f = mid_list[li];
@@ -650,7 +805,7 @@ __global__ void __launch_bounds__(kSmallThreads) nms_small_kernel(NmsArgs A, con
       if (threadIdx.x == 0) large_list[atomicAdd(large_cnt, 1)] = f;
       continue;
     }
-    nms_frame(A, f, b_lo, b_hi, w_lo, w_hi, S, kSmallCap, kSmallCap, boxes, win_box_off, windows, ws_box, ws_src,
+    nms_frame(A, f, b_lo, b_hi, w_lo, w_hi, S, kSmallCap, kSmallMaskCap, boxes, win_box_off, windows, ws_box, ws_src,
               ws_kept);
     __syncthreads();
   }
@@ -801,7 +956,7 @@ extern "C" mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_bo
   cudaStream_t s = (cudaStream_t)stream;
   if (F > 0) {
     MP_CUDA_TRY(cudaMemsetAsync(lcnt, 0, 2 * sizeof(int), s));
-    const size_t sm_small = nms_smem_bytes(kSmallCap, kSmallCap, nullptr, nullptr);
+    const size_t sm_small = nms_smem_bytes(kSmallCap, kSmallMaskCap, nullptr, nullptr);
     const size_t sm_large = nms_smem_bytes(kLargeCap, kLargeMaskCap, nullptr, nullptr);
     MP_CUDA_TRY(cudaFuncSetAttribute(nms_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_small));
     MP_CUDA_TRY(cudaFuncSetAttribute(nms_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_large));
@@ -811,11 +966,11 @@ extern "C" mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_bo
     int dev = 0, sms = 0;
     MP_CUDA_TRY(cudaGetDevice(&dev));
     MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    nms_small_kernel<<<sms * 4, kSmallThreads, sm_small, s>>>(A, d_boxes, d_win_box_off, d_windows, d_frame_off,
+    nms_small_kernel<<<sms * 6, kSmallThreads, sm_small, s>>>(A, d_boxes, d_win_box_off, d_windows, d_frame_off,
                                                              ws_box, ws_src, ws_kept, mcnt, mlist, lcnt, llist,
                                                              d_status);
     MP_CUDA_TRY(cudaGetLastError());
-    nms_large_kernel<<<sms, kLargeThreads, sm_large, s>>>(A, d_boxes, d_win_box_off, d_windows, d_frame_off,
+    nms_large_kernel<<<sms * 2, kLargeThreads, sm_large, s>>>(A, d_boxes, d_win_box_off, d_windows, d_frame_off,
                                                           ws_box, ws_src, ws_kept, lcnt, llist, g, d_status);
     MP_CUDA_TRY(cudaGetLastError());
   }

@@ -166,6 +166,18 @@ extern __shared__ __align__(16) unsigned char smem_raw[];
 // appends the merged cluster and finds the next i, then publishes.
 constexpr int kAbsList = 64;   // absorbed members recorded by warp 0 (beyond: block-wide mark)
 
+#ifdef MP_PLAN_PROF
+// development builds only (-DMP_PLAN_PROF): thread 0's clock64 cycles per
+// cooperative-merge phase, summed over all CTAs: [0] arg-min + its barrier,
+// [1] fit ballots + barrier, [2] warp-0 walk + publish barrier, [3] steps
+__device__ unsigned long long g_plan_prof[4];
+#define MP_PROF_T(v) long long v = clock64();
+#define MP_PROF_ADD(k, d) if (threadIdx.x == 0) atomicAdd(&g_plan_prof[k], (unsigned long long)(d));
+#else
+#define MP_PROF_T(v)
+#define MP_PROF_ADD(k, d)
+#endif
+
 __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n, int cap) {
   __shared__ unsigned long long red[64];
   __shared__ int pub[8];
@@ -222,6 +234,7 @@ __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n, int cap) 
     while (i < len && alive >= 2) {
       if (len >= cap) i = compact(i);   // full: no room to append a merged cluster
       gen++;
+      MP_PROF_T(t0)
       const int ic0 = S.bc0[i], ir0 = S.br0[i], ic1 = S.bc1[i], ir1 = S.br1[i];
       const int sx = ic0 + ic1, sy = ir0 + ir1;
       unsigned long long best = ~0ull;
@@ -233,6 +246,7 @@ __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n, int cap) 
         best = key < best ? key : best;
       }
       best = block_min_u64(best, red, par);
+      MP_PROF_T(t1)
       const int j = (int)(best & 0xffffffffu);
       int m0 = min(ic0, S.bc0[j]), n0 = min(ir0, S.br0[j]);
       int m1 = max(ic1, S.bc1[j]), n1 = max(ir1, S.br1[j]);
@@ -254,6 +268,7 @@ __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n, int cap) 
         if (lane == 0) fitm[c] = msk;
       }
       __syncthreads();
+      MP_PROF_T(t2)
       if (wid == 0) {
         // absorption (k ascending, each fitting cluster at once, R7) over the
         // initial candidates only
@@ -341,6 +356,11 @@ __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n, int cap) 
         }
       }
       __syncthreads();
+      MP_PROF_T(t3)
+      MP_PROF_ADD(0, t1 - t0)
+      MP_PROF_ADD(1, t2 - t1)
+      MP_PROF_ADD(2, t3 - t2)
+      MP_PROF_ADD(3, 1)
       const int acc = pub[0];
       i = pub[1];
       if (acc) {
@@ -1078,6 +1098,17 @@ extern "C" mp_status mp_plan_windows(const mp_plan_params* p, const float* d_sco
   }
   return MP_OK;
 }
+
+#ifdef MP_PLAN_PROF
+extern "C" int mp_debug_plan_prof(unsigned long long* out4, int reset) {
+  if (cudaMemcpyFromSymbol(out4, g_plan_prof, sizeof(g_plan_prof)) != cudaSuccess) return -1;
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(g_plan_prof, z, sizeof(z)) != cudaSuccess) return -1;
+  }
+  return 0;
+}
+#endif
 
 extern "C" size_t mp_proxy_sweep_workspace_size(const mp_plan_params* p, int32_t F) {
   return mp_plan_workspace_size(p, F);

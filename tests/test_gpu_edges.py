@@ -172,3 +172,37 @@ def test_hungarian_tie_heavy_is_optimal(G, floor):
         got = float(vals.astype(np.float64).sum())
         assert abs(got - best) <= 1e-9 * max(1.0, best), (b, got, best)
         assert abs(tot[b] - got) <= 1e-9 * max(1.0, got)
+
+
+# --------------------------------------------------------------------------- spatial-grid NMS path
+@pytest.mark.parametrize("iou", [0.0, 0.5, 0.9, 1.0, -0.25])
+@pytest.mark.parametrize("n,layout", [(97, "spread"), (500, "spread"), (1000, "spread"), (900, "giant"),
+                                      (1000, "stacked"), (480, "grid_edges")])
+def test_nms_grid_path(G, n, layout, iou):
+    """Frames above 96 candidates with iou_thr >= 0 take the spatial-grid
+    path (sparse adjacency of intersecting same-class pairs, greedy over it);
+    iou_thr < 0 keeps the dense paths.  Layouts: drone-like boxes spread over
+    a 4K frame; the same plus one frame-sized box (cells become the whole
+    frame); 1000 near-identical stacked boxes (the adjacency overflows its
+    scratch -> dense fallback); boxes on exact cell-size multiples."""
+    rng = np.random.default_rng(n * 7 + len(layout))
+    rows = np.zeros(n, O.BOX_DTYPE)
+    if layout == "stacked":
+        xy = 100 + rng.integers(0, 3, (n, 2)).astype(np.float32)
+        wh = np.full((n, 2), 40, np.float32)
+    elif layout == "grid_edges":
+        xy = (rng.integers(0, 40, (n, 2)) * 64).astype(np.float32)
+        wh = np.full((n, 2), 64, np.float32)
+    else:
+        xy = np.stack([rng.uniform(0, 2800, n), rng.uniform(0, 1580, n)], 1).astype(np.float32)
+        wh = rng.uniform(8, 60, (n, 2)).astype(np.float32)
+        dup = rng.random(n) < 0.5                     # jittered duplicates of the previous box
+        xy[1:][dup[1:]] = xy[:-1][dup[1:]] + rng.uniform(-4, 4, (int(dup[1:].sum()), 2)).astype(np.float32)
+    rows["x1"], rows["y1"] = xy[:, 0], xy[:, 1]
+    rows["x2"], rows["y2"] = xy[:, 0] + wh[:, 0], xy[:, 1] + wh[:, 1]
+    if layout == "giant":
+        rows[n // 2] = (0, 0, 2880, 1620, 0.7, 1)
+    rows["score"] = rng.choice(np.array([0.3, 0.5, 0.5, 0.9, 0.7], np.float32), n)
+    rows["cls"] = rng.integers(0, 2, n)
+    win = np.array([[0, 0, 0, 3840, 2160, 0, 0]], np.int32)
+    _nms_compare(G, rows, [0, n], win, [0, 1], [(2880, 1620)], 3840, 2160, 0.25, iou)
