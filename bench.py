@@ -607,7 +607,7 @@ def run_b200(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "host_enqueue_ms_per_step": host_enqueue_ms / args.steps,
-            "gpu_launches": args.steps * (mp.launches_per_call(0) + int(R * ((C + 1) // 2) > 1024) +
+            "gpu_launches": args.steps * (mp.launches_per_call(0) + int(R * ((C + 1) // 2) > 960) +
                                           mp.launches_per_call(1) * (2 if nv12 else 1) + mp.launches_per_call(2)),
             "proxy_input": proxy,
             "counters": dataclasses.asdict(glob),

@@ -107,8 +107,8 @@ size_t mp_plan_workspace_size(const mp_plan_params* p, int32_t F);
  *  d_status      device int32: set to MP_ERR_CAPACITY if total > max_windows.
  *  Execution: one CTA per frame; frames with <= 256 horizontal runs of
  *  positive cells are planned in shared memory by a 128-thread tier, others by
- *  a persistent 128-thread tier whose CTAs hold up to 1024 runs in shared
- *  memory (~36 KB, so they fit beside a persistent gather CTA on the same SM);
+ *  a persistent 128-thread tier whose CTAs hold up to 960 runs in shared
+ *  memory (~33 KB: three fit beside a persistent gather CTA on the same SM);
  *  frames with more runs (up to R*ceil(C/2)) are planned by a third tier
  *  whose run/component arrays live in a per-CTA global scratch slot in d_ws
  *  (same arithmetic).
@@ -454,7 +454,7 @@ const char* mp_status_string(mp_status st);
  * by bench.py to count launches): which = 0 plan, 1 gather, 2 remap_nms,
  * 3 proxy_sweep, 4 window_set_cost, 5 hungarian, 6 track_resample,
  * 7 dbscan, 8 cluster_centers, 9 refine_tracks.  The plan adds one launch
- * (plan_huge_kernel) for grids with R*ceil(C/2) > 1024 possible runs. */
+ * (plan_huge_kernel) for grids with R*ceil(C/2) > 960 possible runs. */
 int32_t mp_launches_per_call(int32_t which);
 
 #ifdef __cplusplus

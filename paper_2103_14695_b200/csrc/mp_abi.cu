@@ -14,7 +14,7 @@ extern "C" const char* mp_status_string(mp_status st) {
 
 // Kernel launches per call (for bench.py's gpu_launches count):
 //   plan: memset (not a kernel) + plan_fast + plan_full + plan_scan + plan_scatter
-//         (+ plan_huge when R*ceil(C/2) > 1024, not counted here)
+//         (+ plan_huge when R*ceil(C/2) > 960, not counted here)
 //   gather: gather_prep + gather_kernel
 //   remap_nms: memset (not a kernel) + tiny + small + large + scan + scatter
 //   proxy_sweep: memset (not a kernel) + proxy_sweep_kernel

@@ -1017,6 +1017,7 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
   int* ws_cnt = (int*)(ws + L.cnt_off);
   int* ws_list = (int*)(ws + L.list_off);
   int2* ws_tap = (int2*)(ws + L.tap_off);
+  MP_CUDA_TRY(prefer_max_shared((const void*)gather_prep_kernel));
   MP_CUDA_TRY(cudaMemsetAsync(ws_cnt, 0, (kMaxClasses + 1) * sizeof(int), s));   // class counts + tile counter
   gather_prep_kernel<<<256, kPrepThreads, 0, s>>>(A, d_windows, d_frame_off, ws_cnt, ws_list, ws_tap, n_taps, d_status);
   MP_CUDA_TRY(cudaGetLastError());
@@ -1073,6 +1074,7 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
     for (int i = 0; i < occ_n; i++)
       if (occ_cache[i].fn == (const void*)kern && occ_cache[i].dev == dev && occ_cache[i].smem == smem)
         per_sm = occ_cache[i].per_sm;
+    MP_CUDA_TRY(prefer_max_shared((const void*)kern));
     if (dev < 0 || dev >= 64 || attr_max[dev][inst] < smem) {
       MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       if (dev >= 0 && dev < 64) attr_max[dev][inst] = smem;

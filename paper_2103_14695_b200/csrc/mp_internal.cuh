@@ -6,11 +6,14 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <mutex>
+
 #include "../../include/mp.h"
 
 namespace mpk {
 
 constexpr int kMaxClasses = 16;
+constexpr int kScanThreads = 256;   // single-CTA CSR scans of the plan / NMS
 
 // ----------------------------------------------------------------- status
 __device__ __forceinline__ void set_status(int32_t* d_status, int32_t code) {
@@ -205,3 +208,32 @@ __host__ __device__ __forceinline__ int64_t ceil_div64(int64_t a, int64_t b) { r
       return MP_ERR_CUDA;                                  \
     }                                                      \
   } while (0)
+
+namespace mpk {
+// Every kernel of the hot path asks for the maximum shared-memory carveout
+// (228 KB shared, the rest L1).  The carveout of an SM is fixed while CTAs are
+// resident on it and defaults to the smallest one that fits the first kernel
+// there: a persistent gather CTA of ~122 KB would leave the SM at the 132-KB
+// carveout, with no room for the plan / remap-NMS CTAs of the neighbouring
+// batches, which then queue until the gather ends.  Set once per (kernel,
+// device).
+inline cudaError_t prefer_max_shared(const void* fn) {
+  static std::mutex mu;
+  static const void* seen_fn[128];
+  static int seen_dev[128];
+  static int n = 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < n; i++)
+    if (seen_fn[i] == fn && seen_dev[i] == dev) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess && n < 128) {
+    seen_fn[n] = fn;
+    seen_dev[n] = dev;
+    n++;
+  }
+  return e;
+}
+}  // namespace mpk

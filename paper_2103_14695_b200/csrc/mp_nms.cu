@@ -152,6 +152,7 @@ __device__ __forceinline__ int window_of(const int* __restrict__ off, int lo, in
 // Returns the kept count, or -1 if the adjacency does not fit (the caller
 // then runs a dense path).
 constexpr int kGridMaxCells = 1024;
+constexpr int kRankSortMax = 256;   // candidates up to which nms_frame rank-sorts its keys
 constexpr int kGridMin = 96;   // candidates above which the grid path runs (below: the bitmask)
 
 __device__ int nms_grid(const NmsArgs& A, const NmsSmem& S, int n) {
@@ -327,26 +328,40 @@ __device__ void nms_frame(const NmsArgs& A, int f, int b_lo, int b_hi, int w_lo,
     __syncthreads();
   }
   // ---- sort keys ascending = (score desc, candidate index asc)
-  const int P = pow2_at_least(n < 1 ? 1 : n);
-  for (int p = n + tid; p < P; p += blockDim.x) S.key[p] = ~0ull;
-  __syncthreads();
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = tid; t < (P >> 1); t += blockDim.x) {
-        const int i = 2 * j * (t / j) + (t % j);
-        const int l = i + j;
-        const bool up = (i & k) == 0;
-        const unsigned long long a = S.key[i], c = S.key[l];
-        if ((a > c) == up) {
-          S.key[i] = c;
-          S.key[l] = a;
-        }
-      }
-      __syncthreads();
+  if (n <= kRankSortMax) {
+    // rank sort (the keys are unique): one barrier instead of the bitonic
+    // network's log^2 barriers — beside a persistent gather every barrier
+    // phase is slow, and c3's 100-150-candidate frames would spend most of
+    // their time in the network's ~36 phases
+    for (int p = tid; p < n; p += blockDim.x) {
+      const unsigned long long k = S.key[p];
+      int r = 0;
+      for (int q = 0; q < n; q++) r += S.key[q] < k ? 1 : 0;
+      S.order[r] = p;
     }
+    __syncthreads();
+  } else {
+    const int P = pow2_at_least(n < 1 ? 1 : n);
+    for (int p = n + tid; p < P; p += blockDim.x) S.key[p] = ~0ull;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int t = tid; t < (P >> 1); t += blockDim.x) {
+          const int i = 2 * j * (t / j) + (t % j);
+          const int l = i + j;
+          const bool up = (i & k) == 0;
+          const unsigned long long a = S.key[i], c = S.key[l];
+          if ((a > c) == up) {
+            S.key[i] = c;
+            S.key[l] = a;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int p = tid; p < n; p += blockDim.x) S.order[p] = (int)(S.key[p] & 0xffffffffu);
+    __syncthreads();
   }
-  for (int p = tid; p < n; p += blockDim.x) S.order[p] = (int)(S.key[p] & 0xffffffffu);
-  __syncthreads();
   // physically permute the candidates into the sorted order (one array at a
   // time through the now free key region, 16 B per candidate) so the O(n^2)
   // IoU loops read consecutive entries instead of order[]-scattered ones;
@@ -836,7 +851,9 @@ __global__ void __launch_bounds__(kLargeThreads) nms_large_kernel(NmsArgs A, con
   }
 }
 
-__global__ void __launch_bounds__(1024) nms_scan_kernel(int F, const int* __restrict__ ws_kept,
+// 256 threads (not 1024): a 1024-thread CTA needs ~32 K registers, more than a
+// persistent gather CTA leaves of an SM, and would wait for the gather to end.
+__global__ void __launch_bounds__(kScanThreads) nms_scan_kernel(int F, const int* __restrict__ ws_kept,
                                                         int* __restrict__ out_frame_off, int max_out,
                                                         int* __restrict__ d_status) {
   __shared__ int tmp[40];
@@ -956,6 +973,10 @@ extern "C" mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_bo
   cudaStream_t s = (cudaStream_t)stream;
   if (F > 0) {
     MP_CUDA_TRY(cudaMemsetAsync(lcnt, 0, 2 * sizeof(int), s));
+    for (const void* k : {(const void*)nms_tiny_kernel, (const void*)nms_small_kernel,
+                          (const void*)nms_large_kernel, (const void*)nms_scan_kernel,
+                          (const void*)nms_scatter_kernel})
+      MP_CUDA_TRY(prefer_max_shared(k));
     const size_t sm_small = nms_smem_bytes(kSmallCap, kSmallMaskCap, nullptr, nullptr);
     const size_t sm_large = nms_smem_bytes(kLargeCap, kLargeMaskCap, nullptr, nullptr);
     MP_CUDA_TRY(cudaFuncSetAttribute(nms_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_small));
@@ -974,7 +995,7 @@ extern "C" mp_status mp_remap_nms(const mp_box* d_boxes, const int32_t* d_win_bo
                                                           ws_box, ws_src, ws_kept, lcnt, llist, g, d_status);
     MP_CUDA_TRY(cudaGetLastError());
   }
-  nms_scan_kernel<<<1, 1024, 0, s>>>(F, ws_kept, d_out_frame_off, max_out, d_status);
+  nms_scan_kernel<<<1, kScanThreads, 0, s>>>(F, ws_kept, d_out_frame_off, max_out, d_status);
   MP_CUDA_TRY(cudaGetLastError());
   if (F > 0) {
     nms_scatter_kernel<<<(F + 7) / 8, 256, 0, s>>>(F, d_frame_off, d_win_box_off, ws_box, ws_src, ws_kept,

@@ -118,22 +118,25 @@ __host__ __device__ inline size_t plan_smem_bytes(int R, int words, int maxc, Pl
 constexpr int kPlanThreads = 128;      // full-capacity tier (128 threads: two CTAs fit beside a gather CTA)
 constexpr int kFastThreads = 128;      // fast tier: frames with <= kFastCap runs
 constexpr int kFastCap = 256;
-// full tier: runs held in shared memory (~33 KB at 1024 runs, so a CTA fits
-// in what the gather's ring leaves of an SM); beyond -> global scratch.
-// c4 (4K, 68 x 120 cells) frames have 756-888 runs.
-constexpr int kMidCap = 1024;
+// full tier: runs held in shared memory (~32 KB at 960 runs + ~1.5 KB
+// static: three CTAs fit in the ~108 KB a c4 gather CTA leaves of an SM, so
+// all 300 frames of a c4 batch plan in one wave beside the gather); beyond
+// -> the huge tier (global scratch).  c4 (4K, 68 x 120 cells) frames have
+// 756-888 runs.
+constexpr int kMidCap = 960;
 constexpr int kFullGrid = 4;        // plan_full CTAs per SM (one frame each at c4: 300 frames)
 constexpr int kHugeGrid = 1;        // plan_huge CTAs per SM (each owns a global scratch slot)
 
 constexpr int kCoopMergeMin = 96;   // components above which the whole CTA runs the merge
 
-// Block-wide minimum of a 64-bit key; `red` = 2 x 32 shared slots used
-// alternately (par) so consecutive calls need one barrier each.
+// Block-wide minimum of a 64-bit key; `red` = 2 x kRedWarps shared slots
+// used alternately (par) so consecutive calls need one barrier each.
+constexpr int kRedWarps = 8;   // every planner CTA has <= 256 threads
 __device__ __forceinline__ unsigned long long block_min_u64(unsigned long long v, unsigned long long* red,
                                                             int& par) {
   v = warp_min_u64(v);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  unsigned long long* r = red + 32 * par;
+  unsigned long long* r = red + kRedWarps * par;
   if (lane == 0) r[wid] = v;
   __syncthreads();
   unsigned long long m = ~0ull;
@@ -178,10 +181,14 @@ __device__ unsigned long long g_plan_prof[4];
 #define MP_PROF_ADD(k, d)
 #endif
 
+// FW: words of initial-fit ballots, one per 32 list entries (len <= 32 FW):
+// the shared-memory tiers (<= kMidCap + 1 entries) keep their static shared
+// memory small so three full-tier CTAs fit beside a gather CTA.
+template <int FW>
 __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n, int cap) {
-  __shared__ unsigned long long red[64];
+  __shared__ unsigned long long red[2 * kRedWarps];
   __shared__ int pub[8];
-  __shared__ uint32_t fitm[256];   // initial-fit ballots, one word per 32 entries (len <= 8192)
+  __shared__ uint32_t fitm[FW];
   __shared__ int absl[kAbsList];
   int par = 0;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, BS = blockDim.x, NW = BS >> 5;
@@ -381,7 +388,7 @@ __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n, int cap) 
 // `gbig` (capacity maxc, L2-resident) and only the bit rows and scan scratch
 // in shared memory; a separate instantiation, so the shared-memory tiers keep
 // plain LDS/STS accesses.
-template <bool GB = false>
+template <bool GB = false, bool SMALL = false>
 __device__ __forceinline__ bool plan_frame(const PlanArgs& P, int f, int cap, const float* __restrict__ scores,
                                            uint32_t* __restrict__ mask_out, int4* __restrict__ ws_win,
                                            int* __restrict__ ws_count, int* __restrict__ ws_cls,
@@ -537,7 +544,7 @@ __device__ __forceinline__ bool plan_frame(const PlanArgs& P, int f, int cap, co
   if (ncomp > kCoopMergeMin) {
     // many components: the CTA runs the greedy (same order rules) with block-wide
     // arg-mins; warp 0 then only places the final clusters
-    n = coop_merge(P, S, ncomp, ext_cap);
+    n = SMALL ? coop_merge<(kMidCap + 1 + 31) / 32>(P, S, ncomp, ext_cap) : coop_merge<256>(P, S, ncomp, ext_cap);
     again = false;
   }
   if (wid != 0) return true;
@@ -691,7 +698,8 @@ __global__ void __launch_bounds__(kFastThreads) plan_fast_kernel(PlanArgs P, con
                                                                   int4* __restrict__ ws_win, int* __restrict__ ws_count,
                                                                   int* __restrict__ ws_cls, int* __restrict__ q_cnt,
                                                                   int* __restrict__ q_list) {
-  plan_frame(P, blockIdx.x, min(kFastCap, P.maxc), scores, mask_out, ws_win, ws_count, ws_cls, q_cnt, q_list);
+  plan_frame<false, true>(P, blockIdx.x, min(kFastCap, P.maxc), scores, mask_out, ws_win, ws_count, ws_cls, q_cnt,
+                          q_list);
 }
 
 // Persistent over the frames the fast tier queued (dense / checkerboard grids).
@@ -707,7 +715,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_full_kernel(PlanArgs P, con
                                                                  int* __restrict__ q2_cnt, int* __restrict__ q2_list) {
   const int nq = *q_cnt;
   for (int qi = blockIdx.x; qi < nq; qi += gridDim.x) {
-    plan_frame(P, q_list[qi], cap, scores, mask_out, ws_win, ws_count, ws_cls, q2_cnt, q2_list);
+    plan_frame<false, true>(P, q_list[qi], cap, scores, mask_out, ws_win, ws_count, ws_cls, q2_cnt, q2_list);
     __syncthreads();
   }
 }
@@ -730,7 +738,9 @@ __global__ void __launch_bounds__(kPlanThreads) plan_huge_kernel(PlanArgs P, con
   }
 }
 
-__global__ void __launch_bounds__(1024) plan_scan_kernel(int F, int k, int* __restrict__ ws_count,
+// 256 threads (not 1024): a 1024-thread CTA needs ~32 K registers, more than a
+// persistent gather CTA leaves of an SM, and would wait for the gather to end.
+__global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(int F, int k, int* __restrict__ ws_count,
                                                          int* __restrict__ ws_cls, int* __restrict__ frame_off,
                                                          int* __restrict__ class_count, int max_windows,
                                                          int* __restrict__ d_status) {
@@ -1071,6 +1081,10 @@ extern "C" mp_status mp_plan_windows(const mp_plan_params* p, const float* d_sco
     if (smem > 227 * 1024) return MP_ERR_UNSUPPORTED;
     const size_t smem_fast = plan_smem_bytes(A.R, A.words, kFastCap < A.maxc ? kFastCap : A.maxc, nullptr, nullptr);
     MP_CUDA_TRY(cudaMemsetAsync(q_cnt, 0, 2 * sizeof(int), s));
+    for (const void* k : {(const void*)plan_fast_kernel, (const void*)plan_full_kernel,
+                          (const void*)plan_huge_kernel, (const void*)plan_scan_kernel,
+                          (const void*)plan_scatter_kernel})
+      MP_CUDA_TRY(prefer_max_shared(k));
     MP_CUDA_TRY(cudaFuncSetAttribute(plan_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_fast));
     MP_CUDA_TRY(cudaFuncSetAttribute(plan_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1088,7 +1102,7 @@ extern "C" mp_status mp_plan_windows(const mp_plan_params* p, const float* d_sco
       MP_CUDA_TRY(cudaGetLastError());
     }
   }
-  plan_scan_kernel<<<1, 1024, 0, s>>>(F, A.k, ws_count, ws_cls, d_frame_off, d_class_count, max_windows,
+  plan_scan_kernel<<<1, kScanThreads, 0, s>>>(F, A.k, ws_count, ws_cls, d_frame_off, d_class_count, max_windows,
                                       d_status);
   MP_CUDA_TRY(cudaGetLastError());
   if (F > 0) {

@@ -136,13 +136,13 @@ def test_plan_unsupported_grid(G):
 
 def test_plan_largest_grid_global_scratch(G):
     """128 x 128 cells (the R*C limit): frames with more than the full tier's
-    1024 shared-memory runs plan over the CTA's global scratch slot (up to
+    960 shared-memory runs are planned by the huge tier over a global scratch slot (up to
     R*ceil(C/2) = 8192 runs) with the same results as the oracle."""
     W = H = 4096
     sizes, cost = [(256, 256), (1024, 1024), (4096, 4096)], [80, 1040, 10 ** 9]   # full frame never pays
     rng = np.random.default_rng(5)
     grids = [np.zeros((128, 128), np.float32)]
-    for n_blobs in (150, 400, 700):           # narrow blobs: 743 / 1623 / ~2700 runs (> 1024: global scratch)
+    for n_blobs in (150, 400, 700):           # narrow blobs: 743 / 1623 / ~2700 runs (> 960: global scratch)
         g = np.zeros((128, 128), np.float32)
         for _ in range(n_blobs):
             r, c = rng.integers(0, 120), rng.integers(0, 126)
