@@ -230,36 +230,56 @@ __device__ int nms_grid(const NmsArgs& A, const NmsSmem& S, int n) {
   }
   __syncthreads();
   const float thr = A.iou_thr;
-  // pass 0: count each candidate's suppressees; pass 1: write them
-  for (int pass = 0; pass < 2; pass++) {
-    for (int i = tid; i < n; i += BS) {
-      const float4 bi = S.bx[i];
-      const int ci = S.cls[i];
-      const int cx = cell_x(bi.x), cy = cell_y(bi.y);
-      int d = 0, w = pass ? off[i] : 0;
-      for (int yy = max(cy - 1, 0); yy <= min(cy + 1, gy - 1); yy++) {
-        for (int xx = max(cx - 1, 0); xx <= min(cx + 1, gx - 1); xx++) {
-          const int c = yy * gx + xx;
-          for (int k = (c ? cend[c - 1] : 0); k < cend[c]; k++) {
-            const int j = cellm[k];
-            if (j > i && S.cls[j] == ci && iou_rn(bi, S.bx[j]) > thr) {
-              if (pass) adj[w + d] = (unsigned short)j;
-              d++;
-            }
-          }
+  // each candidate i scans the three rows of its 3x3 neighbourhood (the
+  // cells of a row are contiguous in cellm) in a fixed order; test k of the
+  // scan records its outcome in bit k of `hits` (k < 64), so after
+  // reserving popc(hits) adjacency slots with one shared atomic the scan is
+  // replayed writing the hits without recomputing any IoU.  The exact
+  // intersection test first skips the (most) pairs that cannot overlap:
+  // iou_rn > thr >= 0 needs min(x2) > max(x1) and min(y2) > max(y1).
+  int* nadj = S.tmp + 48;
+  if (tid == 0) *nadj = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += BS) {
+    const float4 bi = S.bx[i];
+    const int ci = S.cls[i];
+    const int cx = cell_x(bi.x), cy = cell_y(bi.y);
+    const int x0 = max(cx - 1, 0), x1 = min(cx + 1, gx - 1);
+    const int y0 = max(cy - 1, 0), y1 = min(cy + 1, gy - 1);
+    auto test = [&](int j) -> bool {
+      if (j <= i || S.cls[j] != ci) return false;
+      const float4 bj = S.bx[j];
+      if (!(fminf(bi.z, bj.z) > fmaxf(bi.x, bj.x)) || !(fminf(bi.w, bj.w) > fmaxf(bi.y, bj.y))) return false;
+      return iou_rn(bi, bj) > thr;
+    };
+    unsigned long long hits = 0;
+    int d = 0, k = 0;
+    for (int yy = y0; yy <= y1; yy++) {
+      const int c0 = yy * gx + x0, c1 = yy * gx + x1;
+      for (int e = (c0 ? cend[c0 - 1] : 0); e < cend[c1]; e++, k++) {
+        if (test(cellm[e])) {
+          if (k < 64) hits |= 1ull << k;
+          d++;
         }
       }
-      if (!pass) off[i] = d;
     }
-    __syncthreads();
-    if (!pass) {
-      const int total = block_excl_scan_smem(off, n, S.tmp);
-      if (total > cap_adj) return -1;   // (uniform)
-      for (int p = tid; p < n; p += BS) supp[p] = 0;
-      if (tid == 0) off[n] = total;
-      __syncthreads();
+    const int base = d ? atomicAdd(nadj, d) : 0;
+    off[i] = (base << 16) | d;   // (base, degree); both < 65536
+    if (base + d <= cap_adj && d) {
+      int w = base;
+      k = 0;
+      for (int yy = y0; yy <= y1; yy++) {
+        const int c0 = yy * gx + x0, c1 = yy * gx + x1;
+        for (int e = (c0 ? cend[c0 - 1] : 0); e < cend[c1]; e++, k++) {
+          const int j = cellm[e];
+          if (k < 64 ? ((hits >> k) & 1ull) != 0 : test(j)) adj[w++] = (unsigned short)j;
+        }
+      }
     }
   }
+  for (int p = tid; p < n; p += BS) supp[p] = 0;
+  __syncthreads();
+  if (*nadj > cap_adj) return -1;   // (uniform) the adjacency does not fit: dense path
   // greedy in score order (warp 0): per chunk of 32 candidates, repeatedly
   // take the first candidate neither suppressed nor already kept, keep it and
   // flag its suppressees (later chunk members included, re-read next round)
@@ -276,7 +296,8 @@ __device__ int nms_grid(const NmsArgs& A, const NmsSmem& S, int n) {
         taken |= 1u << b;
         if (lane == 0) S.keep[nk] = k;
         nk++;
-        for (int e = off[k] + lane; e < off[k + 1]; e += 32) supp[adj[e]] = 1;
+        const int ob = off[k] >> 16, od = off[k] & 0xffff;
+        for (int e = lane; e < od; e += 32) supp[adj[ob + e]] = 1;
         __syncwarp();
       }
     }
