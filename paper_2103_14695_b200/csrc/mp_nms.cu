@@ -264,7 +264,7 @@ __device__ int nms_grid(const NmsArgs& A, const NmsSmem& S, int n) {
       }
     }
     const int base = d ? atomicAdd(nadj, d) : 0;
-    off[i] = (base << 16) | d;   // (base, degree); both < 65536
+    off[i] = (int)(((unsigned int)base << 16) | (unsigned int)d);   // (base, degree), both < 65536 when it fits
     if (base + d <= cap_adj && d) {
       int w = base;
       k = 0;
@@ -290,13 +290,14 @@ __device__ int nms_grid(const NmsArgs& A, const NmsSmem& S, int n) {
       uint32_t taken = 0;
       while (true) {
         const uint32_t free = __ballot_sync(0xffffffffu, i < n && !supp[i]) & ~taken;
+        __syncwarp();   // every lane's supp read is ordered before this round's writes
         if (!free) break;
         const int b = __ffs(free) - 1;
         const int k = b0 + b;
         taken |= 1u << b;
         if (lane == 0) S.keep[nk] = k;
         nk++;
-        const int ob = off[k] >> 16, od = off[k] & 0xffff;
+        const int ob = (int)((unsigned int)off[k] >> 16), od = off[k] & 0xffff;
         for (int e = lane; e < od; e += 32) supp[adj[ob + e]] = 1;
         __syncwarp();
       }
