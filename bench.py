@@ -542,8 +542,12 @@ def run_b200(args):
     if not args.no_e2e:
         e2e = run_e2e(cfg, clip, scene, scores_np, boxes, wbo, fmt, dev, args, ab)
     proxy = None
+    step_bytes = ab["step"]
     if nv12:
         pb, pbs = (x * F for x in proxy_input_bytes(cfg))
+        # the proxy-input downscale is part of the NV12 step (it shares HBM
+        # with the crop gather; both persistent kernels alternate on the SMs)
+        step_bytes += int(pb)
         proxy = {"dims": list(cfg.proxy_dims), "kernel": "gather_kernel<.., NV12> row-sparse (tile::gather4)",
                  "launch_ms": proxy_ms, "alg_bytes_per_launch": int(pb),
                  "alg_bytes_per_launch_samples": int(pbs),
@@ -601,8 +605,9 @@ def run_b200(args):
                          "nominal_source": "B200 HBM3e 7.7 TB/s (HGX datasheet, B200_PROFILING.md)",
                          "alg_bytes_per_launch": ab["gather_union"],
                          "alg_bytes_per_launch_window_sum": ab["gather_sum"],
-                         "launch_ms": gather_ms, "step_alg_bytes": ab["step"],
-                         "step_GBps": ab["step"] / (tmax_ms / args.steps * 1e-3) / 1e9,
+                         "launch_ms": gather_ms, "step_alg_bytes": step_bytes,
+                         "step_GBps": step_bytes / (tmax_ms / args.steps * 1e-3) / 1e9,
+                         "step_frac": step_bytes / (tmax_ms / args.steps * 1e-3) / 1e9 / peak,
                          "gather_share_of_step": gather_ms / (tmax_ms / args.steps)},
             "cpu_baseline": cpu,
             "e2e": e2e,

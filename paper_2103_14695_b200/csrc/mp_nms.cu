@@ -122,6 +122,16 @@ __device__ __forceinline__ float iou_rn(const float4 a, const float4 b) {
   return __fdiv_rn(inter, uni);
 }
 
+// The suppression predicate of every NMS path: iou_rn(a, b) > thr.  For
+// thr >= 0 it needs a positive-area intersection (IoU > 0), so the exact
+// test min(x2) > max(x1) && min(y2) > max(y1) rejects the (most) disjoint
+// pairs before the areas and the division; thr < 0 suppresses every pair
+// (IoU >= 0 > thr) and takes the plain predicate.
+__device__ __forceinline__ bool suppresses(const float4 a, const float4 b, float thr) {
+  if (thr >= 0.0f && (!(fminf(a.z, b.z) > fmaxf(a.x, b.x)) || !(fminf(a.w, b.w) > fmaxf(a.y, b.y)))) return false;
+  return iou_rn(a, b) > thr;
+}
+
 __device__ __forceinline__ unsigned int score_desc_bits(float s) {
   if (s == 0.0f) s = 0.0f;   // -0.0 -> +0.0 (equal in fp32 value order)
   const unsigned int u = __float_as_uint(s);
@@ -248,9 +258,7 @@ __device__ int nms_grid(const NmsArgs& A, const NmsSmem& S, int n) {
     const int y0 = max(cy - 1, 0), y1 = min(cy + 1, gy - 1);
     auto test = [&](int j) -> bool {
       if (j <= i || S.cls[j] != ci) return false;
-      const float4 bj = S.bx[j];
-      if (!(fminf(bi.z, bj.z) > fmaxf(bi.x, bj.x)) || !(fminf(bi.w, bj.w) > fmaxf(bi.y, bj.y))) return false;
-      return iou_rn(bi, bj) > thr;
+      return suppresses(bi, S.bx[j], thr);   // (thr >= 0 here)
     };
     unsigned long long hits = 0;
     int d = 0, k = 0;
@@ -428,7 +436,7 @@ __device__ void nms_frame(const NmsArgs& A, int f, int b_lo, int b_hi, int w_lo,
       const int j0 = max(i + 1, wd * 64), j1 = min(n, wd * 64 + 64);
       for (int j = j0; j < j1; j++) {
         const int qj = S.order[j];
-        if (S.cls[qj] == ci && iou_rn(bi, S.bx[qj]) > A.iou_thr) bits |= 1ull << (j - wd * 64);
+        if (S.cls[qj] == ci && suppresses(bi, S.bx[qj], A.iou_thr)) bits |= 1ull << (j - wd * 64);
       }
       mask[(size_t)i * words + wd] = bits;
     }
@@ -468,7 +476,7 @@ __device__ void nms_frame(const NmsArgs& A, int f, int b_lo, int b_hi, int w_lo,
         unsigned long long bits = 0;
         for (int j = i + 1; j < b1; j++) {
           const int qj = S.order[j];
-          if (S.cls[qj] == ci && iou_rn(bi, S.bx[qj]) > A.iou_thr) bits |= 1ull << (j - b0);
+          if (S.cls[qj] == ci && suppresses(bi, S.bx[qj], A.iou_thr)) bits |= 1ull << (j - b0);
         }
         S.bmask[i - b0] = bits;
       }
@@ -496,7 +504,7 @@ __device__ void nms_frame(const NmsArgs& A, int f, int b_lo, int b_hi, int w_lo,
         const int cj = S.cls[qj];
         for (int r = 0; r < nb; r++) {
           const int qk = S.order[S.bkeep[r]];
-          if (S.cls[qk] == cj && iou_rn(S.bx[qk], bj) > A.iou_thr) {
+          if (S.cls[qk] == cj && suppresses(S.bx[qk], bj, A.iou_thr)) {
             S.supp[j] = 1;
             break;
           }
@@ -628,7 +636,7 @@ __device__ void nms_frame_global(const NmsArgs& A, int f, int b_lo, int b_hi, in
       unsigned long long bits = 0;
       for (int j = i + 1; j < b1; j++) {
         const int qj = (int)(ka[j] & 0xffffffffu);
-        if (gcls[qj] == ci && iou_rn(bi, gbx[qj]) > A.iou_thr) bits |= 1ull << (j - b0);
+        if (gcls[qj] == ci && suppresses(bi, gbx[qj], A.iou_thr)) bits |= 1ull << (j - b0);
       }
       S.bmask[i - b0] = bits;
     }
@@ -656,7 +664,7 @@ __device__ void nms_frame_global(const NmsArgs& A, int f, int b_lo, int b_hi, in
       const int cj = gcls[qj];
       for (int r = 0; r < nb; r++) {
         const int qk = (int)(ka[S.bkeep[r]] & 0xffffffffu);
-        if (gcls[qk] == cj && iou_rn(gbx[qk], bj) > A.iou_thr) {
+        if (gcls[qk] == cj && suppresses(gbx[qk], bj, A.iou_thr)) {
           supp[j] = 1;
           break;
         }
@@ -787,7 +795,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) nms_tiny_kernel(NmsArgs A, co
       unsigned long long bits = 0;
       for (int j = i + 1; j < n; j++) {
         const int qj = S.order[j];
-        if (S.cls[qj] == ci && iou_rn(bi, S.bx[qj]) > A.iou_thr) bits |= 1ull << j;
+        if (S.cls[qj] == ci && suppresses(bi, S.bx[qj], A.iou_thr)) bits |= 1ull << j;
       }
       S.mask[i] = bits;
     }

@@ -216,3 +216,60 @@ def test_plan_overflow_then_gather_and_merge(G, cap_frac):
             assert np.array_equal(src[kfo[f]:kfo[f + 1]], r["src"][a:b]), f
         elif ref["frame_off"][f] >= cap:
             assert kfo[f + 1] == kfo[f], f                              # its windows do not exist
+
+
+@pytest.mark.parametrize("replays", [1, 3])
+def test_runner_capture_steps_whole_step_graphs(G, replays):
+    """PipelinedRunner.capture_steps (the bench's mode for small batches):
+    three whole pipelined steps (plan / gather / merge of three clips on the
+    runner's streams) captured as ONE CUDA graph and replayed; after the
+    last replay buffer set u holds batch u, and every set equals the oracle
+    for its clip.  The gather events recorded as graph nodes (external
+    events) time every replayed gather."""
+    import paper_2103_14695_b200 as mp
+    cfg = S.CONFIGS["c1_540p"]
+    F = cfg.frames
+    clips = [_clip_inputs(cfg, c, F) for c in (21, 22, 23)]
+    n_max = max(len(c["ref"]["windows"]) for c in clips)
+    caps = [max(int(c["ref"]["class_count"][q]) for c in clips) for q in range(len(cfg.sizes))]
+    nb = max(max(len(c["boxes"]) for c in clips), 1)
+    pipes = []
+    for _ in range(3):
+        p = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
+                              cfg.iou_thr, device=G.DEV)
+        p.reserve(F, n_max + 4, caps=caps, max_boxes=nb)
+        pipes.append(p)
+    runner = mp.PipelinedRunner(pipes, device=G.DEV)
+    batches = []
+    for c in clips:
+        b = np.zeros((nb, 6), np.float32)
+        if len(c["boxes"]):
+            b[:len(c["boxes"])] = c["boxes"].view(np.float32).reshape(-1, 6)
+        w = np.full(n_max + 5, c["wbo"][-1], np.int32)
+        w[:len(c["wbo"])] = c["wbo"]
+        batches.append((torch.from_numpy(c["scores"]).to(G.DEV), torch.from_numpy(c["frames"]).to(G.DEV),
+                        torch.from_numpy(b).to(G.DEV), torch.from_numpy(w).to(G.DEV)))
+    evs = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+           for _ in batches]
+    runner.capture_steps(batches, evs)
+    for p in pipes:                                  # capture only records: nothing ran yet
+        p.status.zero_()
+        p.nms_frame_off.fill_(-3)
+    for _ in range(replays):
+        runner.replay_steps()
+    torch.cuda.synchronize()
+    assert all(a.elapsed_time(b) > 0.0 for a, b in evs)
+    rng = np.random.default_rng(7)
+    for u, c in enumerate(clips):
+        p = pipes[u]
+        s = dict(frame_off=p.frame_off.cpu().numpy(), windows=p.windows.cpu().numpy(),
+                 nms_frame_off=p.nms_frame_off.cpu().numpy(), nms_src=p.nms_src.cpu().numpy(),
+                 nms_out=p.nms_out.cpu().numpy(), outs=[o.cpu().numpy() for o in p.outs],
+                 status=int(p.status.item()))
+        _check_batch(cfg, c, s, rng)
+    # the runner is reusable eagerly after a capture
+    k = runner.enqueue(*batches[0][:2])
+    runner.merge(k, batches[0][2], batches[0][3])
+    runner.wait_all()
+    torch.cuda.synchronize()
+    assert int(pipes[k].status.item()) == 0
