@@ -30,7 +30,11 @@
  *    would fall outside the buffers.
  *  - Determinism: outputs are a pure function of the inputs, independent of
  *    launch configuration, stream, or how frames are sharded across GPUs.
- *    The library is re-entrant and keeps no global mutable state.
+ *    The library is re-entrant and keeps no global data state; the only
+ *    process-wide state is a cache of immutable driver facts (the tensor-map
+ *    encoder entry point, per-device SM counts, per-kernel attribute /
+ *    occupancy results, the max-shared carveout already set), filled on first
+ *    use under a mutex, so steady-state calls issue only their launches.
  */
 #ifndef MP_H_
 #define MP_H_
@@ -112,7 +116,8 @@ size_t mp_plan_workspace_size(const mp_plan_params* p, int32_t F);
  *  frames with more runs (up to R*ceil(C/2)) are planned by a third tier
  *  whose run/component arrays live in a per-CTA global scratch slot in d_ws
  *  (same arithmetic).
- *  Limits: R*C <= 16384 cells (4K at 32 px = 8160); larger grids return
+ *  Limits: R*C <= 65536 cells (4K at 32 px = 8160, 8K = 32400); larger
+ *  grids (and grids whose bit rows alone exceed shared memory) return
  *  MP_ERR_UNSUPPORTED.
  */
 mp_status mp_plan_windows(const mp_plan_params* p, const float* d_scores, int32_t F,

@@ -124,6 +124,10 @@ constexpr int kFastCap = 256;
 // -> the huge tier (global scratch).  c4 (4K, 68 x 120 cells) frames have
 // 756-888 runs.
 constexpr int kMidCap = 960;
+// largest cell grid: the fast / full tiers keep only the bit rows and run
+// offsets of the grid in shared memory, the huge tier's per-run arrays are in
+// global scratch (R*ceil(C/2) runs), and run rows / columns are int16
+constexpr int kMaxCells = 65536;
 constexpr int kFullGrid = 4;        // plan_full CTAs per SM (one frame each at c4: 300 frames)
 constexpr int kHugeGrid = 1;        // plan_huge CTAs per SM (each owns a global scratch slot)
 
@@ -388,7 +392,11 @@ __device__ int coop_merge(const PlanArgs& P, const PlanSmem& S, int n, int cap) 
 // `gbig` (capacity maxc, L2-resident) and only the bit rows and scan scratch
 // in shared memory; a separate instantiation, so the shared-memory tiers keep
 // plain LDS/STS accesses.
-template <bool GB = false, bool SMALL = false>
+// FW: fit-ballot words of the cooperative merge (list length <= 32 FW)
+constexpr int kFwSmall = (kMidCap + 1 + 31) / 32 + 1;   // shared-memory tiers
+constexpr int kFwFull = 256;                             // sweep / window-set kernels (whole frame in smem)
+constexpr int kFwHuge = kMaxCells / 32 + 2;              // global tier: up to R*ceil(C/2) + 1 <= kMaxCells + 1 entries
+template <bool GB = false, int FW = kFwFull>
 __device__ __forceinline__ bool plan_frame(const PlanArgs& P, int f, int cap, const float* __restrict__ scores,
                                            uint32_t* __restrict__ mask_out, int4* __restrict__ ws_win,
                                            int* __restrict__ ws_count, int* __restrict__ ws_cls,
@@ -544,7 +552,7 @@ __device__ __forceinline__ bool plan_frame(const PlanArgs& P, int f, int cap, co
   if (ncomp > kCoopMergeMin) {
     // many components: the CTA runs the greedy (same order rules) with block-wide
     // arg-mins; warp 0 then only places the final clusters
-    n = SMALL ? coop_merge<(kMidCap + 1 + 31) / 32>(P, S, ncomp, ext_cap) : coop_merge<256>(P, S, ncomp, ext_cap);
+    n = coop_merge<FW>(P, S, ncomp, ext_cap);
     again = false;
   }
   if (wid != 0) return true;
@@ -698,7 +706,7 @@ __global__ void __launch_bounds__(kFastThreads) plan_fast_kernel(PlanArgs P, con
                                                                   int4* __restrict__ ws_win, int* __restrict__ ws_count,
                                                                   int* __restrict__ ws_cls, int* __restrict__ q_cnt,
                                                                   int* __restrict__ q_list) {
-  plan_frame<false, true>(P, blockIdx.x, min(kFastCap, P.maxc), scores, mask_out, ws_win, ws_count, ws_cls, q_cnt,
+  plan_frame<false, kFwSmall>(P, blockIdx.x, min(kFastCap, P.maxc), scores, mask_out, ws_win, ws_count, ws_cls, q_cnt,
                           q_list);
 }
 
@@ -715,7 +723,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_full_kernel(PlanArgs P, con
                                                                  int* __restrict__ q2_cnt, int* __restrict__ q2_list) {
   const int nq = *q_cnt;
   for (int qi = blockIdx.x; qi < nq; qi += gridDim.x) {
-    plan_frame<false, true>(P, q_list[qi], cap, scores, mask_out, ws_win, ws_count, ws_cls, q2_cnt, q2_list);
+    plan_frame<false, kFwSmall>(P, q_list[qi], cap, scores, mask_out, ws_win, ws_count, ws_cls, q2_cnt, q2_list);
     __syncthreads();
   }
 }
@@ -732,7 +740,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_huge_kernel(PlanArgs P, con
   const int nq = *q_cnt;
   unsigned char* slot = gbig + (size_t)blockIdx.x * slot_bytes;
   for (int qi = blockIdx.x; qi < nq; qi += gridDim.x) {
-    plan_frame<true>(P, q_list[qi], P.maxc, scores, mask_out, ws_win, ws_count, ws_cls, nullptr, nullptr, nullptr,
+    plan_frame<true, kFwHuge>(P, q_list[qi], P.maxc, scores, mask_out, ws_win, ws_count, ws_cls, nullptr, nullptr, nullptr,
                      slot);
     __syncthreads();
   }
@@ -981,7 +989,7 @@ static bool build_plan_args(const mp_plan_params* p, PlanArgs* A, mp_status* err
   A->k = p->k;
   A->full = full;
   A->b = p->b_proxy;
-  if ((long long)A->R * A->C > 16384) {
+  if ((long long)A->R * A->C > kMaxCells) {
     *err = MP_ERR_UNSUPPORTED;
     return false;
   }
@@ -1080,6 +1088,8 @@ extern "C" mp_status mp_plan_windows(const mp_plan_params* p, const float* d_sco
     const size_t smem = plan_smem_bytes(A.R, A.words, cap_full, nullptr, nullptr);
     if (smem > 227 * 1024) return MP_ERR_UNSUPPORTED;
     const size_t smem_fast = plan_smem_bytes(A.R, A.words, kFastCap < A.maxc ? kFastCap : A.maxc, nullptr, nullptr);
+    if (smem_fast > 227 * 1024 || plan_smem_bytes(A.R, A.words, 0, nullptr, nullptr) > 227 * 1024)
+      return MP_ERR_UNSUPPORTED;   // (the bit rows of very tall grids)
     MP_CUDA_TRY(cudaMemsetAsync(q_cnt, 0, 2 * sizeof(int), s));
     for (const void* k : {(const void*)plan_fast_kernel, (const void*)plan_full_kernel,
                           (const void*)plan_huge_kernel, (const void*)plan_scan_kernel,

@@ -128,14 +128,35 @@ def test_plan_capacity_and_zero_frames(G):
 
 def test_plan_unsupported_grid(G):
     import paper_2103_14695_b200 as mp
-    with pytest.raises(mp.MPError) as e:     # 128 x 129 cells > 16384
-        G.gpu_plan(4128, 4096, 32, 32, 0.5, [(256, 256), (4128, 4096)], [80, 16400],
-                   np.zeros((1, 128, 129), np.float32))
+    with pytest.raises(mp.MPError) as e:     # 257 x 256 cells > 65536
+        G.gpu_plan(8192, 8224, 32, 32, 0.5, [(256, 256), (8192, 8224)], [80, 16400],
+                   np.zeros((1, 257, 256), np.float32))
     assert e.value.code == mp.MP_ERR_UNSUPPORTED
 
 
+@pytest.mark.parametrize("cost_full", [10 ** 9, 5000])
+def test_plan_parity_8k_grid(G, cost_full):
+    """7680 x 4320 frames at 32-px cells (240 x 135 = 32,400 cells, above
+    round 1's 16,384-cell limit): blob frames of ~1.5 K and ~4.8 K runs and a
+    checkerboard of 16,200 single-cell components, all in the huge tier
+    (global scratch, fit ballots over up to 16,201 list entries)."""
+    W, H, R, C = 7680, 4320, 135, 240
+    sizes, cost = [(256, 256), (1024, 1024), (W, H)], [80, 1040, cost_full]
+    rng = np.random.default_rng(9)
+    grids = []
+    for n_blobs in (300, 1500):
+        g = np.zeros((R, C), np.float32)
+        for _ in range(n_blobs):
+            r, c = rng.integers(0, R - 8), rng.integers(0, C - 3)
+            g[r:r + rng.integers(3, 9), c:c + rng.integers(1, 3)] = 0.9
+        grids.append(g)
+    grids.append(((np.add.outer(np.arange(R), np.arange(C)) % 2) == 0).astype(np.float32))
+    ref, got = _plan_both(G, W, H, 32, 32, 0.5, sizes, cost, np.stack(grids))
+    _assert_plan_equal(ref, got)
+
+
 def test_plan_largest_grid_global_scratch(G):
-    """128 x 128 cells (the R*C limit): frames with more than the full tier's
+    """128 x 128 cells (round 1's R*C limit): frames with more than the full tier's
     960 shared-memory runs are planned by the huge tier over a global scratch slot (up to
     R*ceil(C/2) = 8192 runs) with the same results as the oracle."""
     W = H = 4096
