@@ -71,6 +71,7 @@ struct GatherArgs {
   int wait_mode;             // bit 0: producer sleeps on empty slots, bit 1: consumers sleep on full slots
   int rpf;                   // row-sparse: rows per frame in the 2-D row view of the frame batch
   int max_windows;           // capacity of the windows buffer: n_win = min(frame_off[F], max_windows)
+  int lam_off;               // MP_LAM_SMEM builds: byte offset of the per-warp lambda-pair scratch
   int ncol[kMaxClasses];
   int box_w[kMaxClasses], box_h[kMaxClasses];
   int w[kMaxClasses], h[kMaxClasses], ow[kMaxClasses], oh[kMaxClasses];
@@ -138,6 +139,15 @@ __device__ __forceinline__ float2 ffma2_w(float2 a, unsigned long long w, float2
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a)), "l"(w), "l"(pk2(c)));
   return upk2(r);
 }
+
+#ifdef MP_LAM_SMEM
+constexpr int kMaxNP = 4;   // column pairs per lane (NCOL <= 8)
+__device__ __forceinline__ unsigned long long lds64(unsigned int addr) {
+  unsigned long long v;
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr));
+  return v;
+}
+#endif
 
 __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {   // packed a - b (FADD2 with negated operand)
   return __fadd2_rn(a, make_float2(-b.x, -b.y));
@@ -291,12 +301,28 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
     }
     lx[p] = pk2(make_float2(__int_as_float(xa.y), __int_as_float(xb.y)));
   }
+#ifdef MP_LAM_SMEM
+  // the (lambda_A, lambda_B) pairs go to this warp's shared scratch and are
+  // re-loaded (LDS.64 into an aligned register pair) at every use, instead of
+  // being copied into an aligned pair before every FFMA2 (IMAD.MOV / MOV were
+  // 12 % of the u8 kernel's instructions)
+  const unsigned int lam_base = smem_u32(smem + A.lam_off) + (unsigned int)(wid * kMaxNP * 32 + lane) * 8u;
+#pragma unroll
+  for (int p = 0; p < NP; p++) {
+    const unsigned long long v = lx[p];
+    asm volatile("st.shared.b64 [%0], %1;" ::"r"(lam_base + (unsigned int)p * 256u), "l"(v) : "memory");
+  }
+  __syncwarp();
+#define MP_LX(p) lds64(lam_base + (unsigned int)(p) * 256u)
+#else
+#define MP_LX(p) lx[p]
+#endif
   float2 P[NP][3], N[NP][3];   // ping-pong horizontal lerps (3 channels x column pair)
 #define MP_HL(H, CH, A0, B0, A1, B1)                                                           \
   {                                                                                             \
     const float2 m_ = make_float2(u8m(smem[A0]), u8m(smem[B0]));                                \
     const float2 n_ = make_float2(u8m(smem[A1]), u8m(smem[B1]));                                \
-    H[p][CH] = ffma2_w(fsub2(n_, m_), lx[p], fsub2(m_, M2));                                     \
+    H[p][CH] = ffma2_w(fsub2(n_, m_), MP_LX(p), fsub2(m_, M2));                                  \
   }
   // NV12 chroma: one 16-bit load per tap fetches the (U, V) pair; bytes are
   // placed into the 2^23 fp32 pattern with one byte-permute each
@@ -365,17 +391,17 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
       {                                                                                         \
         const float2 m_ = make_float2(MP_MB(la_, 0), MP_MB(lb_, 0));                            \
         const float2 n_ = make_float2(MP_MB(la_, 3), MP_MB(lb_, 3));                            \
-        H[p][0] = ffma2_w(fsub2(n_, m_), lx[p], fsub2(m_, M2));                                 \
+        H[p][0] = ffma2_w(fsub2(n_, m_), MP_LX(p), fsub2(m_, M2));                              \
       }                                                                                         \
       {                                                                                         \
         const float2 m_ = make_float2(MP_MB(la_, 1), MP_MB(lb_, 1));                            \
         const float2 n_ = make_float2(MP_MB(ha_, 0), MP_MB(hb_, 0));                            \
-        H[p][1] = ffma2_w(fsub2(n_, m_), lx[p], fsub2(m_, M2));                                 \
+        H[p][1] = ffma2_w(fsub2(n_, m_), MP_LX(p), fsub2(m_, M2));                              \
       }                                                                                         \
       {                                                                                         \
         const float2 m_ = make_float2(MP_MB(la_, 2), MP_MB(lb_, 2));                            \
         const float2 n_ = make_float2(MP_MB(ha_, 1), MP_MB(hb_, 1));                            \
-        H[p][2] = ffma2_w(fsub2(n_, m_), lx[p], fsub2(m_, M2));                                 \
+        H[p][2] = ffma2_w(fsub2(n_, m_), MP_LX(p), fsub2(m_, M2));                              \
       }                                                                                         \
     }                                                                                           \
   } else {                                                                                      \
@@ -507,6 +533,7 @@ __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr*
 #undef MP_HRGB
 #undef MP_W6
 #undef MP_MB
+#undef MP_LX
 }
 
 template <int FMT, int SRC>
@@ -1037,8 +1064,15 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
   // classes stage 96 KB: the proxy-input downscale keeps its 2 x 96 KB ring)
   const size_t ring_cap = (2 * (size_t)A.stage_bytes + 4 * sizeof(uint64_t) <= 227 * 1024 - kSideReserve)
                               ? 227 * 1024 - kSideReserve : 227 * 1024;
-  while (A.stages > 2 && (size_t)A.stages * A.stage_bytes + 2 * A.stages * sizeof(uint64_t) > ring_cap) A.stages--;
-  const size_t smem = (size_t)A.stages * A.stage_bytes + 2 * A.stages * sizeof(uint64_t);
+#ifdef MP_LAM_SMEM
+  const size_t lam_bytes = (size_t)kCW * kMaxNP * 32 * 8;
+#else
+  const size_t lam_bytes = 0;
+#endif
+  while (A.stages > 2 && (size_t)A.stages * A.stage_bytes + 2 * A.stages * sizeof(uint64_t) + lam_bytes > ring_cap)
+    A.stages--;
+  A.lam_off = (int)(((size_t)A.stages * A.stage_bytes + 2 * A.stages * sizeof(uint64_t) + 15) & ~size_t(15));
+  const size_t smem = (size_t)A.lam_off + lam_bytes;
   if (smem > 227 * 1024) return MP_ERR_UNSUPPORTED;
   int dev = 0, sms = 0, per_sm = 0;
   MP_CUDA_TRY(cudaGetDevice(&dev));
