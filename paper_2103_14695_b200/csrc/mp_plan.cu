@@ -1107,7 +1107,12 @@ extern "C" mp_status mp_plan_windows(const mp_plan_params* p, const float* d_sco
     MP_CUDA_TRY(cudaGetLastError());
     if (L.slot_bytes) {   // grids whose worst case exceeds the shared-memory tiers
       const size_t smem_huge = plan_smem_bytes(A.R, A.words, 0, nullptr, nullptr);
-      plan_huge_kernel<<<plan_sms() * kHugeGrid, kPlanThreads, smem_huge, s>>>(
+      // one CTA per global scratch slot the caller's workspace holds (the
+      // workspace may have been sized on a device with fewer SMs)
+      const size_t slots = (ws_bytes - L.big_off) / L.slot_bytes;
+      const int grid = (int)(slots < (size_t)plan_sms() * kHugeGrid ? slots : (size_t)plan_sms() * kHugeGrid);
+      if (grid < 1) return MP_ERR_INVALID;
+      plan_huge_kernel<<<grid, kPlanThreads, smem_huge, s>>>(
           A, d_scores, d_mask, ws_win, ws_count, ws_cls, q2_cnt, q2_list, ws + L.big_off, L.slot_bytes);
       MP_CUDA_TRY(cudaGetLastError());
     }

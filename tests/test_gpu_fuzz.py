@@ -110,3 +110,50 @@ def test_random_end_to_end(G, seed):
     assert np.array_equal(g["frame_off"], r["frame_off"])
     assert np.array_equal(g["src"], r["src"])
     assert np.array_equal(g["boxes"].view(np.uint32), r["boxes"].view(np.float32).reshape(-1, 6).view(np.uint32))
+
+
+def _merge_heavy_problem(seed):
+    """Grids with many components (hundreds to thousands): every plan tier
+    (fast + its cooperative merge above 96 components, full <= 960 runs,
+    huge beyond) and cost tables from merge-averse to merge-happy."""
+    rng = np.random.default_rng(77000 + seed)
+    W, H = [(1920, 1080), (3840, 2160), (2560, 1440), (7680, 4320), (1280, 720)][seed % 5]
+    cw = ch = 32
+    R, C = -(-H // ch), -(-W // cw)
+    k = int(rng.integers(1, 5))
+    sizes = set()
+    while len(sizes) < k:
+        s = int(rng.choice([64, 96, 128, 192, 256, 384, 512, 768, 1024]))
+        sizes.add((min(s, W), min(int(s * rng.choice([0.5, 1.0, 1.5])), H)))
+    sizes.discard((W, H))
+    sizes = sorted(sizes, key=lambda s: (s[0] * s[1], s)) + [(W, H)]
+    areas = sorted({w * h for w, h in sizes})
+    style = seed % 3   # 0: cost ~ area (merges pay), 1: big fixed overhead (merges pay a lot), 2: steep (rarely pay)
+    base = {}
+    for i, a in enumerate(areas):
+        cells = a / (cw * ch)
+        base[a] = int(cells + (64 if style == 1 else 4) + (cells * cells / 50 if style == 2 else 0)) + i
+    cost = [base[w * h] for w, h in sizes]
+    if seed % 4 != 3:   # full frame never pays: the greedy's clusters are the output (no R11 fallback)
+        cost[-1] = 10 ** 9
+    F = 2
+    dens = float(rng.choice([0.03, 0.08, 0.2, 0.45]))
+    scores = np.zeros((F, R, C), np.float32)
+    for f in range(F):
+        z = (rng.random((R, C)) < dens).astype(np.float32) * 0.9
+        for _ in range(int(rng.integers(0, 40))):
+            r0, c0 = rng.integers(0, R), rng.integers(0, C)
+            z[r0:r0 + int(rng.integers(1, 6)), c0:c0 + int(rng.integers(1, 6))] = 0.9
+        scores[f] = z
+    return W, H, cw, ch, sizes, cost, scores
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_plan_merge_heavy(G, seed):
+    W, H, cw, ch, sizes, cost, scores = _merge_heavy_problem(seed)
+    ref = O.plan_windows(W, H, cw, ch, 0.5, sizes, cost, scores)
+    got = G.gpu_plan(W, H, cw, ch, 0.5, sizes, cost, scores)
+    assert got["status"] == ref["status"]
+    assert np.array_equal(got["frame_off"], ref["frame_off"])
+    assert np.array_equal(got["class_count"], ref["class_count"])
+    assert np.array_equal(got["windows"], ref["windows"])
