@@ -256,6 +256,40 @@ def test_gather_parity_scales_and_edges(G, scale, fmt, strided):
                 assert np.array_equal(got[q], ref[q])
 
 
+@pytest.mark.parametrize("strided", [True, False], ids=["tma_tensor", "ptr_array"])
+def test_gather_u8_fixed_tap_4_3_classes(G, strided):
+    """The u8 consumer of exact 4:3 classes (consume_tile_r43: fixed taps
+    i0 = 4k + j, lambda = 1/6, 1/2, 5/6) on every column-group width it
+    tiles with (ncg = 16, 8, 4: 192-, 96-, 48-wide tiles), full-frame and
+    ragged last row tiles, windows on the 16-px grid (fixed-tap path) and off
+    it (per-column fallback in the same launch), and 4:3 classes it does not
+    tile (ow / 12 not a multiple of 4: per-column consumer).  Within 1 LSB of
+    the oracle, and off by one only at near-ties (the fixed-tap arithmetic
+    errs by <= ~0.004 LSB): fewer than 0.5 % of the bytes."""
+    W, H = 960, 540
+    pitch = 3 * W
+    sizes = [(64, 64), (128, 128), (256, 256), (512, 384), (96, 72), (960, 540)]
+    out_dims = [(48, 48), (96, 96), (192, 192), (384, 288), (72, 54), (720, 405)]
+    frames = [S.frame_pixels_np(S.frame_seed(77, f), H, pitch) for f in range(3)]
+    rng = np.random.default_rng(43)
+    win = []
+    for f in range(3):
+        for q, (w, h) in enumerate(sizes):
+            xs = {0, W - w, 16 * int(rng.integers(0, (W - w) // 16 + 1)), int(rng.integers(0, W - w + 1))}
+            ys = {0, H - h, int(rng.integers(0, H - h + 1))}
+            for x in sorted(xs):
+                for y in sorted(ys):
+                    win.append([f, x, y, w, h, q, 0])
+    win = np.array(win, np.int32)
+    for q in range(len(sizes)):
+        sel = np.nonzero(win[:, 5] == q)[0]
+        win[sel, 6] = np.arange(len(sel))
+    ref, got = _gather_compare(G, frames, pitch, W, H, win, sizes, out_dims, 1, strided)
+    for q in range(len(sizes)):
+        d = got[q].astype(np.int32) != ref[q].astype(np.int32)
+        assert d.mean() < 0.005, (q, d.mean())
+
+
 def test_gather_capacity_and_invalid(G):
     W, H = 256, 128
     pitch = 3 * W
