@@ -532,8 +532,9 @@ def run_b200(args):
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            if pj.get("config") == cfg.name and pj.get("fmt") == args.fmt and pj.get("src", "rgb24") == args.src:
-                traffic = pj.get("dram_bytes_per_step")
+            for e in (pj if isinstance(pj, list) else [pj]):   # one ncu summary per (config, fmt, src)
+                if e.get("config") == cfg.name and e.get("fmt") == args.fmt and e.get("src", "rgb24") == args.src:
+                    traffic = e.get("dram_bytes_per_step")
         except (OSError, ValueError):
             pass
 
