@@ -759,16 +759,21 @@ __device__ __forceinline__ void consume_tile_u8rgb(const GatherArgs& A, const Ti
 constexpr float kR43L0 = 1.0f / 6.0f, kR43L1 = 0.5f, kR43L2 = 5.0f / 6.0f;
 constexpr int kR43Buf = 32 * 36;   // one warp output row: 32 tasks x 12 pixels x 3 bytes
 constexpr int kR43BufBytes = kCW * 2 * kR43Buf;
+constexpr int kR43FBuf = 32 * 48;  // one warp plane row (f32): 32 tasks x 12 floats
+constexpr int kR43FBufBytes = kCW * 2 * kR43FBuf;
 
 // horizontal lerps of one 48-byte source run at shared byte address A_:
 // H[j][c][kp] = (value of column 3(2kp) + j, column 3(2kp+1) + j), channel c
+#define MP_R43_LD(A_, Q)                                                                        \
+  uint4 Q[3];                                                                                   \
+  Q[0] = *reinterpret_cast<const uint4*>(&smem[(A_)]);                                          \
+  Q[1] = *reinterpret_cast<const uint4*>(&smem[(A_) + 16]);                                     \
+  Q[2] = *reinterpret_cast<const uint4*>(&smem[(A_) + 32]);
 #define MP_R43_H(A_, H)                                                                         \
   {                                                                                             \
-    const uint4 q0_ = *reinterpret_cast<const uint4*>(&smem[(A_)]);                             \
-    const uint4 q1_ = *reinterpret_cast<const uint4*>(&smem[(A_) + 16]);                        \
-    const uint4 q2_ = *reinterpret_cast<const uint4*>(&smem[(A_) + 32]);                        \
-    const uint32_t w_[12] = {q0_.x, q0_.y, q0_.z, q0_.w, q1_.x, q1_.y, q1_.z, q1_.w,            \
-                             q2_.x, q2_.y, q2_.z, q2_.w};                                       \
+    MP_R43_LD(A_, q_)                                                                           \
+    const uint32_t w_[12] = {q_[0].x, q_[0].y, q_[0].z, q_[0].w, q_[1].x, q_[1].y, q_[1].z, q_[1].w, \
+                             q_[2].x, q_[2].y, q_[2].z, q_[2].w};                               \
     _Pragma("unroll") for (int j = 0; j < 3; j++) {                                             \
       const float lam_ = j == 0 ? kR43L0 : (j == 1 ? kR43L1 : kR43L2);                          \
       _Pragma("unroll") for (int c = 0; c < 3; c++) {                                           \
@@ -886,6 +891,121 @@ __device__ __forceinline__ void consume_tile_r43(const GatherArgs& A, const Tile
 #undef MP_R43_H
 #undef MP_R43_ROW
 #undef MP_B1
+
+// f32 NCHW from RGB24 at an exact 4:3 downscale: the same fixed-tap tasks
+// (12 output columns x 3 output rows per consumer thread, LDS.128 source
+// runs), f32 arithmetic on the unbiased 0-255 scale (the 1e-3 bar is tighter
+// than the u8 path's 1 + b 2^-15 representation allows).  Value pairs are
+// output-ADJACENT columns (2i, 2i+1) so each plane row of a task leaves as
+// three 16-B stores (12 floats, 48 B) — the per-column consumer issued 6
+// LDS.U8 per column per staged row and 3 STG.32 per pixel (~12 LSU
+// instructions per pixel against ~1.1 here); the lambda of a pair is then a
+// constant pair: (L0, L1), (L2, L0), (L1, L2) for i mod 3 = 0, 1, 2.
+// H[c][i]: channel c, output columns (2i, 2i+1).
+__device__ __forceinline__ unsigned long long r43_lpair(int i) {
+  const int ja = (2 * i) % 3, jb = (2 * i + 1) % 3;
+  const float la = ja == 0 ? kR43L0 : (ja == 1 ? kR43L1 : kR43L2);
+  const float lb = jb == 0 ? kR43L0 : (jb == 1 ? kR43L1 : kR43L2);
+  return pk2(make_float2(la, lb));
+}
+#define MP_R43F_H(Q, H)                                                                         \
+  {                                                                                             \
+    const uint32_t w_[12] = {Q[0].x, Q[0].y, Q[0].z, Q[0].w, Q[1].x, Q[1].y, Q[1].z, Q[1].w,    \
+                             Q[2].x, Q[2].y, Q[2].z, Q[2].w};                                   \
+    _Pragma("unroll") for (int c = 0; c < 3; c++) {                                             \
+      _Pragma("unroll") for (int i = 0; i < 6; i++) {                                           \
+        const int ca_ = 2 * i, cb_ = 2 * i + 1;                                                 \
+        const int ma_ = 3 * (4 * (ca_ / 3) + ca_ % 3) + c, mb_ = 3 * (4 * (cb_ / 3) + cb_ % 3) + c; \
+        const float2 m_ = make_float2(MP_MB(w_[ma_ >> 2], ma_ & 3), MP_MB(w_[mb_ >> 2], mb_ & 3)); \
+        const float2 n_ = make_float2(MP_MB(w_[(ma_ + 3) >> 2], (ma_ + 3) & 3),                 \
+                                      MP_MB(w_[(mb_ + 3) >> 2], (mb_ + 3) & 3));                \
+        H[c][i] = ffma2_w(fsub2(n_, m_), r43_lpair(i), fsub2(m_, make_float2(8388608.0f, 8388608.0f))); \
+      }                                                                                         \
+    }                                                                                           \
+  }
+// one output row of the task, plane by plane: 12 floats (48 B) into this
+// lane's slot of the warp's plane-row buffer (3 STS.128, alternating between
+// two buffers), then the warp writes its 32 x 48 = 1536 bytes as 16-B chunks
+// (3 LDS.128 + 3 STG.128 per lane), every 32-B sector once.  (Three STG.128
+// per lane straight to global memory wrote each sector in two halves from
+// two instructions: 347 M L2 write sectors, lg_throttle, 1.69 ms at c2.)
+#define MP_R43F_ROW(T, B, LY, RR)                                                               \
+  {                                                                                             \
+    _Pragma("unroll") for (int c = 0; c < 3; c++) {                                             \
+      float2 v_[6];                                                                             \
+      _Pragma("unroll") for (int i = 0; i < 6; i++) v_[i] = ffma2_s(fsub2(B[c][i], T[c][i]), (LY), T[c][i]); \
+      const unsigned int sb_ = buf0 + (unsigned int)(par * kR43FBuf);                           \
+      float4* const sp_ = reinterpret_cast<float4*>(&smem[sb_ + 48u * (unsigned int)lane]);     \
+      sp_[0] = make_float4(v_[0].x, v_[0].y, v_[1].x, v_[1].y);                                 \
+      sp_[1] = make_float4(v_[2].x, v_[2].y, v_[3].x, v_[3].y);                                 \
+      sp_[2] = make_float4(v_[4].x, v_[4].y, v_[5].x, v_[5].y);                                 \
+      __syncwarp();                                                                             \
+      float* const o_ = orow + (size_t)c * plane + (size_t)(RR) * ow;                           \
+      if (full) {                                                                               \
+        _Pragma("unroll") for (int k = 0; k < 3; k++)                                           \
+          __stcs(reinterpret_cast<float4*>(o_ + coff[k]),                                       \
+                 *reinterpret_cast<const float4*>(&smem[sb_ + 16u * (unsigned int)(lane + 32 * k)])); \
+      } else {                                                                                  \
+        _Pragma("unroll") for (int k = 0; k < 3; k++)                                           \
+          if (rgw + cseg[k] < nrg)                                                              \
+            __stcs(reinterpret_cast<float4*>(o_ + coff[k]),                                     \
+                   *reinterpret_cast<const float4*>(&smem[sb_ + 16u * (unsigned int)(lane + 32 * k)])); \
+      }                                                                                         \
+      par ^= 1;                                                                                 \
+    }                                                                                           \
+  }
+#define MP_MB(W, K) __int_as_float(__byte_perm((W), 0x4B000000u, 0x7440u | (K)))
+__device__ __forceinline__ void consume_tile_r43f(const GatherArgs& A, const TileHdr* hdr, unsigned int soff,
+                                                  int wid, int lane) {
+  const int2* xt = reinterpret_cast<const int2*>(&smem[soff + kHdrBytes]) + hdr->xs;
+  const int q = hdr->k, rows = hdr->rows, cols = hdr->cols;
+  const int ncg = cols / 12, nrg = rows / 3, ntask = ncg * nrg;
+  const int ow = A.ow[q], oh = A.oh[q];
+  const size_t plane = (size_t)oh * ow;
+  const unsigned int stride = (unsigned int)hdr->stride;
+  const unsigned int a0 = soff + kDataOff + (unsigned int)(3 * hdr->x - hdr->b0 + 3 * xt[0].x);
+  float* const out0 = reinterpret_cast<float*>(A.out[q]) + (size_t)hdr->slot * 3 * plane +
+                      (size_t)hdr->oy0 * ow + hdr->ox0;
+  // this lane's copy-out chunks (96 per plane row: lane, lane + 32, lane + 64):
+  // run (row group offset) and float offset relative to the warp's first row
+  const int cps = 3 * ncg;   // 16-B chunks per run (ncg x 48 bytes)
+  size_t coff[3];
+  int cseg[3];
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    const int c = lane + 32 * k;
+    cseg[k] = c / cps;
+    coff[k] = (size_t)(3 * cseg[k]) * ow + 4 * (c - cseg[k] * cps);
+  }
+  const unsigned int buf0 = (unsigned int)A.obuf_off + (unsigned int)wid * (2 * kR43FBuf);
+  const int rpw = 32 / ncg;
+  int par = 0;
+  for (int base = 32 * wid; base < ntask; base += kCW * 32) {
+    const int rgw = base / ncg;
+    const int t = min(base + lane, ntask - 1);   // lanes past the tile redo its last task
+    const int rg = t / ncg, cg = t - rg * ncg;
+    const unsigned int a = a0 + (unsigned int)(4 * rg) * stride + 48u * (unsigned int)cg;
+    float* const orow = out0 + (size_t)(3 * rgw) * ow;
+    const bool full = rgw + rpw <= nrg;
+    float2 X[3][6], Y[3][6];
+    MP_R43_LD(a, ra)
+    MP_R43F_H(ra, X)
+    MP_R43_LD(a + stride, rb)
+    MP_R43F_H(rb, Y)
+    MP_R43F_ROW(X, Y, kR43L0, 0)
+    MP_R43_LD(a + 2 * stride, rc)
+    MP_R43F_H(rc, X)
+    MP_R43F_ROW(Y, X, kR43L1, 1)
+    MP_R43_LD(a + 3 * stride, rd)
+    MP_R43F_H(rd, Y)
+    MP_R43F_ROW(X, Y, kR43L2, 2)
+  }
+  __syncwarp();   // the last buffer's chunks are read before the next tile writes
+}
+#undef MP_MB
+#undef MP_R43F_H
+#undef MP_R43F_ROW
+#undef MP_R43_LD
 
 template <int FMT, int SRC>
 __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(const __grid_constant__ GatherArgs A,
@@ -1157,6 +1277,9 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
         }
       } else
 #endif
+      if (FMT == MP_OUT_F32_NCHW && SRC == kSrcRGB24 && A.r43[hdr->k] && (hdr->x & 15) == 0) {
+        consume_tile_r43f(A, hdr, soff, wid, lane);
+      } else
       switch (A.ncol[hdr->k]) {
         case 2: consume_tile<FMT, 2, SRC>(A, hdr, soff, wid, lane); break;
         case 4: consume_tile<FMT, 4, SRC>(A, hdr, soff, wid, lane); break;
@@ -1273,11 +1396,11 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
                               : (!bud && fmt == MP_OUT_F32_NCHW && src == kSrcRGB24 && ow > 512)
                                     ? (long long)kStageDataBudgetWide : budget;
     int TW = 0, TR = 0, bw = 0, bh = 0;
-    // u8 from RGB24 at an exact 4:3 downscale: fixed-tap tasks of 12 columns
-    // x 3 rows, one per consumer thread (consume_tile_r43): the widest column
+    // RGB24 at an exact 4:3 downscale: fixed-tap tasks of 12 columns x 3
+    // rows, one per consumer thread (consume_tile_r43 / _r43f): the widest column
     // group count ncg in {16, 8, 4} dividing ow / 12, then as many row groups
     // as there are consumer threads left (box within the stage budget)
-    const bool r43 = fmt == MP_OUT_U8_NHWC && src == kSrcRGB24 && !sparse && 3 * w == 4 * ow && 3 * h == 4 * oh &&
+    const bool r43 = src == kSrcRGB24 && !sparse && 3 * w == 4 * ow && 3 * h == 4 * oh &&
                      ow % 12 == 0 && oh % 3 == 0 && !knob("MP_GATHER_TILE");
     if (r43) {
       // ncg: a multiple of 4 dividing 32 (whole row groups per warp, 16-B runs)
@@ -1286,7 +1409,10 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
         for (int nrg = min(min(kCW * 32 / ncg, oh / 3), kMaxTR / 3); nrg >= 1; nrg--) {
           int cbw, cbh;
           class_box(w, h, ow, oh, 12 * ncg, 3 * nrg, src, &cbw, &cbh);
-          if (stage_data_bytes(src, false, cbw, cbh, 3 * nrg) <= cbudget && cbw <= 2048 && cbh <= 256) {
+          // stage budget: every consumer thread busy beats more stages (u8
+          // A/B: 3 x 40 KB 1.047 ms, 3 x 44 KB 0.962, 2 x ~53 KB 0.859)
+          if (stage_data_bytes(src, false, cbw, cbh, 3 * nrg) <= (bud ? budget : kStageDataBudgetU8) &&
+              cbw <= 2048 && cbh <= 256) {
             TW = 12 * ncg;
             TR = 3 * nrg;
             bw = cbw;
@@ -1454,9 +1580,9 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
   // (they must co-run beside this persistent kernel, or they queue behind it
   // and serialise the pipeline), or when it does not fit at all (row-sparse
   // classes stage 96 KB: the proxy-input downscale keeps its 2 x 96 KB ring)
-  bool any_r43 = false;
+  bool any_r43 = false;   // fixed-tap classes stage their output rows per warp
   for (int q = 0; q < A.k; q++) any_r43 = any_r43 || A.r43[q];
-  const size_t obuf_bytes = any_r43 ? (size_t)kR43BufBytes : 0;   // r43 output-row buffers
+  const size_t obuf_bytes = !any_r43 ? 0 : (fmt == MP_OUT_U8_NHWC ? (size_t)kR43BufBytes : (size_t)kR43FBufBytes);
   const size_t ring_cap = (2 * (size_t)A.stage_bytes + 4 * sizeof(uint64_t) + obuf_bytes <= 227 * 1024 - kSideReserve)
                               ? 227 * 1024 - kSideReserve : 227 * 1024;
 #ifdef MP_LAM_SMEM
