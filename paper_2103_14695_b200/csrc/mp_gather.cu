@@ -41,7 +41,17 @@ constexpr int kTileChunk = MP_TILE_CHUNK;   // tiles per dynamic-scheduling tick
 #ifndef MP_KCW
 #define MP_KCW 8
 #endif
-constexpr int kCW = MP_KCW;   // consumer warps per CTA; each owns a block of TR/kCW output rows
+// consumer warps per CTA (each owns a block of TR / cw output rows): cw_of()
+#ifndef MP_KCW_U8
+#define MP_KCW_U8 12
+#endif
+// u8 output from RGB24 runs 12 consumer warps (the fixed-tap consumer is
+// latency-bound at 8: 128 registers x 416 threads; gather alone c2 0.860 ->
+// 0.748 ms, c3 3.62 -> 3.02, c4 2.39 -> 1.92; f32 is faster with 8: c2 1.369
+// vs 1.429 ms; 16 warps spill; profiles/ab/r02_consumer_warps_r43.jsonl)
+__host__ __device__ constexpr int cw_of(int fmt, int src) {
+  return (fmt == MP_OUT_U8_NHWC && src == 0) ? MP_KCW_U8 : MP_KCW;
+}
 constexpr int kStages = 2;      // default ring depth (A.stages; MP_GATHER_STAGES overrides, <= kMaxStages)
 constexpr int kStagesF32 = 3;   // f32 output: 3 x 40 KB (measured c2 1.424 -> 1.389 ms, c3 6.86 -> 6.35, c4 4.22 -> 4.27
                                 // against 2 x 44 KB; 2 x 40 KB is slower, 1.53)
@@ -51,7 +61,7 @@ constexpr int kMaxStages = 8;
 constexpr size_t kSideReserve = 56 * 1024;
 constexpr int kHdrBytes = 64;
 constexpr int kMaxTW = 256;
-constexpr int kMaxTR = 8 * kCW > 192 ? 8 * kCW : 192;   // Rw <= 8 rows per consumer warp; r43 tiles <= 64 row groups
+constexpr int kMaxTR = 192;   // Rw <= 8 rows per consumer warp (<= 16 warps); r43 tiles <= 64 row groups
 constexpr int kXtapBytes = (kMaxTW + 2) * 8, kYtapBytes = (kMaxTR + 2) * 8;
 constexpr int kTapBytes = kXtapBytes + kYtapBytes;
 constexpr int kStageDataBudget = 40 * 1024;        // dense classes, RGB f32 output (three stages, kStagesF32)
@@ -262,6 +272,7 @@ static inline const char* knob(const char* name) {
 template <int FMT, int NCOL, int SRC>
 __device__ __forceinline__ void consume_tile(const GatherArgs& A, const TileHdr* hdr, unsigned int soff, int wid,
                                              int lane) {
+  constexpr int kCW = cw_of(FMT, SRC);
   constexpr int NP = NCOL / 2;
   const int2* xt = reinterpret_cast<const int2*>(&smem[soff + kHdrBytes]);
   const int2* yt = reinterpret_cast<const int2*>(&smem[soff + kHdrBytes + kXtapBytes]) + hdr->ys;
@@ -590,6 +601,7 @@ __device__ __forceinline__ float2 ffma2_s(float2 a, float s, float2 c) {   // a 
 template <int NCOL>
 __device__ __forceinline__ void consume_tile_u8rgb(const GatherArgs& A, const TileHdr* hdr, unsigned int soff,
                                                    int wid, int lane) {
+  constexpr int kCW = cw_of(MP_OUT_U8_NHWC, kSrcRGB24);
   constexpr int SRC = kSrcRGB24;
   constexpr int NP = NCOL / 2;
   const int2* xt = reinterpret_cast<const int2*>(&smem[soff + kHdrBytes]) + hdr->xs;
@@ -758,9 +770,9 @@ __device__ __forceinline__ void consume_tile_u8rgb(const GatherArgs& A, const Ti
 // and every lerp takes its weight as an immediate broadcast.
 constexpr float kR43L0 = 1.0f / 6.0f, kR43L1 = 0.5f, kR43L2 = 5.0f / 6.0f;
 constexpr int kR43Buf = 32 * 36;   // one warp output row: 32 tasks x 12 pixels x 3 bytes
-constexpr int kR43BufBytes = kCW * 2 * kR43Buf;
+constexpr int kR43BufBytes = MP_KCW_U8 * kR43Buf;   // one row buffer per u8 consumer warp
 constexpr int kR43FBuf = 32 * 48;  // one warp plane row (f32): 32 tasks x 12 floats
-constexpr int kR43FBufBytes = kCW * 2 * kR43FBuf;
+constexpr int kR43FBufBytes = MP_KCW * 2 * kR43FBuf;   // two plane-row buffers per f32 consumer warp
 
 // horizontal lerps of one 48-byte source run at shared byte address A_:
 // H[j][c][kp] = (value of column 3(2kp) + j, column 3(2kp+1) + j), channel c
@@ -822,6 +834,7 @@ constexpr int kR43FBufBytes = kCW * 2 * kR43FBuf;
 // 9 STG.32 directly measured 1.58 ms at c2: 287 M partial L2 sector writes.)
 __device__ __forceinline__ void consume_tile_r43(const GatherArgs& A, const TileHdr* hdr, unsigned int soff,
                                                  int wid, int lane) {
+  constexpr int kCW = cw_of(MP_OUT_U8_NHWC, kSrcRGB24);
   const int2* xt = reinterpret_cast<const int2*>(&smem[soff + kHdrBytes]) + hdr->xs;
   const int q = hdr->k, rows = hdr->rows, cols = hdr->cols;
   const int ncg = cols / 12, nrg = rows / 3, ntask = ncg * nrg;
@@ -846,7 +859,7 @@ __device__ __forceinline__ void consume_tile_r43(const GatherArgs& A, const Tile
     coff[k] = (size_t)(3 * cseg[k]) * row3 + 16 * (c - cseg[k] * cps);
   }
   const bool third = lane < 8;   // chunk lane + 64 exists
-  const unsigned int buf0 = (unsigned int)A.obuf_off + (unsigned int)wid * (2 * kR43Buf);
+  const unsigned int buf0 = (unsigned int)A.obuf_off + (unsigned int)wid * kR43Buf;
   const unsigned int bl = buf0 + 16u * (unsigned int)lane;
   const int rpw = 32 / ncg;   // row groups per warp
   for (int base = 32 * wid; base < ntask; base += kCW * 32) {
@@ -873,18 +886,22 @@ __device__ __forceinline__ void consume_tile_r43(const GatherArgs& A, const Tile
           __stcs(reinterpret_cast<int4*>(o_ + coff[k]), *reinterpret_cast<const int4*>(&smem[s_ + 512 * k])); \
     }                                                                                           \
   }
+    // one row buffer per warp (shared memory beside the 12-warp ring): a
+    // __syncwarp after each copy-out orders its reads before the next row's
+    // writes
     MP_R43_H(a, X)
     MP_R43_H(a + stride, Y)
     MP_R43_ROW(X, Y, kR43L0, buf0 + 36u * (unsigned int)lane)
     MP_R43_OUT(0, 0)
+    __syncwarp();
     MP_R43_H(a + 2 * stride, X)
-    MP_R43_ROW(Y, X, kR43L1, buf0 + kR43Buf + 36u * (unsigned int)lane)
-    MP_R43_OUT(1, 1)
+    MP_R43_ROW(Y, X, kR43L1, buf0 + 36u * (unsigned int)lane)
+    MP_R43_OUT(1, 0)
+    __syncwarp();
     MP_R43_H(a + 3 * stride, Y)
-    __syncwarp();   // row 0's chunks are read before buffer 0 is written again
     MP_R43_ROW(X, Y, kR43L2, buf0 + 36u * (unsigned int)lane)
     MP_R43_OUT(2, 0)
-    __syncwarp();   // ... and row 2's before the next pass writes buffer 0
+    __syncwarp();
 #undef MP_R43_OUT
   }
 }
@@ -957,6 +974,7 @@ __device__ __forceinline__ unsigned long long r43_lpair(int i) {
 #define MP_MB(W, K) __int_as_float(__byte_perm((W), 0x4B000000u, 0x7440u | (K)))
 __device__ __forceinline__ void consume_tile_r43f(const GatherArgs& A, const TileHdr* hdr, unsigned int soff,
                                                   int wid, int lane) {
+  constexpr int kCW = cw_of(MP_OUT_F32_NCHW, kSrcRGB24);
   const int2* xt = reinterpret_cast<const int2*>(&smem[soff + kHdrBytes]) + hdr->xs;
   const int q = hdr->k, rows = hdr->rows, cols = hdr->cols;
   const int ncg = cols / 12, nrg = rows / 3, ntask = ncg * nrg;
@@ -1008,7 +1026,7 @@ __device__ __forceinline__ void consume_tile_r43f(const GatherArgs& A, const Til
 #undef MP_R43_LD
 
 template <int FMT, int SRC>
-__global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(const __grid_constant__ GatherArgs A,
+__global__ void __launch_bounds__((cw_of(FMT, SRC) + kProducerWarps) * 32) gather_kernel(const __grid_constant__ GatherArgs A,
                                                                  const __grid_constant__ TmapArray tm,
                                                                  const uint8_t* const* __restrict__ frames,
                                                                  int* __restrict__ ws_cnt,
@@ -1017,6 +1035,7 @@ __global__ void __launch_bounds__((kCW + kProducerWarps) * 32) gather_kernel(con
                                                                  const int* __restrict__ frame_off,
                                                                  const int2* __restrict__ ws_tap,
                                                                  int* __restrict__ d_status) {
+  constexpr int kCW = cw_of(FMT, SRC);
   const int nst = A.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nst * A.stage_bytes);
   uint64_t* empty = full + nst;
@@ -1351,6 +1370,7 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
   if (!sizes || !out_dims || !d_out || !out_cap) return false;
   if (fmt != MP_OUT_F32_NCHW && fmt != MP_OUT_U8_NHWC) return false;
   memset(A, 0, sizeof(*A));
+  const int cw = cw_of(fmt, src);   // consumer warps of this instantiation
   A->k = k;
   A->W = W;
   A->H = H;
@@ -1375,7 +1395,7 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
     A->oh[q] = oh;
     // column tiles of equal width TW <= 256 (so every tile's TMA box is the
     // class box, no over-fetch), NCOL = TW/32 rounded up to even columns per
-    // lane; rows: kCW warps x Rw rows each, Rw as large as the stage budget
+    // lane; rows: cw warps x Rw rows each, Rw as large as the stage budget
     // and the TMA box limits (256 rows, 256 x 8 bytes) allow (<= 8).
     // Tile width (measured on B200): stores must start on full 128-B lines —
     // so prefer the largest TW <= 256 that is a multiple of 32 and divides ow
@@ -1406,7 +1426,7 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
       // ncg: a multiple of 4 dividing 32 (whole row groups per warp, 16-B runs)
       for (int ncg = 16; ncg >= 4 && !TW; ncg /= 2) {
         if ((ow / 12) % ncg || 12 * ncg > kMaxTW) continue;
-        for (int nrg = min(min(kCW * 32 / ncg, oh / 3), kMaxTR / 3); nrg >= 1; nrg--) {
+        for (int nrg = min(min(cw * 32 / ncg, oh / 3), kMaxTR / 3); nrg >= 1; nrg--) {
           int cbw, cbh;
           class_box(w, h, ow, oh, 12 * ncg, 3 * nrg, src, &cbw, &cbh);
           // stage budget: every consumer thread busy beats more stages (u8
@@ -1425,12 +1445,12 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
     A->r43[q] = TW ? 1 : 0;
     auto fit_rows = [&](int tw, int& rw, int& cbw, int& cbh) {
       for (rw = 8; rw >= 1; rw--) {
-        class_box(w, h, ow, oh, tw, kCW * rw, src, &cbw, &cbh);
+        class_box(w, h, ow, oh, tw, cw * rw, src, &cbw, &cbh);
         if (sparse) {   // gather4 destinations: 4 rows x box_w bytes, 128-B aligned
           cbh = 1;
           cbw = (cbw + 31) / 32 * 32;
         }
-        if (stage_data_bytes(src, sparse, cbw, cbh, kCW * rw) <= cbudget && cbw <= 2048 && cbh <= 256)
+        if (stage_data_bytes(src, sparse, cbw, cbh, cw * rw) <= cbudget && cbw <= 2048 && cbh <= 256)
           return true;
       }
       return false;
@@ -1442,7 +1462,7 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
       int rw, cbw, cbh;
       if (fit_rows(tw, rw, cbw, cbh) && rw >= min_rw) {
         TW = tw;
-        TR = kCW * rw;
+        TR = cw * rw;
         bw = cbw;
         bh = cbh;
       }
@@ -1453,9 +1473,9 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
     // is the bound (c3, ow = 1440: 160 -> 192 columns, 5.58 -> 5.20 ms)
     if (TW && !A->r43[q] && fmt == MP_OUT_U8_NHWC && ((TW / 32) & 1) && TW + 32 <= kMaxTW && ow > TW + 32) {
       int rw, cbw, cbh;
-      if (fit_rows(TW + 32, rw, cbw, cbh) && kCW * rw >= TR) {
+      if (fit_rows(TW + 32, rw, cbw, cbh) && cw * rw >= TR) {
         TW += 32;
-        TR = kCW * rw;
+        TR = cw * rw;
         bw = cbw;
         bh = cbh;
       }
@@ -1467,7 +1487,7 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
       int rw, cbw, cbh;
       if (fit_rows(tw, rw, cbw, cbh) && (rw >= min_rw || tw <= 32)) {
         TW = tw;
-        TR = kCW * rw;
+        TR = cw * rw;
         bw = cbw;
         bh = cbh;
       }
@@ -1478,7 +1498,7 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
       int fow = 0, ftw = 0, frw = 0;
       if (ft && sscanf(ft, "%d,%d,%d", &fow, &ftw, &frw) == 3 && fow == ow) {
         TW = ftw;
-        TR = kCW * frw;
+        TR = cw * frw;
         class_box(w, h, ow, oh, TW, TR, src, &bw, &bh);
         if (sparse) {
           bh = 1;
@@ -1586,7 +1606,7 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
   const size_t ring_cap = (2 * (size_t)A.stage_bytes + 4 * sizeof(uint64_t) + obuf_bytes <= 227 * 1024 - kSideReserve)
                               ? 227 * 1024 - kSideReserve : 227 * 1024;
 #ifdef MP_LAM_SMEM
-  const size_t lam_bytes = (size_t)kCW * kMaxNP * 32 * 8;
+  const size_t lam_bytes = (size_t)cw_of(fmt, A.src) * kMaxNP * 32 * 8;
 #else
   const size_t lam_bytes = 0;
 #endif
@@ -1612,7 +1632,7 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
   // skips the consumer math, =2 skips the pixel copies.  Unset in production.
   const char* dbg = knob("MP_GATHER_DEBUG");
   A.debug = dbg ? atoi(dbg) : 0;
-  const int threads = (kCW + kProducerWarps) * 32;
+  const int threads = (cw_of(fmt, A.src) + kProducerWarps) * 32;
   auto launch = [&](auto kern) -> mp_status {
     // cache key: kernel instance x device x dynamic shared memory
     struct Occ {
