@@ -1423,16 +1423,23 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
     const bool r43 = src == kSrcRGB24 && !sparse && 3 * w == 4 * ow && 3 * h == 4 * oh &&
                      ow % 12 == 0 && oh % 3 == 0 && !knob("MP_GATHER_TILE");
     if (r43) {
+      // stage budget: two stages and the consumers' output-row buffers leave
+      // kSideReserve (every consumer thread busy beats more, smaller stages:
+      // u8 A/B 3 x 40 KB 1.047 ms, 3 x 44 KB 0.962, 2 x ~53 KB 0.859)
+      const long long obuf = fmt == MP_OUT_U8_NHWC ? kR43BufBytes : kR43FBufBytes;
+      const long long r43_budget =
+          bud ? budget : (227LL * 1024 - (long long)kSideReserve - obuf - 64) / 2 - kDataOff - 64 - 127;
       // ncg: a multiple of 4 dividing 32 (whole row groups per warp, 16-B runs)
       for (int ncg = 16; ncg >= 4 && !TW; ncg /= 2) {
         if ((ow / 12) % ncg || 12 * ncg > kMaxTW) continue;
+        // as many row groups as there are consumer threads (a short last row
+        // tile stages rows no task uses — the TMA box is the class's — but
+        // equal row tiles with idle threads measured slower: c2 u8 0.761 ->
+        // 0.778 ms, c3 3.06 -> 3.15, profiles/ab/r02_u8_equal_row_tiles.jsonl)
         for (int nrg = min(min(cw * 32 / ncg, oh / 3), kMaxTR / 3); nrg >= 1; nrg--) {
           int cbw, cbh;
           class_box(w, h, ow, oh, 12 * ncg, 3 * nrg, src, &cbw, &cbh);
-          // stage budget: every consumer thread busy beats more stages (u8
-          // A/B: 3 x 40 KB 1.047 ms, 3 x 44 KB 0.962, 2 x ~53 KB 0.859)
-          if (stage_data_bytes(src, false, cbw, cbh, 3 * nrg) <= (bud ? budget : kStageDataBudgetU8) &&
-              cbw <= 2048 && cbh <= 256) {
+          if (stage_data_bytes(src, false, cbw, cbh, 3 * nrg) <= r43_budget && cbw <= 2048 && cbh <= 256) {
             TW = 12 * ncg;
             TR = 3 * nrg;
             bw = cbw;
