@@ -772,7 +772,7 @@ constexpr float kR43L0 = 1.0f / 6.0f, kR43L1 = 0.5f, kR43L2 = 5.0f / 6.0f;
 constexpr int kR43Buf = 32 * 36;   // one warp output row: 32 tasks x 12 pixels x 3 bytes
 constexpr int kR43BufBytes = MP_KCW_U8 * kR43Buf;   // one row buffer per u8 consumer warp
 constexpr int kR43FBuf = 32 * 48;  // one warp plane row (f32): 32 tasks x 12 floats
-constexpr int kR43FBufBytes = MP_KCW * 2 * kR43FBuf;   // two plane-row buffers per f32 consumer warp
+constexpr int kR43FBufBytes = MP_KCW * kR43FBuf;   // one plane-row buffer per f32 consumer warp
 
 // horizontal lerps of one 48-byte source run at shared byte address A_:
 // H[j][c][kp] = (value of column 3(2kp) + j, column 3(2kp+1) + j), channel c
@@ -941,9 +941,13 @@ __device__ __forceinline__ unsigned long long r43_lpair(int i) {
     }                                                                                           \
   }
 // one output row of the task, plane by plane: 12 floats (48 B) into this
-// lane's slot of the warp's plane-row buffer (3 STS.128, alternating between
-// two buffers), then the warp writes its 32 x 48 = 1536 bytes as 16-B chunks
-// (3 LDS.128 + 3 STG.128 per lane), every 32-B sector once.  (Three STG.128
+// lane's slot of the warp's plane-row buffer (3 STS.128), then the warp
+// writes its 32 x 48 = 1536 bytes as 16-B chunks (3 LDS.128 + 3 STG.128 per
+// lane), every 32-B sector once; a __syncwarp orders the chunk reads before
+// the next plane's writes.  One buffer per warp: with two, the c4 ring (2 x
+// ~54 KB + 24 KB) left room for only two co-running 34-KB plan CTAs per SM
+// instead of three, and the planner fell behind the gather (c4 step 3.9 ->
+// 4.5 ms, profiles/r02_timeline_c4_r43f_2buf.txt).  (Three STG.128
 // per lane straight to global memory wrote each sector in two halves from
 // two instructions: 347 M L2 write sectors, lg_throttle, 1.69 ms at c2.)
 #define MP_R43F_ROW(T, B, LY, RR)                                                               \
@@ -951,7 +955,7 @@ __device__ __forceinline__ unsigned long long r43_lpair(int i) {
     _Pragma("unroll") for (int c = 0; c < 3; c++) {                                             \
       float2 v_[6];                                                                             \
       _Pragma("unroll") for (int i = 0; i < 6; i++) v_[i] = ffma2_s(fsub2(B[c][i], T[c][i]), (LY), T[c][i]); \
-      const unsigned int sb_ = buf0 + (unsigned int)(par * kR43FBuf);                           \
+      const unsigned int sb_ = buf0;                                                            \
       float4* const sp_ = reinterpret_cast<float4*>(&smem[sb_ + 48u * (unsigned int)lane]);     \
       sp_[0] = make_float4(v_[0].x, v_[0].y, v_[1].x, v_[1].y);                                 \
       sp_[1] = make_float4(v_[2].x, v_[2].y, v_[3].x, v_[3].y);                                 \
@@ -968,7 +972,7 @@ __device__ __forceinline__ unsigned long long r43_lpair(int i) {
             __stcs(reinterpret_cast<float4*>(o_ + coff[k]),                                     \
                    *reinterpret_cast<const float4*>(&smem[sb_ + 16u * (unsigned int)(lane + 32 * k)])); \
       }                                                                                         \
-      par ^= 1;                                                                                 \
+      __syncwarp();                                                                             \
     }                                                                                           \
   }
 #define MP_MB(W, K) __int_as_float(__byte_perm((W), 0x4B000000u, 0x7440u | (K)))
@@ -995,9 +999,8 @@ __device__ __forceinline__ void consume_tile_r43f(const GatherArgs& A, const Til
     cseg[k] = c / cps;
     coff[k] = (size_t)(3 * cseg[k]) * ow + 4 * (c - cseg[k] * cps);
   }
-  const unsigned int buf0 = (unsigned int)A.obuf_off + (unsigned int)wid * (2 * kR43FBuf);
+  const unsigned int buf0 = (unsigned int)A.obuf_off + (unsigned int)wid * kR43FBuf;
   const int rpw = 32 / ncg;
-  int par = 0;
   for (int base = 32 * wid; base < ntask; base += kCW * 32) {
     const int rgw = base / ncg;
     const int t = min(base + lane, ntask - 1);   // lanes past the tile redo its last task
@@ -1018,7 +1021,6 @@ __device__ __forceinline__ void consume_tile_r43f(const GatherArgs& A, const Til
     MP_R43F_H(rd, Y)
     MP_R43F_ROW(X, Y, kR43L2, 2)
   }
-  __syncwarp();   // the last buffer's chunks are read before the next tile writes
 }
 #undef MP_MB
 #undef MP_R43F_H
