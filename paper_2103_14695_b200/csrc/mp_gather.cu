@@ -583,6 +583,31 @@ __device__ __forceinline__ float2 ffma2_s(float2 a, float s, float2 c) {   // a 
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(make_float2(s, s))), "l"(pk2(c)));
   return upk2(r);
 }
+// Bounds-checked dev builds (-DMP_BOUNDS_CHECK; the GPU suite runs through
+// one — the pool's compute-sanitizer is closed): every shared-memory access
+// of the round-2b consumers stays inside its stage's staged box / its warp's
+// row buffer, and every global store inside its class's output tensor;
+// a violation prints and traps.
+#ifdef MP_BOUNDS_CHECK
+__device__ __noinline__ void mp_bounds_fail(const char* what, long long a, long long lo, long long hi) {
+  printf("MP_BOUNDS_CHECK %s: [%lld] not in [%lld, %lld) block %d thread %d\n", what, a, lo, hi, (int)blockIdx.x,
+         (int)threadIdx.x);
+  __trap();
+}
+#define MP_BCHK(WHAT, A_, N_, LO_, HI_)                                                         \
+  {                                                                                             \
+    const long long a__ = (long long)(A_), lo__ = (long long)(LO_), hi__ = (long long)(HI_);    \
+    if ((long long)(N_) > 0 && (a__ < lo__ || a__ + (long long)(N_) > hi__))                    \
+      mp_bounds_fail(WHAT, a__, lo__, hi__);                                                    \
+  }
+#else
+#define MP_BCHK(WHAT, A_, N_, LO_, HI_) {}   /* a statement: "if (c) MP_BCHK(...)" stays an if */
+#endif
+// output tensor of class q in bytes (fmt: u8 NHWC or f32 NCHW)
+__device__ __forceinline__ long long out_bytes(const GatherArgs& A, int q) {
+  return (long long)A.cap[q] * A.oh[q] * A.ow[q] * (A.fmt == MP_OUT_U8_NHWC ? 3 : 12);
+}
+
 // byte K of W -> 1 + byte * 2^-15 (bits 8..15 of 1.0f = 0x3F800000)
 #define MP_B1(W, K) __int_as_float(__byte_perm((W), 0x3F800000u, 0x7604u | ((K) << 4)))
 
@@ -632,6 +657,7 @@ __device__ __forceinline__ void consume_tile_u8rgb(const GatherArgs& A, const Ti
   float2 P[NP][3], N[NP][3];   // [0] (R, G) of A, [1] (R, G) of B, [2] (B of A, B of B)
 #define MP_W6(WB, SH, LO, HI)                                                                   \
   {                                                                                             \
+    MP_BCHK("u8rgb lds", WB, 12, doff, soff + A.stage_bytes)                                    \
     const uint32_t w0_ = *reinterpret_cast<const uint32_t*>(&smem[WB]);                         \
     const uint32_t w1_ = *reinterpret_cast<const uint32_t*>(&smem[(WB) + 4]);                   \
     const uint32_t w2_ = *reinterpret_cast<const uint32_t*>(&smem[(WB) + 8]);                   \
@@ -689,6 +715,7 @@ __device__ __forceinline__ void consume_tile_u8rgb(const GatherArgs& A, const Ti
     uint8_t* const ol_ = o + 3 * lane;                                                          \
     _Pragma("unroll") for (int p = 0; p < NP; p++) {                                            \
       MP_U8V(T, B)                                                                              \
+      MP_BCHK("u8rgb stg", ol_ + 192 * p - (uint8_t*)A.out[q], ok[2 * p + 1] ? 99 : (ok[2 * p] ? 3 : 0), 0, out_bytes(A, q)) \
       MP_U8_STORE(ol_, p, u0, u1, u2)                                                           \
     }                                                                                           \
     o += (size_t)ow * 3;                                                                        \
@@ -777,6 +804,7 @@ constexpr int kR43FBufBytes = MP_KCW * kR43FBuf;   // one plane-row buffer per f
 // horizontal lerps of one 48-byte source run at shared byte address A_:
 // H[j][c][kp] = (value of column 3(2kp) + j, column 3(2kp+1) + j), channel c
 #define MP_R43_LD(A_, Q)                                                                        \
+  MP_BCHK("r43 lds", A_, 48, soff + kDataOff, soff + A.stage_bytes)                              \
   uint4 Q[3];                                                                                   \
   Q[0] = *reinterpret_cast<const uint4*>(&smem[(A_)]);                                          \
   Q[1] = *reinterpret_cast<const uint4*>(&smem[(A_) + 16]);                                     \
@@ -818,6 +846,7 @@ constexpr int kR43FBufBytes = MP_KCW * kR43FBuf;   // one plane-row buffer per f
         b_[e] = __float_as_uint((k & 1) ? u_[j][c][k >> 1].y : u_[j][c][k >> 1].x);             \
       }                                                                                         \
       const uint32_t lo_ = __byte_perm(b_[0], b_[1], 0x0040u), hi_ = __byte_perm(b_[2], b_[3], 0x0040u); \
+      MP_BCHK("r43 sts", (BUF_) + 4 * wi, 4, buf0, buf0 + kR43Buf)                               \
       *reinterpret_cast<uint32_t*>(&smem[(BUF_) + 4 * wi]) = __byte_perm(lo_, hi_, 0x5410u);    \
     }                                                                                           \
   }
@@ -867,6 +896,8 @@ __device__ __forceinline__ void consume_tile_r43(const GatherArgs& A, const Tile
     const int t = min(base + lane, ntask - 1);            // lanes past the tile redo its last task
     const int rg = t / ncg, cg = t - rg * ncg;
     const unsigned int a = a0 + (unsigned int)(4 * rg) * stride + 48u * (unsigned int)cg;
+    MP_BCHK("r43 box rows", 4 * rg, 4, 0, A.box_h[q])
+    MP_BCHK("r43 box cols", a0 - (soff + kDataOff) + 48u * cg, 48, 0, stride)
     uint8_t* const orow = out0 + (size_t)(3 * rgw) * row3;
     const bool full = rgw + rpw <= nrg;   // every run of the warp lies in the tile (all but a ragged last tile)
     float2 X[3][3][2], Y[3][3][2];
@@ -876,14 +907,20 @@ __device__ __forceinline__ void consume_tile_r43(const GatherArgs& A, const Tile
     uint8_t* const o_ = orow + (size_t)(RR) * row3;                                             \
     const unsigned int s_ = bl + (BUFI) * kR43Buf;                                              \
     if (full) {                                                                                 \
+      MP_BCHK("r43 stg", o_ + coff[0] - (uint8_t*)A.out[q], 16, 0, out_bytes(A, q))             \
+      MP_BCHK("r43 stg", o_ + coff[1] - (uint8_t*)A.out[q], 16, 0, out_bytes(A, q))             \
+      MP_BCHK("r43 lds.128", s_ + (third ? 1024 : 512), 16, buf0, buf0 + kR43Buf)                \
+      if (third) MP_BCHK("r43 stg", o_ + coff[2] - (uint8_t*)A.out[q], 16, 0, out_bytes(A, q))  \
       __stcs(reinterpret_cast<int4*>(o_ + coff[0]), *reinterpret_cast<const int4*>(&smem[s_])); \
       __stcs(reinterpret_cast<int4*>(o_ + coff[1]), *reinterpret_cast<const int4*>(&smem[s_ + 512])); \
       if (third)                                                                                \
         __stcs(reinterpret_cast<int4*>(o_ + coff[2]), *reinterpret_cast<const int4*>(&smem[s_ + 1024])); \
     } else {                                                                                    \
       _Pragma("unroll") for (int k = 0; k < 3; k++)                                             \
-        if ((k < 2 || third) && rgw + cseg[k] < nrg)                                            \
+        if ((k < 2 || third) && rgw + cseg[k] < nrg) {                                          \
+          MP_BCHK("r43 stg", o_ + coff[k] - (uint8_t*)A.out[q], 16, 0, out_bytes(A, q))         \
           __stcs(reinterpret_cast<int4*>(o_ + coff[k]), *reinterpret_cast<const int4*>(&smem[s_ + 512 * k])); \
+        }                                                                                       \
     }                                                                                           \
   }
     // one row buffer per warp (shared memory beside the 12-warp ring): a
@@ -956,6 +993,7 @@ __device__ __forceinline__ unsigned long long r43_lpair(int i) {
       float2 v_[6];                                                                             \
       _Pragma("unroll") for (int i = 0; i < 6; i++) v_[i] = ffma2_s(fsub2(B[c][i], T[c][i]), (LY), T[c][i]); \
       const unsigned int sb_ = buf0;                                                            \
+      MP_BCHK("r43f sts", sb_ + 48u * (unsigned int)lane, 48, buf0, buf0 + kR43FBuf)            \
       float4* const sp_ = reinterpret_cast<float4*>(&smem[sb_ + 48u * (unsigned int)lane]);     \
       sp_[0] = make_float4(v_[0].x, v_[0].y, v_[1].x, v_[1].y);                                 \
       sp_[1] = make_float4(v_[2].x, v_[2].y, v_[3].x, v_[3].y);                                 \
@@ -963,14 +1001,19 @@ __device__ __forceinline__ unsigned long long r43_lpair(int i) {
       __syncwarp();                                                                             \
       float* const o_ = orow + (size_t)c * plane + (size_t)(RR) * ow;                           \
       if (full) {                                                                               \
+        _Pragma("unroll") for (int k = 0; k < 3; k++) {                                         \
+          MP_BCHK("r43f stg", (const char*)(o_ + coff[k]) - (const char*)A.out[q], 16, 0, out_bytes(A, q)) \
+        }                                                                                       \
         _Pragma("unroll") for (int k = 0; k < 3; k++)                                           \
           __stcs(reinterpret_cast<float4*>(o_ + coff[k]),                                       \
                  *reinterpret_cast<const float4*>(&smem[sb_ + 16u * (unsigned int)(lane + 32 * k)])); \
       } else {                                                                                  \
         _Pragma("unroll") for (int k = 0; k < 3; k++)                                           \
-          if (rgw + cseg[k] < nrg)                                                              \
+          if (rgw + cseg[k] < nrg) {                                                            \
+            MP_BCHK("r43f stg", (const char*)(o_ + coff[k]) - (const char*)A.out[q], 16, 0, out_bytes(A, q)) \
             __stcs(reinterpret_cast<float4*>(o_ + coff[k]),                                     \
                    *reinterpret_cast<const float4*>(&smem[sb_ + 16u * (unsigned int)(lane + 32 * k)])); \
+          }                                                                                     \
       }                                                                                         \
       __syncwarp();                                                                             \
     }                                                                                           \
@@ -1006,6 +1049,8 @@ __device__ __forceinline__ void consume_tile_r43f(const GatherArgs& A, const Til
     const int t = min(base + lane, ntask - 1);   // lanes past the tile redo its last task
     const int rg = t / ncg, cg = t - rg * ncg;
     const unsigned int a = a0 + (unsigned int)(4 * rg) * stride + 48u * (unsigned int)cg;
+    MP_BCHK("r43f box rows", 4 * rg, 4, 0, A.box_h[q])
+    MP_BCHK("r43f box cols", a0 - (soff + kDataOff) + 48u * cg, 48, 0, stride)
     float* const orow = out0 + (size_t)(3 * rgw) * ow;
     const bool full = rgw + rpw <= nrg;
     float2 X[3][6], Y[3][6];
