@@ -1067,6 +1067,148 @@ __device__ __forceinline__ void consume_tile_r43f(const GatherArgs& A, const Til
     MP_R43F_ROW(X, Y, kR43L2, 2)
   }
 }
+
+// NV12 -> f32 NCHW at an exact 4:3 downscale (NEXT-3 crops): the same tasks.
+// A task's 16 luma pixels are one 16-byte run (LDS.128) and their 8 (U, V)
+// pairs one 16-byte run of the staged chroma box (R23 siting: luma column a
+// reads chroma pair a >> 1, so output column 3k + j reads pairs (2k, 2k),
+// (2k, 2k+1), (2k+1, 2k+1) for j = 0, 1, 2).  Chroma rows: luma row a reads
+// chroma row (ya + a) >> 1 (ya = the tile's first staged luma row), so the 4
+// luma rows of a task read 2 chroma rows (ya even) or 3 (ya odd) — a
+// tile-uniform choice, two instantiations.  Every lerp, the conversion and
+// the clamp are the per-column NV12 consumer's operations in the same order
+// (bit-identical results), then the planes leave like consume_tile_r43f's.
+// Y pairs / U, V pairs: output columns (2i, 2i+1).
+#define MP_NVY_H(R_, H)                                                                         \
+  {                                                                                             \
+    MP_BCHK("r43nv lds y", R_, 16, soff + kDataOff, soff + A.stage_bytes)                       \
+    const uint4 q_ = *reinterpret_cast<const uint4*>(&smem[(R_)]);                              \
+    const uint32_t w_[4] = {q_.x, q_.y, q_.z, q_.w};                                            \
+    _Pragma("unroll") for (int i = 0; i < 6; i++) {                                             \
+      const int ca_ = 2 * i, cb_ = 2 * i + 1;                                                   \
+      const int ma_ = 4 * (ca_ / 3) + ca_ % 3, mb_ = 4 * (cb_ / 3) + cb_ % 3;                   \
+      const float2 m_ = make_float2(MP_MB(w_[ma_ >> 2], ma_ & 3), MP_MB(w_[mb_ >> 2], mb_ & 3)); \
+      const float2 n_ = make_float2(MP_MB(w_[(ma_ + 1) >> 2], (ma_ + 1) & 3),                   \
+                                    MP_MB(w_[(mb_ + 1) >> 2], (mb_ + 1) & 3));                  \
+      H[i] = ffma2_w(fsub2(n_, m_), r43_lpair(i), fsub2(m_, make_float2(8388608.0f, 8388608.0f))); \
+    }                                                                                           \
+  }
+// U (ch 0) and V (ch 1) of the 12 columns from one 16-byte chroma run
+#define MP_NVC_H(R_, H)                                                                         \
+  {                                                                                             \
+    MP_BCHK("r43nv lds uv", R_, 16, soff + kDataOff, soff + A.stage_bytes)                      \
+    const uint4 q_ = *reinterpret_cast<const uint4*>(&smem[(R_)]);                              \
+    const uint32_t w_[4] = {q_.x, q_.y, q_.z, q_.w};                                            \
+    _Pragma("unroll") for (int ch = 0; ch < 2; ch++) {                                          \
+      _Pragma("unroll") for (int i = 0; i < 6; i++) {                                           \
+        const int ca_ = 2 * i, cb_ = 2 * i + 1;                                                 \
+        const int la_ = 4 * (ca_ / 3) + ca_ % 3, lb_ = 4 * (cb_ / 3) + cb_ % 3; /* left luma taps */ \
+        const int ma_ = 2 * (la_ >> 1) + ch, mb_ = 2 * (lb_ >> 1) + ch;                         \
+        const int na_ = 2 * ((la_ + 1) >> 1) + ch, nb_ = 2 * ((lb_ + 1) >> 1) + ch;            \
+        const float2 m_ = make_float2(MP_MB(w_[ma_ >> 2], ma_ & 3), MP_MB(w_[mb_ >> 2], mb_ & 3)); \
+        const float2 n_ = make_float2(MP_MB(w_[na_ >> 2], na_ & 3), MP_MB(w_[nb_ >> 2], nb_ & 3)); \
+        H[ch][i] = ffma2_w(fsub2(n_, m_), r43_lpair(i), fsub2(m_, make_float2(8388608.0f, 8388608.0f))); \
+      }                                                                                         \
+    }                                                                                           \
+  }
+template <bool ODD>
+__device__ __forceinline__ void r43nv_task(const GatherArgs& A, unsigned int soff, unsigned int al, unsigned int ac,
+                                           unsigned int stride, float* orow, size_t plane, int ow, int lane,
+                                           unsigned int buf0, const size_t (&coff)[3], const int (&cseg)[3],
+                                           bool full, int rgw, int nrg, int q) {
+  const float2 CY = make_float2(A.cvt[0], A.cvt[0]), CYO = make_float2(A.cvt[1], A.cvt[1]);
+  const float2 CRV = make_float2(A.cvt[2], A.cvt[2]), CGU = make_float2(A.cvt[3], A.cvt[3]);
+  const float2 CGV = make_float2(A.cvt[4], A.cvt[4]), CBU = make_float2(A.cvt[5], A.cvt[5]);
+  const float2 C128 = make_float2(-128.0f, -128.0f);
+  float2 Y[4][6];
+  float2 C[ODD ? 3 : 2][2][6];
+  MP_NVY_H(al, Y[0])
+  MP_NVY_H(al + stride, Y[1])
+  MP_NVY_H(al + 2 * stride, Y[2])
+  MP_NVY_H(al + 3 * stride, Y[3])
+  MP_NVC_H(ac, C[0])
+  MP_NVC_H(ac + stride, C[1])
+  if (ODD) MP_NVC_H(ac + 2 * stride, C[ODD ? 2 : 1])
+  _Pragma("unroll") for (int r = 0; r < 3; r++) {
+    const float ly = r == 0 ? kR43L0 : (r == 1 ? kR43L1 : kR43L2);
+    // chroma rows of luma rows r and r + 1 (relative to the task's first)
+    const int ct = ODD ? (r + 1) >> 1 : r >> 1, cbt = ODD ? (r + 2) >> 1 : (r + 1) >> 1;
+    float2 v_[3][6];
+    _Pragma("unroll") for (int i = 0; i < 6; i++) {
+      float2 v0 = ffma2_s(fsub2(Y[r + 1][i], Y[r][i]), ly, Y[r][i]);
+      float2 v1 = ffma2_s(fsub2(C[cbt][0][i], C[ct][0][i]), ly, C[ct][0][i]);
+      float2 v2 = ffma2_s(fsub2(C[cbt][1][i], C[ct][1][i]), ly, C[ct][1][i]);
+      const float2 yy_ = __ffma2_rn(CY, v0, CYO);
+      const float2 uu_ = __fadd2_rn(v1, C128), vv_ = __fadd2_rn(v2, C128);
+      v0 = __ffma2_rn(CRV, vv_, yy_);
+      v1 = __ffma2_rn(CGU, uu_, __ffma2_rn(CGV, vv_, yy_));
+      v2 = __ffma2_rn(CBU, uu_, yy_);
+      v_[0][i] = make_float2(clamp255(v0.x), clamp255(v0.y));
+      v_[1][i] = make_float2(clamp255(v1.x), clamp255(v1.y));
+      v_[2][i] = make_float2(clamp255(v2.x), clamp255(v2.y));
+    }
+    _Pragma("unroll") for (int c = 0; c < 3; c++) {
+      MP_BCHK("r43nv sts", buf0 + 48u * (unsigned int)lane, 48, buf0, buf0 + kR43FBuf)
+      float4* const sp_ = reinterpret_cast<float4*>(&smem[buf0 + 48u * (unsigned int)lane]);
+      sp_[0] = make_float4(v_[c][0].x, v_[c][0].y, v_[c][1].x, v_[c][1].y);
+      sp_[1] = make_float4(v_[c][2].x, v_[c][2].y, v_[c][3].x, v_[c][3].y);
+      sp_[2] = make_float4(v_[c][4].x, v_[c][4].y, v_[c][5].x, v_[c][5].y);
+      __syncwarp();
+      float* const o_ = orow + (size_t)c * plane + (size_t)r * ow;
+      _Pragma("unroll") for (int k = 0; k < 3; k++) {
+        if (full || rgw + cseg[k] < nrg) {
+          MP_BCHK("r43nv stg", (const char*)(o_ + coff[k]) - (const char*)A.out[q], 16, 0, out_bytes(A, q))
+          __stcs(reinterpret_cast<float4*>(o_ + coff[k]),
+                 *reinterpret_cast<const float4*>(&smem[buf0 + 16u * (unsigned int)(lane + 32 * k)]));
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+__device__ __forceinline__ void consume_tile_r43nv(const GatherArgs& A, const TileHdr* hdr, unsigned int soff,
+                                                   int wid, int lane) {
+  constexpr int kCW = cw_of(MP_OUT_F32_NCHW, kSrcNV12);
+  const int2* xt = reinterpret_cast<const int2*>(&smem[soff + kHdrBytes]) + hdr->xs;
+  const int q = hdr->k, rows = hdr->rows, cols = hdr->cols;
+  const int ncg = cols / 12, nrg = rows / 3, ntask = ncg * nrg;
+  const int ow = A.ow[q], oh = A.oh[q];
+  const size_t plane = (size_t)oh * ow;
+  const unsigned int stride = (unsigned int)hdr->stride;
+  const int ya = hdr->ya;
+  // first luma tap of the tile (even: x and the tile origin are multiples of 16)
+  const unsigned int l0 = (unsigned int)(hdr->x + xt[0].x - hdr->b0);
+  const unsigned int a0 = soff + kDataOff + l0, c0 = soff + kDataOff + (unsigned int)A.uv_off[q] + l0;
+  float* const out0 = reinterpret_cast<float*>(A.out[q]) + (size_t)hdr->slot * 3 * plane +
+                      (size_t)hdr->oy0 * ow + hdr->ox0;
+  const int cps = 3 * ncg;
+  size_t coff[3];
+  int cseg[3];
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    const int c = lane + 32 * k;
+    cseg[k] = c / cps;
+    coff[k] = (size_t)(3 * cseg[k]) * ow + 4 * (c - cseg[k] * cps);
+  }
+  const unsigned int buf0 = (unsigned int)A.obuf_off + (unsigned int)wid * kR43FBuf;
+  const int rpw = 32 / ncg;
+  for (int base = 32 * wid; base < ntask; base += kCW * 32) {
+    const int rgw = base / ncg;
+    const int t = min(base + lane, ntask - 1);
+    const int rg = t / ncg, cg = t - rg * ncg;
+    const unsigned int al = a0 + (unsigned int)(4 * rg) * stride + 16u * (unsigned int)cg;
+    const int cr = ((ya + 4 * rg) >> 1) - (ya >> 1);   // chroma box row of the task's first luma row
+    const unsigned int ac = c0 + (unsigned int)cr * stride + 16u * (unsigned int)cg;
+    MP_BCHK("r43nv box rows", 4 * rg, 4, 0, A.box_h[q])
+    MP_BCHK("r43nv uv rows", cr, (ya & 1) ? 3 : 2, 0, A.box_huv[q])
+    float* const orow = out0 + (size_t)(3 * rgw) * ow;
+    const bool full = rgw + rpw <= nrg;
+    if (ya & 1) r43nv_task<true>(A, soff, al, ac, stride, orow, plane, ow, lane, buf0, coff, cseg, full, rgw, nrg, q);
+    else r43nv_task<false>(A, soff, al, ac, stride, orow, plane, ow, lane, buf0, coff, cseg, full, rgw, nrg, q);
+  }
+}
+#undef MP_NVY_H
+#undef MP_NVC_H
 #undef MP_MB
 #undef MP_R43F_H
 #undef MP_R43F_ROW
@@ -1345,6 +1487,8 @@ __global__ void __launch_bounds__((cw_of(FMT, SRC) + kProducerWarps) * 32) gathe
 #endif
       if (FMT == MP_OUT_F32_NCHW && SRC == kSrcRGB24 && A.r43[hdr->k] && (hdr->x & 15) == 0) {
         consume_tile_r43f(A, hdr, soff, wid, lane);
+      } else if (FMT == MP_OUT_F32_NCHW && SRC == kSrcNV12 && A.r43[hdr->k] && (hdr->x & 15) == 0) {
+        consume_tile_r43nv(A, hdr, soff, wid, lane);
       } else
       switch (A.ncol[hdr->k]) {
         case 2: consume_tile<FMT, 2, SRC>(A, hdr, soff, wid, lane); break;
@@ -1467,7 +1611,8 @@ static bool build_gather_args(int src, bool allow_sparse, int pitch, int W, int 
     // rows, one per consumer thread (consume_tile_r43 / _r43f): the widest column
     // group count ncg in {16, 8, 4} dividing ow / 12, then as many row groups
     // as there are consumer threads left (box within the stage budget)
-    const bool r43 = src == kSrcRGB24 && !sparse && 3 * w == 4 * ow && 3 * h == 4 * oh &&
+    const bool r43 = (src == kSrcRGB24 || (src == kSrcNV12 && fmt == MP_OUT_F32_NCHW)) && !sparse &&
+                     3 * w == 4 * ow && 3 * h == 4 * oh &&
                      ow % 12 == 0 && oh % 3 == 0 && !knob("MP_GATHER_TILE");
     if (r43) {
       // stage budget: two stages and the consumers' output-row buffers leave
@@ -1646,8 +1791,13 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
   A.wait_mode = wm ? atoi(wm) : 0;
   const char* stg = knob("MP_GATHER_STAGES");   // experiment knob
   // RGB24: three stages where they fit beside kSideReserve (f32 3 x 40 KB;
-  // u8 4:3 classes ~50 KB; larger u8 stages fall back to two below)
-  A.stages = stg ? atoi(stg) : (A.src == kSrcRGB24 ? kStagesF32 : kStages);
+  // larger stages fall back to two below).  NV12: three when every class is
+  // a fixed-tap class (~30-KB stages; c2 crops alone 1.247 -> 1.192 ms,
+  // profiles/ab/r02_nv12_r43.jsonl), else two (3 x 40 KB measured slower for
+  // the per-column NV12 consumer)
+  bool all_r43 = true;
+  for (int q = 0; q < A.k; q++) all_r43 = all_r43 && A.r43[q];
+  A.stages = stg ? atoi(stg) : ((A.src == kSrcRGB24 || all_r43) ? kStagesF32 : kStages);
   if (A.stages < 2 || A.stages > kMaxStages) A.stages = kStages;
   // fewer stages when the ring would not leave kSideReserve of the SM's shared
   // memory to the latency-bound plan / remap-NMS CTAs of neighbouring batches
