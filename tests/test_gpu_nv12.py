@@ -215,3 +215,33 @@ def test_full_size_nv12_bench_config_parity(G):
             st, o = O.gather_resize_nv12([fr], cfg.pitch_nv12, cfg.W, cfg.H, [[0, 0, 0, cfg.W, cfg.H, 0, 0]],
                                          [(cfg.W, cfg.H)], [cfg.proxy_dims], [1])
             assert np.abs(p.proxy_out[int(f)].cpu().numpy() - o[0][0]).max() <= F32_TOL
+
+
+@pytest.mark.parametrize("matrix", [0, 3])
+def test_nv12_fixed_tap_4_3_classes(G, matrix):
+    """The NV12 fixed-tap consumer (consume_tile_r43nv, f32 out): 4:3 classes
+    tiled with every column-group width (ncg 16 / 8 / 4), windows on the
+    16-px grid (fixed-tap path) and off it (per-column fallback in the same
+    launch), odd and even window y (the chroma-row parity of the task rows),
+    a full-frame class and ragged row tiles — within 1e-3 of the oracle."""
+    W, H = 960, 540
+    pitch = W
+    sizes = [(64, 64), (128, 128), (256, 256), (512, 384), (960, 540)]
+    out_dims = [(48, 48), (96, 96), (192, 192), (384, 288), (720, 405)]
+    frames = [S.frame_nv12_np(S.frame_seed(71, f), H, pitch) for f in range(2)]
+    rng = np.random.default_rng(434)
+    win = []
+    for f in range(2):
+        for q, (w, h) in enumerate(sizes):
+            xs = {0, W - w, 16 * int(rng.integers(0, (W - w) // 16 + 1)), int(rng.integers(0, W - w + 1))}
+            ys = {0, H - h, 2 * int(rng.integers(0, (H - h) // 2 + 1))}
+            if H - h >= 2:
+                ys.add(2 * int(rng.integers(0, (H - h) // 2)) + 1)   # odd y: chroma rows at the other parity
+            for x in sorted(xs):
+                for y in sorted(y for y in ys if 0 <= y <= H - h):
+                    win.append([f, x, y, w, h, q, 0])
+    win = np.array(win, np.int32)
+    for q in range(len(sizes)):
+        sel = np.nonzero(win[:, 5] == q)[0]
+        win[sel, 6] = np.arange(len(sel))
+    _compare(G, frames, pitch, W, H, win, sizes, out_dims, 0, matrix)
