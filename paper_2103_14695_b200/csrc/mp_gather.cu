@@ -822,7 +822,9 @@ constexpr int kR43FBufBytes = MP_KCW * kR43FBuf;   // one plane-row buffer per f
           const float2 m_ = make_float2(MP_B1(w_[i_ >> 2], i_ & 3), MP_B1(w_[(i_ + 12) >> 2], (i_ + 12) & 3)); \
           const float2 n_ = make_float2(MP_B1(w_[(i_ + 3) >> 2], (i_ + 3) & 3),                 \
                                         MP_B1(w_[(i_ + 15) >> 2], (i_ + 15) & 3));              \
-          H[j][c][kp] = ffma2_s(fsub2(n_, m_), lam_, m_);                                       \
+          /* lambda = 1/2 (j = 1): the unscaled sum m + n (exact); the 1/2 is  \
+             applied in the rounding of MP_R43_ROW (a power of two: exact) */   \
+          H[j][c][kp] = j == 1 ? __fadd2_rn(m_, n_) : ffma2_s(fsub2(n_, m_), lam_, m_);         \
         }                                                                                       \
       }                                                                                         \
     }                                                                                           \
@@ -830,15 +832,21 @@ constexpr int kR43FBufBytes = MP_KCW * kR43FBuf;   // one plane-row buffer per f
 // one output row (12 pixels, 36 bytes) from tap rows T, B with weight LY:
 // R16 rounding as in consume_tile_u8rgb, bytes packed 4 per word into this
 // lane's 36-byte slot of the warp's row buffer at shared byte address BUF_
-#define MP_R43_ROW(T, B, LY, BUF_)                                                              \
+// HALF: the row weight is 1/2 (output row 3m + 1) — V = T + B, the 1/2
+// joins the j = 1 columns' 1/2 in the rounding's exact power-of-two scale
+#define MP_R43_ROW(T, B, LY, HALF, BUF_)                                                        \
   {                                                                                             \
     constexpr float kRnd_ = 255.0f + 1.52587890625e-05f;                                        \
     float2 u_[3][3][2];                                                                         \
     _Pragma("unroll") for (int j = 0; j < 3; j++)                                               \
       _Pragma("unroll") for (int c = 0; c < 3; c++)                                             \
         _Pragma("unroll") for (int kp = 0; kp < 2; kp++)                                        \
-          u_[j][c][kp] = __fadd2_rd(ffma2_s(fsub2(B[j][c][kp], T[j][c][kp]), (LY), T[j][c][kp]), \
-                                    make_float2(kRnd_, kRnd_));                                 \
+        {                                                                                       \
+          const float sc_ = (j == 1 ? 0.5f : 1.0f) * ((HALF) ? 0.5f : 1.0f);                    \
+          const float2 v_ = (HALF) ? __fadd2_rn(T[j][c][kp], B[j][c][kp])                       \
+                                   : ffma2_s(fsub2(B[j][c][kp], T[j][c][kp]), (LY), T[j][c][kp]); \
+          u_[j][c][kp] = __ffma2_rd(v_, make_float2(sc_, sc_), make_float2(kRnd_, kRnd_));      \
+        }                                                                                       \
     _Pragma("unroll") for (int wi = 0; wi < 9; wi++) {                                          \
       uint32_t b_[4];                                                                           \
       _Pragma("unroll") for (int e = 0; e < 4; e++) {                                           \
@@ -928,15 +936,15 @@ __device__ __forceinline__ void consume_tile_r43(const GatherArgs& A, const Tile
     // writes
     MP_R43_H(a, X)
     MP_R43_H(a + stride, Y)
-    MP_R43_ROW(X, Y, kR43L0, buf0 + 36u * (unsigned int)lane)
+    MP_R43_ROW(X, Y, kR43L0, false, buf0 + 36u * (unsigned int)lane)
     MP_R43_OUT(0, 0)
     __syncwarp();
     MP_R43_H(a + 2 * stride, X)
-    MP_R43_ROW(Y, X, kR43L1, buf0 + 36u * (unsigned int)lane)
+    MP_R43_ROW(Y, X, kR43L1, true, buf0 + 36u * (unsigned int)lane)
     MP_R43_OUT(1, 0)
     __syncwarp();
     MP_R43_H(a + 3 * stride, Y)
-    MP_R43_ROW(X, Y, kR43L2, buf0 + 36u * (unsigned int)lane)
+    MP_R43_ROW(X, Y, kR43L2, false, buf0 + 36u * (unsigned int)lane)
     MP_R43_OUT(2, 0)
     __syncwarp();
 #undef MP_R43_OUT
