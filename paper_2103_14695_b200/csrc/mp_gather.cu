@@ -874,7 +874,7 @@ __device__ __forceinline__ void consume_tile_r43(const GatherArgs& A, const Tile
   constexpr int kCW = cw_of(MP_OUT_U8_NHWC, kSrcRGB24);
   const int2* xt = reinterpret_cast<const int2*>(&smem[soff + kHdrBytes]) + hdr->xs;
   const int q = hdr->k, rows = hdr->rows, cols = hdr->cols;
-  const int ncg = cols / 12, nrg = rows / 3, ntask = ncg * nrg;
+  const int ncg = cols / 12, nrg = rows / 3, ntask = ncg * nrg, lg = __ffs(ncg) - 1;
   const int ow = A.ow[q];
   const size_t row3 = (size_t)ow * 3;
   const unsigned int stride = (unsigned int)hdr->stride;
@@ -900,9 +900,9 @@ __device__ __forceinline__ void consume_tile_r43(const GatherArgs& A, const Tile
   const unsigned int bl = buf0 + 16u * (unsigned int)lane;
   const int rpw = 32 / ncg;   // row groups per warp
   for (int base = 32 * wid; base < ntask; base += kCW * 32) {
-    const int rgw = base / ncg;                           // first row group of this warp's tasks
+    const int rgw = base >> lg;                           // first row group of this warp's tasks
     const int t = min(base + lane, ntask - 1);            // lanes past the tile redo its last task
-    const int rg = t / ncg, cg = t - rg * ncg;
+    const int rg = t >> lg, cg = t & (ncg - 1);   // ncg is 4, 8 or 16 (host)
     const unsigned int a = a0 + (unsigned int)(4 * rg) * stride + 48u * (unsigned int)cg;
     MP_BCHK("r43 box rows", 4 * rg, 4, 0, A.box_h[q])
     MP_BCHK("r43 box cols", a0 - (soff + kDataOff) + 48u * cg, 48, 0, stride)
@@ -1032,7 +1032,7 @@ __device__ __forceinline__ void consume_tile_r43f(const GatherArgs& A, const Til
   constexpr int kCW = cw_of(MP_OUT_F32_NCHW, kSrcRGB24);
   const int2* xt = reinterpret_cast<const int2*>(&smem[soff + kHdrBytes]) + hdr->xs;
   const int q = hdr->k, rows = hdr->rows, cols = hdr->cols;
-  const int ncg = cols / 12, nrg = rows / 3, ntask = ncg * nrg;
+  const int ncg = cols / 12, nrg = rows / 3, ntask = ncg * nrg, lg = __ffs(ncg) - 1;
   const int ow = A.ow[q], oh = A.oh[q];
   const size_t plane = (size_t)oh * ow;
   const unsigned int stride = (unsigned int)hdr->stride;
@@ -1053,9 +1053,9 @@ __device__ __forceinline__ void consume_tile_r43f(const GatherArgs& A, const Til
   const unsigned int buf0 = (unsigned int)A.obuf_off + (unsigned int)wid * kR43FBuf;
   const int rpw = 32 / ncg;
   for (int base = 32 * wid; base < ntask; base += kCW * 32) {
-    const int rgw = base / ncg;
+    const int rgw = base >> lg;
     const int t = min(base + lane, ntask - 1);   // lanes past the tile redo its last task
-    const int rg = t / ncg, cg = t - rg * ncg;
+    const int rg = t >> lg, cg = t & (ncg - 1);   // ncg is 4, 8 or 16 (host)
     const unsigned int a = a0 + (unsigned int)(4 * rg) * stride + 48u * (unsigned int)cg;
     MP_BCHK("r43f box rows", 4 * rg, 4, 0, A.box_h[q])
     MP_BCHK("r43f box cols", a0 - (soff + kDataOff) + 48u * cg, 48, 0, stride)
@@ -1179,7 +1179,7 @@ __device__ __forceinline__ void consume_tile_r43nv(const GatherArgs& A, const Ti
   constexpr int kCW = cw_of(MP_OUT_F32_NCHW, kSrcNV12);
   const int2* xt = reinterpret_cast<const int2*>(&smem[soff + kHdrBytes]) + hdr->xs;
   const int q = hdr->k, rows = hdr->rows, cols = hdr->cols;
-  const int ncg = cols / 12, nrg = rows / 3, ntask = ncg * nrg;
+  const int ncg = cols / 12, nrg = rows / 3, ntask = ncg * nrg, lg = __ffs(ncg) - 1;
   const int ow = A.ow[q], oh = A.oh[q];
   const size_t plane = (size_t)oh * ow;
   const unsigned int stride = (unsigned int)hdr->stride;
@@ -1201,9 +1201,9 @@ __device__ __forceinline__ void consume_tile_r43nv(const GatherArgs& A, const Ti
   const unsigned int buf0 = (unsigned int)A.obuf_off + (unsigned int)wid * kR43FBuf;
   const int rpw = 32 / ncg;
   for (int base = 32 * wid; base < ntask; base += kCW * 32) {
-    const int rgw = base / ncg;
+    const int rgw = base >> lg;
     const int t = min(base + lane, ntask - 1);
-    const int rg = t / ncg, cg = t - rg * ncg;
+    const int rg = t >> lg, cg = t & (ncg - 1);   // ncg is 4, 8 or 16 (host)
     const unsigned int al = a0 + (unsigned int)(4 * rg) * stride + 16u * (unsigned int)cg;
     const int cr = ((ya + 4 * rg) >> 1) - (ya >> 1);   // chroma box row of the task's first luma row
     const unsigned int ac = c0 + (unsigned int)cr * stride + 16u * (unsigned int)cg;
