@@ -444,8 +444,15 @@ def run_b200(args):
                                cfg.iou_thr, fmt=fmt, device=dev, **pkw)
         p2.reserve(F, n_win, caps=counts, max_boxes=max(len(boxes), 1))
         pipes.append(p2)
+    # SMs the persistent gather leaves to the planner of the next batch (auto:
+    # 16 for u8 output on 4K grids, where the dense frames' plan, not the
+    # 4x-smaller u8 gather, bounds the step: c4 u8 2.65 -> 2.25 ms; every other
+    # line is gather-bound and loses 1-9 % with a reserve, DESIGN 6f)
+    sm_reserve = args.gather_sm_reserve if args.gather_sm_reserve >= 0 else \
+        (16 if args.fmt == "u8" and R * C >= 4096 else 0)
     runner = mp.PipelinedRunner(pipes, device=dev, merge_on_gather_stream=bool(args.merge_on_gather),
-                                side_streams=args.side_streams, plan_priority=bool(args.plan_priority))
+                                side_streams=args.side_streams, plan_priority=bool(args.plan_priority),
+                                gather_sm_reserve=sm_reserve)
     stream = torch.cuda.current_stream(dev)
     # whole-step graphs (auto: small batches, whose steps are otherwise bound
     # by the host-side issue of ~20 launches and events per step): U
@@ -597,6 +604,8 @@ def run_b200(args):
                        "parallelism": f"clip-sharded x{world}", "host_numa": numa,
                        "pipeline": f"plan/gather/merge on {1 + 2 * len(runner.s_plans)} CUDA streams, "
                                    f"{args.depth} buffer sets, "
+                                   + (f"gather leaves {runner.gather_sm_reserve} SMs to the planner, "
+                                      if runner.gather_sm_reserve else "")
                                    + (f"whole steps as CUDA graphs ({U} steps per graph launch)" if step_graph
                                       else f"plan/merge as CUDA graphs: {bool(args.graphs)}")},
             "roofline": {"bound": "hbm", "kernel": "gather_resize (prep + gather_kernel)",
@@ -1192,6 +1201,8 @@ def main():
     ap.add_argument("--no-e2e-staged", action="store_true", help="skip the whole-frame-copy e2e variant")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=3, help="batches in flight (buffer sets) in the stream pipeline")
+    ap.add_argument("--gather-sm-reserve", type=int, default=-1,
+                    help="SMs the persistent gather leaves to the co-running planner (-1 = auto, DESIGN 6f)")
     ap.add_argument("--graphs", type=int, default=1, help="replay plan/merge as CUDA graphs")
     ap.add_argument("--plan-priority", type=int, default=1, help="plan streams at the highest stream priority")
     ap.add_argument("--trace", default="", help="evidence run: write a torch.profiler (CUPTI) trace of the timed "

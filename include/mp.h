@@ -112,13 +112,15 @@ size_t mp_plan_workspace_size(const mp_plan_params* p, int32_t F);
  *  Execution: one CTA per frame; frames with <= 256 horizontal runs of
  *  positive cells are planned in shared memory by a 128-thread tier, others by
  *  a persistent 128-thread tier whose CTAs hold up to 960 runs in shared
- *  memory (~33 KB: three fit beside a persistent gather CTA on the same SM);
+ *  memory (~26 KB with int16 run / box coordinates: three fit beside a
+ *  persistent f32 gather CTA on the same SM, two beside a u8 one);
  *  frames with more runs (up to R*ceil(C/2)) are planned by a third tier
  *  whose run/component arrays live in a per-CTA global scratch slot in d_ws
  *  (same arithmetic).
  *  Limits: R*C <= 65536 cells (4K at 32 px = 8160, 8K = 32400); larger
  *  grids (and grids whose bit rows alone exceed shared memory) return
- *  MP_ERR_UNSUPPORTED.
+ *  MP_ERR_UNSUPPORTED.  (W, H <= 16384 keep every cell row / column index
+ *  within the planner's int16 run and box coordinates.)
  */
 mp_status mp_plan_windows(const mp_plan_params* p, const float* d_scores, int32_t F,
                           uint32_t* d_mask, mp_window* d_windows, int32_t max_windows,
@@ -451,6 +453,19 @@ mp_status mp_refine_tracks(const double* d_paths, const double* d_ends, int32_t 
                            int32_t C_max, int32_t W, int32_t H, double cell, int32_t k, int32_t max_cand,
                            double* d_out, int32_t* d_taken, int32_t* d_status, void* d_ws, size_t ws_bytes,
                            void* stream);
+
+/* Launch setting of the persistent gather kernels (mp_gather_resize*): leave
+ * `sms` SMs' worth of CTAs out of the grid (process-wide, read at every
+ * subsequent gather launch from any host thread; default 0 = one wave of
+ * resident CTAs on every SM).  A gather CTA leaves room beside it for only one
+ * or two latency-bound planner CTAs (mp_plan_windows of the next batch, run on
+ * another stream), which then issue at a fraction of their solo rate; SMs left
+ * free take several planner CTAs at full rate.  Worth it only when the plan,
+ * not the gather, bounds a pipelined step (4K dense frames with u8 output:
+ * DESIGN.md 6f); it lengthens every other gather.
+ *  0 <= sms <= 1024, else MP_ERR_INVALID (the setting is unchanged).  Launches
+ *  nothing; the grid is clamped to at least one SM. */
+mp_status mp_gather_set_sm_reserve(int32_t sms);
 
 /* Human-readable name of a status code (static string, never NULL). */
 const char* mp_status_string(mp_status st);

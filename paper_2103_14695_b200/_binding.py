@@ -55,6 +55,8 @@ def _load():
     L.mp_status_string.argtypes = [C.c_int]
     L.mp_launches_per_call.restype = i32
     L.mp_launches_per_call.argtypes = [i32]
+    L.mp_gather_set_sm_reserve.restype = C.c_int
+    L.mp_gather_set_sm_reserve.argtypes = [i32]
     L.mp_plan_workspace_size.restype = sz
     L.mp_plan_workspace_size.argtypes = [C.POINTER(mp_plan_params), i32]
     L.mp_plan_windows.restype = C.c_int
@@ -106,7 +108,8 @@ _lib = _load()
 EXPORTED = ("mp_plan_workspace_size", "mp_plan_windows", "mp_gather_workspace_size", "mp_gather_resize",
             "mp_gather_resize_strided", "mp_proxy_sweep_workspace_size", "mp_proxy_sweep",
             "mp_window_set_cost",
-            "mp_remap_nms_workspace_size", "mp_remap_nms", "mp_status_string", "mp_launches_per_call")
+            "mp_remap_nms_workspace_size", "mp_remap_nms", "mp_status_string", "mp_launches_per_call",
+            "mp_gather_set_sm_reserve")
 
 
 def lib():
@@ -119,6 +122,14 @@ def status_string(code: int) -> str:
 
 def launches_per_call(which: int) -> int:
     return int(_lib.mp_launches_per_call(which))
+
+
+def mp_gather_set_sm_reserve(sms: int) -> None:
+    """Process-wide launch setting of the persistent gather: SMs left out of
+    its grid for co-running planner CTAs (mp.h; 0 = every SM)."""
+    st = _lib.mp_gather_set_sm_reserve(int(sms))
+    if st != MP_OK:
+        raise MPError(st, "mp_gather_set_sm_reserve")
 
 
 def _p(t) -> C.c_void_p:

@@ -260,6 +260,14 @@ extern __shared__ __align__(128) unsigned char smem[];
 // Experiment knobs (MP_GATHER_BUDGET_KB, _TILE, _WAIT, _STAGES, _DEBUG) are
 // read from the environment only in builds with -DMP_EXPERIMENT_KNOBS (the
 // dev sweeps of scripts/time_gather.py); the production library ignores them.
+static std::atomic<int> g_sm_reserve{0};   // mp_gather_set_sm_reserve
+
+extern "C" mp_status mp_gather_set_sm_reserve(int32_t sms) {
+  if (sms < 0 || sms > 1024) return MP_ERR_INVALID;
+  g_sm_reserve.store(sms, std::memory_order_relaxed);
+  return MP_OK;
+}
+
 static inline const char* knob(const char* name) {
 #ifdef MP_EXPERIMENT_KNOBS
   return getenv(name);
@@ -1873,7 +1881,10 @@ static mp_status gather_launch(GatherArgs& A, const TmapArray& tm, const uint8_t
       if (per_sm < 1) per_sm = 1;
       if (occ_n < 32) occ_cache[occ_n++] = Occ{(const void*)kern, dev, smem, per_sm};
     }
-    kern<<<sms * per_sm, threads, smem, s>>>(A, tm, d_frame_ptrs, ws_cnt, ws_list, d_windows, d_frame_off, ws_tap,
+    // mp_gather_set_sm_reserve: SMs left to the co-running planner
+    const int rsv = g_sm_reserve.load(std::memory_order_relaxed);
+    const int gsms = rsv < sms ? sms - rsv : 1;
+    kern<<<gsms * per_sm, threads, smem, s>>>(A, tm, d_frame_ptrs, ws_cnt, ws_list, d_windows, d_frame_off, ws_tap,
                                              d_status);
     MP_CUDA_TRY(cudaGetLastError());
     return MP_OK;

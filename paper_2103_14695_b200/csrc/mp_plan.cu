@@ -78,9 +78,29 @@ __device__ __forceinline__ void uf_unite(int* parent, int a, int b) {
   }
 }
 
+// 16-bit min (kMax = false) / max of a non-negative value into a shared or
+// global int16 entry: a CAS loop on the aligned 32-bit word holding it (there
+// are no 16-bit atomicMin / atomicMax); the neighbouring entry of the word is
+// carried through unchanged.
+template <bool kMax>
+__device__ __forceinline__ void atomic_minmax_s16(short* p, int v) {
+  unsigned* w = (unsigned*)((size_t)p & ~(size_t)3);
+  const int sh = ((size_t)p & 2) ? 16 : 0;
+  unsigned old = *(volatile unsigned*)w;
+  while (true) {
+    const int cur = (short)(old >> sh);
+    if (kMax ? cur >= v : cur <= v) return;
+    const unsigned nv = (old & ~(0xFFFFu << sh)) | ((unsigned)(v & 0xFFFF) << sh);
+    const unsigned prev = atomicCAS(w, old, nv);
+    if (prev == old) return;
+    old = prev;
+  }
+}
+
 struct PlanSmem {
   uint32_t* bits;
-  int *row_off, *tmp, *parent, *cid, *bc0, *br0, *bc1, *br1, *run;
+  int *row_off, *tmp, *parent, *cid, *run;
+  short *bc0, *br0, *bc1, *br1;   // component boxes in cells (int16 like the runs: half the bytes)
   short *rrow, *rcs, *rce;
   unsigned char *csz, *memb;
 };
@@ -102,10 +122,10 @@ __host__ __device__ inline size_t plan_smem_bytes(int R, int words, int maxc, Pl
   // appends a merged cluster before it compacts (coop_merge, cap = maxc + 1)
   s.parent = (int*)take(sizeof(int) * (maxc + 1));
   s.cid = (int*)take(sizeof(int) * (maxc + 1));
-  s.bc0 = (int*)take(sizeof(int) * (maxc + 1));
-  s.br0 = (int*)take(sizeof(int) * (maxc + 1));
-  s.bc1 = (int*)take(sizeof(int) * (maxc + 1));
-  s.br1 = (int*)take(sizeof(int) * (maxc + 1));
+  s.bc0 = (short*)take(sizeof(short) * (maxc + 1));
+  s.br0 = (short*)take(sizeof(short) * (maxc + 1));
+  s.bc1 = (short*)take(sizeof(short) * (maxc + 1));
+  s.br1 = (short*)take(sizeof(short) * (maxc + 1));
   s.rrow = (short*)take(sizeof(short) * maxc);
   s.rcs = (short*)take(sizeof(short) * maxc);
   s.rce = (short*)take(sizeof(short) * maxc);
@@ -118,10 +138,11 @@ __host__ __device__ inline size_t plan_smem_bytes(int R, int words, int maxc, Pl
 constexpr int kPlanThreads = 128;      // full-capacity tier (128 threads: two CTAs fit beside a gather CTA)
 constexpr int kFastThreads = 128;      // fast tier: frames with <= kFastCap runs
 constexpr int kFastCap = 256;
-// full tier: runs held in shared memory (~32 KB at 960 runs + ~1.5 KB
-// static: three CTAs fit in the ~108 KB a c4 gather CTA leaves of an SM, so
-// all 300 frames of a c4 batch plan in one wave beside the gather); beyond
-// -> the huge tier (global scratch).  c4 (4K, 68 x 120 cells) frames have
+// full tier: runs held in shared memory (~24 KB at 960 runs with int16
+// component boxes + ~1.5 KB static: three CTAs fit in the ~108 KB a c4 f32
+// gather CTA leaves of an SM and two in the ~55 KB beside the u8 ring, so all
+// 300 frames of a c4 batch plan in one wave beside the gather); beyond -> the
+// huge tier (global scratch).  c4 (4K, 68 x 120 cells) frames have
 // 756-888 runs.
 constexpr int kMidCap = 960;
 // largest cell grid: the fast / full tiers keep only the bit rows and run
@@ -523,19 +544,22 @@ __device__ __forceinline__ bool plan_frame(const PlanArgs& P, int f, int cap, co
   for (int u = tid; u < nruns; u += blockDim.x) S.cid[u] = (S.parent[u] == u) ? 1 : 0;
   __syncthreads();
   const int ncomp = block_excl_scan_smem(S.cid, nruns, S.tmp);
+  // a component's root is its first run in row-major order, so its top row
+  // is the root's row (plain store); the other three sides are 16-bit
+  // min / max updates (CAS on the 32-bit word holding the entry)
   for (int q = tid; q < ncomp; q += blockDim.x) {
-    S.bc0[q] = INT_MAX;
-    S.br0[q] = INT_MAX;
+    S.bc0[q] = SHRT_MAX;
     S.bc1[q] = -1;
     S.br1[q] = -1;
   }
   __syncthreads();
   for (int u = tid; u < nruns; u += blockDim.x) {
-    const int q = S.cid[S.parent[u]];
-    atomicMin(&S.bc0[q], (int)S.rcs[u]);
-    atomicMax(&S.bc1[q], (int)S.rce[u]);
-    atomicMin(&S.br0[q], (int)S.rrow[u]);
-    atomicMax(&S.br1[q], (int)S.rrow[u]);
+    const int root = S.parent[u];
+    const int q = S.cid[root];
+    if (root == u) S.br0[q] = S.rrow[u];
+    atomic_minmax_s16<false>(&S.bc0[q], S.rcs[u]);
+    atomic_minmax_s16<true>(&S.bc1[q], S.rce[u]);
+    atomic_minmax_s16<true>(&S.br1[q], S.rrow[u]);
   }
   __syncthreads();
   for (int q = tid; q < ncomp; q += blockDim.x) {
@@ -989,6 +1013,7 @@ static bool build_plan_args(const mp_plan_params* p, PlanArgs* A, mp_status* err
   A->k = p->k;
   A->full = full;
   A->b = p->b_proxy;
+  // (W, H <= 16384: cell rows / columns fit the planner's int16 runs and boxes)
   if ((long long)A->R * A->C > kMaxCells) {
     *err = MP_ERR_UNSUPPORTED;
     return false;

@@ -24,12 +24,23 @@ def main():
     frames = S.frame_pixels_torch([S.frame_seed(0, f) for f in range(F)], cfg.H, cfg.pitch, device=dev)
     pipes = []
     R, C = cfg.grid
+    fmt = int(os.environ.get("FMT", "0"))   # 0 f32 NCHW, 1 u8 NHWC
     p0 = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr, cfg.iou_thr,
-                           device=dev)
+                           fmt=fmt, device=dev)
     p0.reserve(F, F * R * ((C + 1) // 2))
     p0.plan(scores)
     torch.cuda.synchronize()
     n = int(p0.frame_off[F].item())
+    # the plan alone (nothing co-running): median of 20
+    ts = []
+    for _ in range(20):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        p0.plan(scores)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    print(f"plan alone: {sorted(ts)[10]:.3f} ms")
     caps = p0.class_count.cpu().tolist()
     w = p0.windows[:n].cpu().numpy()
     boxes, wbo = S.standin_boxes(cfg, 0, scene, w)
@@ -37,7 +48,7 @@ def main():
     wt = torch.from_numpy(wbo).to(dev)
     for _ in range(depth):
         p = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr,
-                              cfg.iou_thr, device=dev)
+                              cfg.iou_thr, fmt=fmt, device=dev)
         p.reserve(F, n, caps=caps, max_boxes=len(boxes))
         pipes.append(p)
     run = mp.PipelinedRunner(pipes, device=dev, merge_on_gather_stream=bool(int(os.environ.get("MOG", "0"))))

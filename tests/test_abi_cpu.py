@@ -63,6 +63,16 @@ def test_workspace_queries(lib):
     assert lib.mp_remap_nms_workspace_size(100, 1000) >= 1000 * 28
 
 
+def test_gather_sm_reserve_setting(lib):
+    """mp_gather_set_sm_reserve validates its range on the host (no launch)."""
+    for bad in (-1, 1025):
+        with pytest.raises(lib.MPError) as e:
+            lib.mp_gather_set_sm_reserve(bad)
+        assert e.value.code == lib.MP_ERR_INVALID
+    lib.mp_gather_set_sm_reserve(16)
+    lib.mp_gather_set_sm_reserve(0)
+
+
 def test_invalid_host_params_rejected_before_launch(lib):
     """MP_ERR_INVALID is returned synchronously, before any CUDA call (so it
     works without a GPU)."""

@@ -63,15 +63,19 @@ def _check_batch(cfg, inp, snap, rng, n_pix=6):
         assert np.abs(snap["outs"][q][slot].astype(np.float64) - o[q][0]).max() <= F32_TOL, (wi, q)
 
 
-@pytest.mark.parametrize("graphs", [False, True], ids=["eager", "graphs"])
+@pytest.mark.parametrize("graphs,reserve", [(False, 0), (True, 0), (False, 16), (True, 140)],
+                         ids=["eager", "graphs", "eager-reserve16", "graphs-reserve140"])
 @pytest.mark.parametrize("depth", [2, 3])
-def test_runner_new_inputs_every_batch(G, graphs, depth):
+def test_runner_new_inputs_every_batch(G, graphs, reserve, depth, request):
     """Batches from 3 different clips in rotation, each batch's inputs copied
     H2D (non_blocking, pinned) into NEW tensors on the caller's stream and
     released right after the call; each batch's results are snapshotted on a
     reader stream that waits for its merge.  Every snapshot equals the
-    oracle for its own clip."""
+    oracle for its own clip (also with the gather leaving SMs to the
+    planner: mp_gather_set_sm_reserve 16, and 140 of 148 — an 8-CTA grid
+    that must still cover every tile)."""
     import paper_2103_14695_b200 as mp
+    request.addfinalizer(lambda: mp.mp_gather_set_sm_reserve(0))
     cfg = S.CONFIGS["c1_540p"]
     F = cfg.frames
     clips = [_clip_inputs(cfg, c, F) for c in (11, 12, 13)]
@@ -84,7 +88,7 @@ def test_runner_new_inputs_every_batch(G, graphs, depth):
                               cfg.iou_thr, device=G.DEV)
         p.reserve(F, n_max + 4, caps=caps, max_boxes=nb)
         pipes.append(p)
-    runner = mp.PipelinedRunner(pipes, device=G.DEV)
+    runner = mp.PipelinedRunner(pipes, device=G.DEV, gather_sm_reserve=reserve)
 
     def pad_boxes(c):
         b = np.zeros((nb, 6), np.float32)
