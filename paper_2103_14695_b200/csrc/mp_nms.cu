@@ -32,7 +32,13 @@ struct NmsArgs {
   int ow[kMaxClasses], oh[kMaxClasses];
 };
 
-constexpr int kSmallCap = 512, kSmallMaskCap = 128, kSmallThreads = 128;
+#ifndef MP_NMS_SMALL_CAP   // (dev A/B builds may override the small tier's geometry)
+#define MP_NMS_SMALL_CAP 512
+#endif
+#ifndef MP_NMS_SMALL_MINB
+#define MP_NMS_SMALL_MINB 1
+#endif
+constexpr int kSmallCap = MP_NMS_SMALL_CAP, kSmallMaskCap = 128, kSmallThreads = 128;
 // Every tier's CTA fits in what the persistent gather CTA leaves of an SM
 // (<= 54 KB of shared memory = kSideReserve in mp_gather.cu, <= 16K registers), so the
 // remap/NMS of batch i-1 runs beside gather(i) instead of queueing behind it
@@ -705,7 +711,10 @@ __device__ __forceinline__ bool frame_range(const NmsArgs& A, int f, const int* 
   return b_lo >= 0 && b_hi >= b_lo && b_hi <= A.max_boxes;
 }
 
-constexpr int kTinyCap = 64, kTinyWarps = 8;
+#ifndef MP_NMS_TINY_WARPS
+#define MP_NMS_TINY_WARPS 8
+#endif
+constexpr int kTinyCap = 64, kTinyWarps = MP_NMS_TINY_WARPS;
 
 struct TinyWarpSmem {
   float4 bx[kTinyCap];
@@ -830,7 +839,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) nms_tiny_kernel(NmsArgs A, co
 }
 
 // Queued frames with 65..512 raw boxes, one CTA per frame (persistent).
-__global__ void __launch_bounds__(kSmallThreads) nms_small_kernel(NmsArgs A, const mp_box* __restrict__ boxes,
+__global__ void __launch_bounds__(kSmallThreads, MP_NMS_SMALL_MINB) nms_small_kernel(NmsArgs A, const mp_box* __restrict__ boxes,
                                                                   const int* __restrict__ win_box_off,
                                                                   const mp_window* __restrict__ windows,
                                                                   const int* __restrict__ frame_off,
