@@ -13,7 +13,18 @@
 namespace mpk {
 
 constexpr int kMaxClasses = 16;
-constexpr int kScanThreads = 256;   // single-CTA CSR scans of the plan / NMS
+// 128 threads capped at 64 registers (8 K): the plan's scan then fits beside a
+// persistent f32 gather CTA and its co-running side CTAs and finishes before
+// the gather does (256 threads waited for the gather to end: c2 f32 step
+// 1.430 -> 1.414 ms, DESIGN 6f); dev A/B builds may override.
+#ifndef MP_SCAN_THREADS
+#define MP_SCAN_THREADS 128
+#endif
+#ifndef MP_SCAN_MINB
+#define MP_SCAN_MINB 8
+#endif
+constexpr int kScanThreads = MP_SCAN_THREADS;   // single-CTA CSR scans of the plan / NMS
+constexpr int kScanMinBlocks = MP_SCAN_MINB;    // (register cap via __launch_bounds__)
 
 // ----------------------------------------------------------------- status
 __device__ __forceinline__ void set_status(int32_t* d_status, int32_t code) {
@@ -84,12 +95,23 @@ __device__ __forceinline__ int block_excl_scan_smem(int* a, int n, int* tmp) {
 
 // Block-wide exclusive scan over a strided global int sequence
 // a[0], a[stride], ... (n items) in place; returns the total.  One CTA.
+// Each thread owns a contiguous run of items and reads it in batches of
+// kScanBatch independent loads (one memory latency per batch, not per item:
+// the single-CTA scans sit on the pipeline's critical path between two
+// gathers).
+constexpr int kScanBatch = 8;
 __device__ __forceinline__ int block_scan_global(int* a, int n, int stride, int* tmp) {
   const int nt = blockDim.x, tid = threadIdx.x;
   const int per = (n + nt - 1) / nt;
   const int lo = min(n, tid * per), hi = min(n, lo + per);
   int s = 0;
-  for (int i = lo; i < hi; i++) s += a[(size_t)i * stride];
+  for (int i0 = lo; i0 < hi; i0 += kScanBatch) {
+    int v[kScanBatch];
+#pragma unroll
+    for (int j = 0; j < kScanBatch; j++) v[j] = i0 + j < hi ? a[(size_t)(i0 + j) * stride] : 0;
+#pragma unroll
+    for (int j = 0; j < kScanBatch; j++) s += v[j];
+  }
   const int lane = tid & 31, wid = tid >> 5, nw = (nt + 31) >> 5;
   int inc = warp_incl_scan(s);
   if (lane == 31) tmp[wid] = inc;
@@ -102,10 +124,16 @@ __device__ __forceinline__ int block_scan_global(int* a, int n, int stride, int*
   }
   __syncthreads();
   int run = tmp[wid] + inc - s;
-  for (int i = lo; i < hi; i++) {
-    int v = a[(size_t)i * stride];
-    a[(size_t)i * stride] = run;
-    run += v;
+  for (int i0 = lo; i0 < hi; i0 += kScanBatch) {
+    int v[kScanBatch];
+#pragma unroll
+    for (int j = 0; j < kScanBatch; j++) v[j] = i0 + j < hi ? a[(size_t)(i0 + j) * stride] : 0;
+#pragma unroll
+    for (int j = 0; j < kScanBatch; j++)
+      if (i0 + j < hi) {
+        a[(size_t)(i0 + j) * stride] = run;
+        run += v[j];
+      }
   }
   int total = tmp[32];
   __syncthreads();

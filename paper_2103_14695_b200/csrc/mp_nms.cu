@@ -892,7 +892,7 @@ __global__ void __launch_bounds__(kLargeThreads) nms_large_kernel(NmsArgs A, con
 
 // 256 threads (not 1024): a 1024-thread CTA needs ~32 K registers, more than a
 // persistent gather CTA leaves of an SM, and would wait for the gather to end.
-__global__ void __launch_bounds__(kScanThreads) nms_scan_kernel(int F, const int* __restrict__ ws_kept,
+__global__ void __launch_bounds__(kScanThreads, kScanMinBlocks) nms_scan_kernel(int F, const int* __restrict__ ws_kept,
                                                         int* __restrict__ out_frame_off, int max_out,
                                                         int* __restrict__ d_status) {
   __shared__ int tmp[40];

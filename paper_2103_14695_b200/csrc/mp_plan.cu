@@ -770,9 +770,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_huge_kernel(PlanArgs P, con
   }
 }
 
-// 256 threads (not 1024): a 1024-thread CTA needs ~32 K registers, more than a
-// persistent gather CTA leaves of an SM, and would wait for the gather to end.
-__global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(int F, int k, int* __restrict__ ws_count,
+// kScanThreads (128, not 1024): a 1024-thread CTA needs ~32 K registers, more
+// than a persistent gather CTA leaves of an SM, and would wait for the gather
+// to end (so did 256 threads beside an f32 gather and its side CTAs).
+__global__ void __launch_bounds__(kScanThreads, kScanMinBlocks) plan_scan_kernel(int F, int k, int* __restrict__ ws_count,
                                                          int* __restrict__ ws_cls, int* __restrict__ frame_off,
                                                          int* __restrict__ class_count, int max_windows,
                                                          int* __restrict__ d_status) {

@@ -217,13 +217,15 @@ class PipelinedRunner:
     """
 
     def __init__(self, pipes, device="cuda", merge_on_gather_stream: bool = False, side_streams: int = 1,
-                 plan_priority: bool = True, gather_sm_reserve: int = 0):
+                 plan_priority: bool = True, gather_sm_reserve: Optional[int] = None):
         self.pipes = list(pipes)
         # SMs the persistent gather leaves to the co-running planner of the
-        # next batch (mp_gather_set_sm_reserve; process-wide, set once here):
-        # only for plan-bound steps (4K dense frames, u8 output, DESIGN 6f)
-        self.gather_sm_reserve = int(gather_sm_reserve)
-        B.mp_gather_set_sm_reserve(self.gather_sm_reserve)
+        # next batch (mp_gather_set_sm_reserve, a process-wide launch setting,
+        # set here when given; None leaves it as it is): only for plan-bound
+        # steps (4K dense frames, u8 output, DESIGN 6f)
+        self.gather_sm_reserve = gather_sm_reserve
+        if gather_sm_reserve is not None:
+            B.mp_gather_set_sm_reserve(int(gather_sm_reserve))
         self.depth = len(self.pipes)
         self.dev = torch.device(device)
         dev = self.dev
