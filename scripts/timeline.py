@@ -25,6 +25,7 @@ def main():
     pipes = []
     R, C = cfg.grid
     fmt = int(os.environ.get("FMT", "0"))   # 0 f32 NCHW, 1 u8 NHWC
+    mp.mp_gather_set_sm_reserve(int(os.environ.get("RSV", "0")))   # SMs the gather leaves free
     p0 = mp.WindowPipeline(cfg.W, cfg.H, cfg.sizes, cfg.cost, cfg.out_dims, cfg.b_proxy, cfg.score_thr, cfg.iou_thr,
                            fmt=fmt, device=dev)
     p0.reserve(F, F * R * ((C + 1) // 2))
