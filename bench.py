@@ -444,12 +444,14 @@ def run_b200(args):
                                cfg.iou_thr, fmt=fmt, device=dev, **pkw)
         p2.reserve(F, n_win, caps=counts, max_boxes=max(len(boxes), 1))
         pipes.append(p2)
-    # SMs the persistent gather leaves to the planner of the next batch (auto:
-    # 16 for u8 output on 4K grids, where the dense frames' plan, not the
-    # 4x-smaller u8 gather, bounds the step: c4 u8 2.65 -> 2.25 ms; every other
-    # line is gather-bound and loses 1-9 % with a reserve, DESIGN 6f)
+    # SMs the persistent gather leaves to the side kernels (auto, DESIGN 6f):
+    # u8 output on 4K grids 16 (the dense frames' plan, not the 4x-smaller u8
+    # gather, bounds the step: c4 u8 2.65 -> 2.21-2.28 ms); other u8 lines 1
+    # (the plan's scan / scatter and the NMS tiny tier cannot co-reside with a
+    # u8 gather CTA and otherwise run between two gathers: c2 u8 0.803 ->
+    # 0.772 ms); f32 0 (they co-reside; a reserve only costs gather SMs)
     sm_reserve = args.gather_sm_reserve if args.gather_sm_reserve >= 0 else \
-        (16 if args.fmt == "u8" and R * C >= 4096 else 0)
+        (0 if args.fmt != "u8" else 16 if R * C >= 4096 else 1)
     runner = mp.PipelinedRunner(pipes, device=dev, merge_on_gather_stream=bool(args.merge_on_gather),
                                 side_streams=args.side_streams, plan_priority=bool(args.plan_priority),
                                 gather_sm_reserve=sm_reserve)
@@ -604,7 +606,7 @@ def run_b200(args):
                        "parallelism": f"clip-sharded x{world}", "host_numa": numa,
                        "pipeline": f"plan/gather/merge on {1 + 2 * len(runner.s_plans)} CUDA streams, "
                                    f"{args.depth} buffer sets, "
-                                   + (f"gather leaves {runner.gather_sm_reserve} SMs to the planner, "
+                                   + (f"gather leaves {runner.gather_sm_reserve} SMs to the side kernels, "
                                       if runner.gather_sm_reserve else "")
                                    + (f"whole steps as CUDA graphs ({U} steps per graph launch)" if step_graph
                                       else f"plan/merge as CUDA graphs: {bool(args.graphs)}")},
@@ -720,7 +722,10 @@ def run_clips(args):
                                    fmt=fmt, device=dev)
             pp.reserve(F, max(max(n_win), 1), caps=caps, max_boxes=nb)
             pipes.append(pp)
-        runner = mp.PipelinedRunner(pipes, device=dev)
+        Rg, Cg = cfg.grid
+        runner = mp.PipelinedRunner(pipes, device=dev, gather_sm_reserve=args.gather_sm_reserve
+                                    if args.gather_sm_reserve >= 0 else
+                                    (0 if args.fmt != "u8" else 16 if Rg * Cg >= 4096 else 1))
         for i in range(min(args.warmup, len(mine)) or 1):
             e = mine[i % len(mine)] % P if mine else 0
             runner.step(scores[e], frames, *det[e])

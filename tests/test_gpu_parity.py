@@ -470,8 +470,8 @@ def test_pipelined_runner_with_graphs_parity(G, depth):
 def test_full_size_pipelined_parity(G, name, fmt, request):
     """configs[2] and configs[3] at full size in the launch configuration
     bench.py times for them (PipelinedRunner: 3 streams, 3 buffer sets,
-    plan/merge as CUDA graphs, several steps; c4 u8 with the gather leaving
-    16 SMs to the planner, bench.py's auto rule): windows and kept boxes
+    plan/merge as CUDA graphs, several steps; u8 with the gather leaving 1
+    SM (c4: 16) to the side kernels, bench.py's auto rule): windows and kept boxes
     bit-exact against the oracle, pixels on a seeded sample of windows
     (f32 within 1e-3, u8 within 1 LSB)."""
     import paper_2103_14695_b200 as mp
@@ -492,7 +492,7 @@ def test_full_size_pipelined_parity(G, name, fmt, request):
                               cfg.iou_thr, fmt=fmt, device=G.DEV)
         p.reserve(F, n, caps=caps, max_boxes=max(len(boxes), 1))
         pipes.append(p)
-    reserve = 16 if fmt == 1 and name == "c4_4k_drone" else 0
+    reserve = 0 if fmt == 0 else 16 if name == "c4_4k_drone" else 1   # bench.py's auto rule
     request.addfinalizer(lambda: mp.mp_gather_set_sm_reserve(0))
     runner = mp.PipelinedRunner(pipes, device=G.DEV, gather_sm_reserve=reserve)
     sc = torch.from_numpy(scores).to(G.DEV)
@@ -572,11 +572,11 @@ def test_gather_zero_windows_and_repeated_calls(G):
 
 
 @pytest.mark.parametrize("fmt", [0, 1], ids=["f32", "u8"])
-def test_full_size_c2_bench_launch_config_every_window(G, fmt):
+def test_full_size_c2_bench_launch_config_every_window(G, fmt, request):
     """configs[1] (the bench workload: 1800 x 1080p frames) in exactly the
     launch configuration bench.py times — PipelinedRunner, 3 buffer sets, 3
     streams, plan/merge replayed as CUDA graphs over the runner's static
-    inputs, several steps — with EVERY window's pixels compared against the
+    inputs, u8 with one SM left to the side kernels, several steps — with EVERY window's pixels compared against the
     oracle (run frame-parallel over the host's cores in chunks of frames;
     slots of a chunk are contiguous per class), plus windows, CSR, masks-free
     plan outputs and kept boxes bit-exact."""
@@ -600,7 +600,8 @@ def test_full_size_c2_bench_launch_config_every_window(G, fmt):
                               cfg.iou_thr, fmt=fmt, device=G.DEV)
         p.reserve(F, n, caps=caps, max_boxes=max(len(boxes), 1))
         pipes.append(p)
-    runner = mp.PipelinedRunner(pipes, device=G.DEV)
+    request.addfinalizer(lambda: mp.mp_gather_set_sm_reserve(0))
+    runner = mp.PipelinedRunner(pipes, device=G.DEV, gather_sm_reserve=1 if fmt == 1 else 0)   # bench's auto rule
     frames = S.frame_pixels_torch([S.frame_seed(clip, f) for f in range(F)], cfg.H, cfg.pitch, device=G.DEV)
     runner.capture_graphs(torch.from_numpy(scores).to(G.DEV), G.boxes_to_t(boxes), torch.from_numpy(wbo).to(G.DEV))
     for _ in range(4):
