@@ -457,12 +457,14 @@ mp_status mp_refine_tracks(const double* d_paths, const double* d_ends, int32_t 
 /* Launch setting of the persistent gather kernels (mp_gather_resize*): leave
  * `sms` SMs' worth of CTAs out of the grid (process-wide, read at every
  * subsequent gather launch from any host thread; default 0 = one wave of
- * resident CTAs on every SM).  A gather CTA leaves room beside it for only one
- * or two latency-bound planner CTAs (mp_plan_windows of the next batch, run on
- * another stream), which then issue at a fraction of their solo rate; SMs left
- * free take several planner CTAs at full rate.  Worth it only when the plan,
- * not the gather, bounds a pipelined step (4K dense frames with u8 output:
- * DESIGN.md 6f); it lengthens every other gather.
+ * resident CTAs on every SM).  A u8 gather CTA leaves room beside it for only
+ * one or two latency-bound planner CTAs (mp_plan_windows of the next batch, run
+ * on another stream), which then issue at a fraction of their solo rate, and
+ * none for the plan's single-CTA scan or the smallest remap/NMS tier, which
+ * then wait for the gather to end; SMs left free run them at full rate.  Worth
+ * it when those side kernels, not the gather, bound a pipelined step (u8
+ * output: 1 SM, 16 on 4K dense frames — DESIGN.md 6f); it costs the gather
+ * the SMs it leaves (f32: no gain).
  *  0 <= sms <= 1024, else MP_ERR_INVALID (the setting is unchanged).  Launches
  *  nothing; the grid is clamped to at least one SM. */
 mp_status mp_gather_set_sm_reserve(int32_t sms);
