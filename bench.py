@@ -606,7 +606,7 @@ def run_b200(args):
                        "parallelism": f"clip-sharded x{world}", "host_numa": numa,
                        "pipeline": f"plan/gather/merge on {1 + 2 * len(runner.s_plans)} CUDA streams, "
                                    f"{args.depth} buffer sets, "
-                                   + (f"gather leaves {runner.gather_sm_reserve} SMs to the side kernels, "
+                                   + (f"gather leaves {runner.gather_sm_reserve} SM(s) to the side kernels, "
                                       if runner.gather_sm_reserve else "")
                                    + (f"whole steps as CUDA graphs ({U} steps per graph launch)" if step_graph
                                       else f"plan/merge as CUDA graphs: {bool(args.graphs)}")},
