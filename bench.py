@@ -36,6 +36,19 @@ from workloads import synth as S  # noqa: E402
 
 
 # --------------------------------------------------------------------------- shared helpers
+
+def gather_sm_reserve(args, R: int, C: int) -> int:
+    """SMs the persistent gather leaves to the side kernels (--gather-sm-reserve,
+    -1 = auto, DESIGN 6f): u8 output 1 (the plan's single-CTA scan and the NMS
+    tiny tier cannot co-reside with a u8 gather CTA), 16 on 4K grids (the dense
+    frames' plan bounds the step); f32 / NV12 0."""
+    if args.gather_sm_reserve >= 0:
+        return args.gather_sm_reserve
+    if args.fmt != "u8":
+        return 0
+    return 16 if R * C >= 4096 else 1
+
+
 def host_cpu_desc():
     model = "unknown"
     try:
@@ -450,8 +463,7 @@ def run_b200(args):
     # (the plan's scan / scatter and the NMS tiny tier cannot co-reside with a
     # u8 gather CTA and otherwise run between two gathers: c2 u8 0.803 ->
     # 0.772 ms); f32 0 (they co-reside; a reserve only costs gather SMs)
-    sm_reserve = args.gather_sm_reserve if args.gather_sm_reserve >= 0 else \
-        (0 if args.fmt != "u8" else 16 if R * C >= 4096 else 1)
+    sm_reserve = gather_sm_reserve(args, R, C)
     runner = mp.PipelinedRunner(pipes, device=dev, merge_on_gather_stream=bool(args.merge_on_gather),
                                 side_streams=args.side_streams, plan_priority=bool(args.plan_priority),
                                 gather_sm_reserve=sm_reserve)
@@ -722,10 +734,7 @@ def run_clips(args):
                                    fmt=fmt, device=dev)
             pp.reserve(F, max(max(n_win), 1), caps=caps, max_boxes=nb)
             pipes.append(pp)
-        Rg, Cg = cfg.grid
-        runner = mp.PipelinedRunner(pipes, device=dev, gather_sm_reserve=args.gather_sm_reserve
-                                    if args.gather_sm_reserve >= 0 else
-                                    (0 if args.fmt != "u8" else 16 if Rg * Cg >= 4096 else 1))
+        runner = mp.PipelinedRunner(pipes, device=dev, gather_sm_reserve=gather_sm_reserve(args, *cfg.grid))
         for i in range(min(args.warmup, len(mine)) or 1):
             e = mine[i % len(mine)] % P if mine else 0
             runner.step(scores[e], frames, *det[e])

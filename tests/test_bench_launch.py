@@ -79,3 +79,16 @@ def test_lpt_assignment_covers_each_clip_once(world):
     cost = [S.clip_cost_estimate(cfg, c % 8) for c in range(1000)]
     seen = sorted(c for r in range(world) for c in assign_clips(1000, world, r, cost))
     assert seen == list(range(1000))
+
+
+def test_gather_sm_reserve_auto_rule():
+    """bench.py's auto rule for the SMs the gather leaves to the side kernels
+    (DESIGN 6f): u8 1, u8 on 4K grids 16, f32 0; an explicit value wins."""
+    import argparse
+    import bench
+    ns = lambda fmt, k=-1: argparse.Namespace(fmt=fmt, gather_sm_reserve=k)
+    assert bench.gather_sm_reserve(ns("u8"), 34, 60) == 1          # 1080p at 32-px cells
+    assert bench.gather_sm_reserve(ns("u8"), 68, 120) == 16        # 4K
+    assert bench.gather_sm_reserve(ns("f32"), 68, 120) == 0
+    assert bench.gather_sm_reserve(ns("f32", 5), 34, 60) == 5
+    assert bench.gather_sm_reserve(ns("u8", 0), 68, 120) == 0
